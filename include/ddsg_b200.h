@@ -1,0 +1,190 @@
+/*
+ * ddsg_b200.h — C-ABI of the B200-native DDSG evaluation path.
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2202.06555 (batched
+ * evaluation of piecewise-linear hierarchical sparse-grid interpolants composed
+ * as a cut-HDMR sum).  Every entry point replaces one call of the reference's
+ * header-only C++ API (/root/reference/proj/include/ddsg/, cited below as
+ * file:line); the C++ shim in include/ddsg_b200.hpp re-raises the reference's
+ * exception types on top of the status codes returned here.
+ *
+ * Conventions
+ *  - No entry point throws.  Every function returns a ddsg_status; on failure
+ *    ddsg_last_error() returns a thread-local message.
+ *  - Points are row-major x[n][dim], outputs row-major y[n][m] (replacing the
+ *    reference's vector<vector<double>>, ddsg_eval.hpp:130-139).
+ *  - x / y may be host or device pointers (detected with
+ *    cudaPointerGetAttributes).  Host buffers are copied in pipelined chunks
+ *    (pinned host memory gives full PCIe bandwidth); device buffers are used
+ *    in place.
+ *  - Heap keys follow grid_index.hpp:1-38: a 1-d node (l, i) is packed as
+ *    hk = 2^(l-1) + (i-1)/2, l in [1, 30].
+ *  - Objects are immutable after creation except through ddsg_grid_append
+ *    (refinement), which needs external synchronisation, like the reference
+ *    (SPEC.md:109,270).
+ */
+#ifndef DDSG_B200_H_
+#define DDSG_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. */
+typedef enum {
+  DDSG_OK = 0,
+  DDSG_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  DDSG_DOMAIN_ERROR = 2,     /* std::domain_error (x outside [0,1] or NaN) */
+  DDSG_CUDA_ERROR = 3,
+  DDSG_NCCL_ERROR = 4,
+  DDSG_OUT_OF_MEMORY = 5,
+  DDSG_BUILD_ERROR = 6,      /* ddsg::build_error: evaluator returned non-finite */
+  DDSG_OUT_OF_RANGE = 7      /* std::out_of_range (node lookup) */
+} ddsg_status;
+
+/* basis.hpp:22 BoundaryMode. */
+typedef enum { DDSG_ZERO_BOUNDARY = 0, DDSG_MODIFIED_LINEAR = 1 } ddsg_boundary_mode;
+
+/* sparse_grid.hpp:53 SurplusNorm. */
+typedef enum { DDSG_NORM_INF = 0, DDSG_NORM_L2 = 1 } ddsg_surplus_norm;
+
+/* Evaluation arithmetic.  EXACT reproduces the reference rounding sequence
+ * bit for bit (mul then add per node in canonical order, x b, pairwise slot
+ * sum).  FAST contracts the per-node mul+add into one FMA (same order); it is
+ * within 1e-14 abs + 1e-12 rel of the reference on well-conditioned grids. */
+typedef enum { DDSG_EVAL_EXACT = 0, DDSG_EVAL_FAST = 1 } ddsg_eval_mode;
+
+typedef struct ddsg_grid ddsg_grid_t; /* SparseGridFunction (sparse_grid.hpp:72) */
+typedef struct ddsg_hdmr ddsg_hdmr_t; /* VectorizedDdsg (ddsg_eval.hpp:28) over a DdsgFunction (hdmr.hpp:195) */
+
+/* Thread-local message for the last failing call on this thread. */
+const char* ddsg_last_error(void);
+
+/* Library / device information: number of visible CUDA devices (0 if none). */
+int ddsg_device_count(void);
+
+/* ------------------------------------------------------------------ grids */
+
+/* Replaces SparseGridFunction::from_nodes (sparse_grid.hpp:160-179).
+ * heap_keys: [n_nodes][dim] uint32, surplus: [n_nodes][m] fp64, both in the
+ * caller's (stored) node order, which nodes() reports back.  Evaluation walks
+ * the nodes in canonical order (level sum, heap-key lexicographic).
+ * Errors: INVALID_ARGUMENT on dim/m < 1, key validation failure (level > 30
+ * or malformed), duplicate keys (sparse_grid.hpp:172-175). */
+ddsg_status ddsg_grid_create(int dim, int m, int mode, int max_level, double eps_gamma,
+                             int64_t n_nodes, const uint32_t* heap_keys, const double* surplus,
+                             ddsg_grid_t** out);
+
+/* Batched evaluator used by ddsg_grid_build: writes f(xs[i]) into out[i] for
+ * i < count (xs: [count][dim], out: [count][m]).  A non-zero return value
+ * aborts the build with DDSG_BUILD_ERROR.  Replaces GridEvaluator
+ * (sparse_grid.hpp:70), batched so a caller can vectorise. */
+typedef int (*ddsg_batch_evaluator)(const double* xs, int64_t count, double* out, void* ctx);
+
+/* Replaces SparseGridFunction::build (sparse_grid.hpp:84-108) with
+ * SgBuildOptions{max_level, eps_gamma, mode, norm} (sparse_grid.hpp:61-67):
+ * level-sum sweep, children of significant nodes closed under missing
+ * ancestors and sorted by (level sum, key), residual hierarchization
+ * surplus = f(x) - interpolate(grid so far, x) in insertion order.
+ * A non-finite evaluator output yields DDSG_BUILD_ERROR with the offending
+ * point reported through ddsg_last_build_point. */
+ddsg_status ddsg_grid_build(int dim, int m, int mode, int max_level, double eps_gamma, int norm,
+                            ddsg_batch_evaluator f, void* ctx, ddsg_grid_t** out);
+
+/* Coordinates of the point that made the last build fail on this thread
+ * (build_error::point, sparse_grid.hpp:40-48).  Returns its length. */
+int ddsg_last_build_point(double* out, int capacity);
+
+/* Appends refinement nodes (the only mutation).  Keys must
+ * be new.  Device tables are rebuilt lazily on the next evaluation. */
+ddsg_status ddsg_grid_append(ddsg_grid_t* g, int64_t n_new, const uint32_t* heap_keys,
+                             const double* surplus);
+
+/* Residual hierarchization of new nodes against the current grid on the GPU
+ * (sparse_grid.hpp:264-276,302-315): surplus_out[i] = f_values[i] -
+ * interpolate(g, x(keys[i])).  Does not modify g. */
+ddsg_status ddsg_hierarchize(const ddsg_grid_t* g, int64_t n_new, const uint32_t* heap_keys,
+                             const double* f_values, double* surplus_out);
+
+ddsg_status ddsg_grid_destroy(ddsg_grid_t* g);
+
+/* Accessors (sparse_grid.hpp:74-81). */
+ddsg_status ddsg_grid_info(const ddsg_grid_t* g, int* dim, int* m, int* mode, int* max_level,
+                           double* eps_gamma, int64_t* n_nodes);
+/* Copies nodes in stored order: keys [n][dim], surplus [n][m] (either may be NULL). */
+ddsg_status ddsg_grid_nodes(const ddsg_grid_t* g, uint32_t* heap_keys, double* surplus);
+/* SparseGridFunction::quadrature (sparse_grid.hpp:138-149), host, fixed node order. */
+ddsg_status ddsg_grid_quadrature(const ddsg_grid_t* g, double* out);
+
+/* Replaces SparseGridFunction::interpolate (sparse_grid.hpp:111-128) over a
+ * batch: y[i] = interpolate(x[i]).  *bad_index receives the lowest point index
+ * outside [0,1]^dim (or NaN) and the call returns DDSG_DOMAIN_ERROR, mirroring
+ * detail::for_each_index's lowest-task-id task_error (runtime.hpp:104-137).
+ * stream: a cudaStream_t (NULL = legacy default stream).  Synchronous. */
+ddsg_status ddsg_eval_grid(const ddsg_grid_t* g, const double* x, int64_t n, double* y,
+                           int64_t* bad_index, void* stream);
+
+/* ------------------------------------------------------------------- HDMR */
+
+/* Replaces DdsgFunction::from_parts (hdmr.hpp:307-325) + VectorizedDdsg::compile
+ * (ddsg_eval.hpp:40-74).  Slots must be given in the reference's coeff_b order:
+ * the empty index first, then (order, lexicographic) (component_index.hpp:25-28).
+ *   slot_order[s]   = |u_s|
+ *   slot_dims       = concatenated dims of every slot (strictly increasing per slot)
+ *   b[s]            = integer telescoping coefficient
+ *   grids[s]        = grid of slot s (NULL for the empty index; dim == |u_s|)
+ *   f_anchor        = [m] anchor values
+ * Slots with b == 0 are kept but skipped in evaluation (ddsg_eval.hpp:71-72).
+ * Errors: INVALID_ARGUMENT on a missing empty slot, unsorted slots, a grid of
+ * the wrong dimension or output length, or a family that is not downward
+ * closed (ddsg_eval.hpp:61-70). The grids are copied; the caller keeps ownership. */
+ddsg_status ddsg_hdmr_create(int d, int m, const double* f_anchor, int n_slots,
+                             const int32_t* slot_order, const int32_t* slot_dims, const int32_t* b,
+                             const ddsg_grid_t* const* grids, ddsg_hdmr_t** out);
+
+ddsg_status ddsg_hdmr_destroy(ddsg_hdmr_t* h);
+
+ddsg_status ddsg_hdmr_info(const ddsg_hdmr_t* h, int* d, int* m, int* n_slots, int* n_active,
+                           int64_t* n_nodes);
+
+/* Replaces VectorizedDdsg::evaluate_batch (ddsg_eval.hpp:130-139): y[i] =
+ * sum over active slots (pairwise, ddsg_eval.hpp:154-158) of b_s * interp_s(x[i]|u_s).
+ * Errors as ddsg_eval_grid.  Synchronous. */
+ddsg_status ddsg_eval_hdmr(const ddsg_hdmr_t* h, const double* x, int64_t n, double* y,
+                           int64_t* bad_index, void* stream);
+
+/* VectorizedDdsg::quadrature (ddsg_eval.hpp:143-151), host. */
+ddsg_status ddsg_hdmr_quadrature(const ddsg_hdmr_t* h, double* out);
+
+/* --------------------------------------------------------------- controls */
+
+/* Selects the arithmetic of subsequent evaluations on this object. */
+ddsg_status ddsg_grid_set_eval_mode(ddsg_grid_t* g, int eval_mode);
+ddsg_status ddsg_hdmr_set_eval_mode(ddsg_hdmr_t* h, int eval_mode);
+
+/* Kernel statistics of the last evaluation on this thread: number of kernel
+ * launches issued and the device time (ms) of the evaluation kernels alone,
+ * measured with CUDA events on the launching stream. */
+ddsg_status ddsg_last_eval_stats(int64_t* launches, double* kernel_ms);
+
+/* Support statistics (test / roofline helper, computed on the device):
+ * nnz[i] = number of (slot, node) pairs with w != 0 at x[i]; hash[i] = an
+ * order-sensitive FNV-1a hash of the (slot, stored node index) pairs in
+ * evaluation order.  x, nnz, hash: host or device. */
+ddsg_status ddsg_hdmr_support(const ddsg_hdmr_t* h, const double* x, int64_t n, int64_t* nnz,
+                              uint64_t* hash, void* stream);
+ddsg_status ddsg_grid_support(const ddsg_grid_t* g, const double* x, int64_t n, int64_t* nnz,
+                              uint64_t* hash, void* stream);
+
+/* Seeded uniform points exactly as std::mt19937_64 +
+ * std::uniform_real_distribution<double>(0,1) (libstdc++), point-major, as
+ * the reference's test oracle generates them (proj/tests/oracles.hpp:45-53). */
+void ddsg_uniform_points(uint64_t seed, int64_t n, int dim, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDSG_B200_H_ */

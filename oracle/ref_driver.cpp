@@ -1,0 +1,323 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// C-ABI driver around the UNMODIFIED reference implementation
+// (/root/reference/proj/include/ddsg/*.hpp, #included in place, nothing
+// copied).  Built by oracle/Makefile into oracle/_ref/libddsg_ref.so, it is
+// (1) the pin for the C restatement in oracle/ddsg_oracle.c, (2) the source of
+// the golden fixtures under tests/golden/, and (3) the CPU baseline timed by
+// bench.py (cpu_baseline.kind = "reference").
+//
+// Entry points wrap: SparseGridFunction::{from_nodes, build, interpolate,
+// quadrature} (sparse_grid.hpp:84-179), DdsgFunction::{from_parts,
+// evaluate_naive} (hdmr.hpp:257-325), decompose (hdmr.hpp:364-483),
+// VectorizedDdsg::{compile, evaluate, evaluate_batch, quadrature}
+// (ddsg_eval.hpp:40-151), detail::for_each_index (runtime.hpp:104-137),
+// basis_1d / basis_nd (basis.hpp:67-84) and oracle::uniform_points
+// (proj/tests/oracles.hpp:45-53).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ddsg/basis.hpp"
+#include "ddsg/ddsg_eval.hpp"
+#include "ddsg/hdmr.hpp"
+#include "ddsg/runtime.hpp"
+#include "ddsg/sparse_grid.hpp"
+#include "oracles.hpp"
+
+using namespace ddsg;
+
+namespace {
+thread_local std::string g_err;
+thread_local int64_t g_task = -1;
+
+// 0 ok, 1 invalid_argument, 2 domain_error, 6 build_error, 7 out_of_range, 9 other
+template <typename F>
+int guarded(F&& f) {
+  g_task = -1;
+  try {
+    f();
+    return 0;
+  } catch (const task_error& te) {
+    g_task = static_cast<int64_t>(te.task_id());
+    g_err = te.what();
+    try {
+      te.rethrow_cause();
+    } catch (const std::domain_error&) {
+      return 2;
+    } catch (const std::invalid_argument&) {
+      return 1;
+    } catch (...) {
+      return 9;
+    }
+  } catch (const build_error& e) {
+    g_err = e.what();
+    return 6;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 7;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 9;
+  }
+  return 9;
+}
+
+BoundaryMode to_mode(int m) { return m == 1 ? BoundaryMode::modified_linear : BoundaryMode::zero_boundary; }
+
+std::vector<GridNode> make_nodes(int dim, int m, int64_t n, const uint32_t* keys, const double* surplus) {
+  std::vector<GridNode> nodes(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    nodes[i].key.assign(keys + i * dim, keys + (i + 1) * dim);
+    nodes[i].surplus.assign(surplus + i * m, surplus + (i + 1) * m);
+  }
+  return nodes;
+}
+
+using batch_cb = int (*)(const double* xs, int64_t count, double* out, void* ctx);
+
+}  // namespace
+
+struct ref_grid {
+  SparseGridFunction g;
+};
+
+struct ref_hdmr {
+  std::shared_ptr<const DdsgFunction> src;
+  VectorizedDdsg vec;
+};
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+int64_t ref_last_task() { return g_task; }
+
+int ref_basis_1d(int level, uint32_t index, double x, int mode, double* out) {
+  return guarded([&] { *out = basis_1d(level, index, x, to_mode(mode)); });
+}
+
+int ref_heap_key(int level, uint32_t index, uint32_t* out) {
+  return guarded([&] { *out = heap_key(level, index); });
+}
+
+int ref_grid_from_nodes(int dim, int m, int mode, int max_level, double eps, int64_t n, const uint32_t* keys,
+                        const double* surplus, ref_grid** out) {
+  return guarded([&] {
+    auto h = std::make_unique<ref_grid>();
+    h->g = SparseGridFunction::from_nodes(dim, m, max_level, eps, to_mode(mode),
+                                          make_nodes(dim, m, n, keys, surplus));
+    *out = h.release();
+  });
+}
+
+int ref_grid_build(int dim, int m, int mode, int max_level, double eps, int norm, unsigned workers, batch_cb f,
+                   void* ctx, ref_grid** out) {
+  return guarded([&] {
+    SgBuildOptions opt;
+    opt.max_level = max_level;
+    opt.eps_gamma = eps;
+    opt.mode = to_mode(mode);
+    opt.norm = norm == 1 ? SurplusNorm::l2 : SurplusNorm::inf;
+    opt.workers = workers;
+    GridEvaluator ev = [f, ctx](std::span<const double> x, std::span<double> o) {
+      if (f(x.data(), 1, o.data(), ctx) != 0) throw std::runtime_error("evaluator callback failed");
+    };
+    auto h = std::make_unique<ref_grid>();
+    h->g = SparseGridFunction::build(ev, dim, m, opt);
+    *out = h.release();
+  });
+}
+
+void ref_grid_free(ref_grid* g) { delete g; }
+int64_t ref_grid_size(const ref_grid* g) { return static_cast<int64_t>(g->g.size()); }
+
+void ref_grid_nodes(const ref_grid* g, uint32_t* keys, double* surplus) {
+  const int dim = g->g.dim(), m = g->g.out_dim();
+  int64_t i = 0;
+  for (const auto& node : g->g.nodes()) {
+    if (keys) std::copy(node.key.begin(), node.key.end(), keys + i * dim);
+    if (surplus) std::copy(node.surplus.begin(), node.surplus.end(), surplus + i * m);
+    ++i;
+  }
+}
+
+int ref_grid_quadrature(const ref_grid* g, double* out) {
+  return guarded([&] {
+    const auto q = g->g.quadrature();
+    std::copy(q.begin(), q.end(), out);
+  });
+}
+
+// detail::for_each_index over SparseGridFunction::interpolate (the plain-grid
+// CPU baseline of SURVEY.md §8(d)).  x: [n][dim], y: [n][m].
+int ref_grid_eval(const ref_grid* g, const double* x, int64_t n, double* y, unsigned workers) {
+  return guarded([&] {
+    const int dim = g->g.dim(), m = g->g.out_dim();
+    detail::for_each_index(static_cast<size_t>(n), workers, [&](size_t i) {
+      g->g.interpolate(std::span<const double>(x + i * dim, dim), std::span<double>(y + i * m, m));
+    });
+  });
+}
+
+// DdsgFunction::from_parts + VectorizedDdsg::compile.  Slots in coeff_b order
+// (empty index first); grids[s] is null for the empty slot.
+int ref_hdmr_from_parts(int d, int m, const double* f_anchor, int n_slots, const int32_t* slot_order,
+                        const int32_t* slot_dims, const int32_t* b, ref_grid* const* grids, ref_hdmr** out) {
+  return guarded([&] {
+    AnchorPoint anchor;
+    anchor.coords.assign(d, 0.5);
+    anchor.f_anchor.assign(f_anchor, f_anchor + m);
+    std::map<ComponentIndex, SparseGridFunction> accepted;
+    std::map<ComponentIndex, int> coeff;
+    std::map<ComponentIndex, std::vector<double>> quads;
+    int64_t off = 0;
+    for (int s = 0; s < n_slots; ++s) {
+      ComponentIndex u;
+      u.dims.assign(slot_dims + off, slot_dims + off + slot_order[s]);
+      off += slot_order[s];
+      coeff[u] = b[s];
+      if (u.empty()) {
+        quads[u] = anchor.f_anchor;
+      } else {
+        accepted[u] = grids[s]->g;
+        quads[u] = grids[s]->g.quadrature();
+      }
+    }
+    DdsgOptions opt;
+    auto src = std::make_shared<const DdsgFunction>(DdsgFunction::from_parts(
+        d, m, opt, anchor, std::move(accepted), {}, std::move(coeff), std::move(quads)));
+    auto h = std::make_unique<ref_hdmr>();
+    h->vec = VectorizedDdsg::compile(src);
+    h->src = std::move(src);
+    *out = h.release();
+  });
+}
+
+void ref_hdmr_free(ref_hdmr* h) { delete h; }
+
+// VectorizedDdsg::evaluate_batch (ddsg_eval.hpp:130-139).
+int ref_hdmr_eval(const ref_hdmr* h, const double* x, int64_t n, double* y, unsigned workers) {
+  return guarded([&] {
+    const int d = h->vec.dim(), m = h->vec.out_dim();
+    std::vector<std::vector<double>> xs(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) xs[i].assign(x + i * d, x + (i + 1) * d);
+    const auto ys = h->vec.evaluate_batch(xs, workers);
+    for (int64_t i = 0; i < n; ++i) std::copy(ys[i].begin(), ys[i].end(), y + i * m);
+  });
+}
+
+// Same, but without the vector-of-vectors marshalling (for timing the kernel
+// the reference runs, with its thread_local workspace).
+int ref_hdmr_eval_flat(const ref_hdmr* h, const double* x, int64_t n, double* y, unsigned workers) {
+  return guarded([&] {
+    const int d = h->vec.dim(), m = h->vec.out_dim();
+    detail::for_each_index(static_cast<size_t>(n), workers, [&](size_t i) {
+      thread_local EvalWorkspace ws;
+      h->vec.evaluate(std::span<const double>(x + i * d, d), std::span<double>(y + i * m, m), ws);
+    });
+  });
+}
+
+// VectorizedDdsg::evaluate with the interpolation-call counter.
+int ref_hdmr_eval_one(const ref_hdmr* h, const double* x, double* y, uint64_t* calls) {
+  return guarded([&] {
+    const int d = h->vec.dim(), m = h->vec.out_dim();
+    *calls = 0;
+    h->vec.evaluate(std::span<const double>(x, d), std::span<double>(y, m), calls);
+  });
+}
+
+// DdsgFunction::evaluate_naive (hdmr.hpp:257-270).
+int ref_hdmr_eval_naive(const ref_hdmr* h, const double* x, int64_t n, double* y) {
+  return guarded([&] {
+    const int d = h->vec.dim(), m = h->vec.out_dim();
+    for (int64_t i = 0; i < n; ++i)
+      h->src->evaluate_naive(std::span<const double>(x + i * d, d), std::span<double>(y + i * m, m));
+  });
+}
+
+int ref_hdmr_quadrature(const ref_hdmr* h, double* out) {
+  return guarded([&] {
+    const auto q = h->vec.quadrature();
+    std::copy(q.begin(), q.end(), out);
+  });
+}
+
+// decompose (hdmr.hpp:364-483) with a center anchor; the result is exported
+// as parts (slots in coeff_b order + one ref_grid per accepted slot).
+struct ref_decomp {
+  std::shared_ptr<const DdsgFunction> src;
+  std::vector<ComponentIndex> slots;
+  std::vector<int> b;
+};
+
+int ref_decompose(int d, int m, int k_max, double eps_rho, double eps_eta, int max_level, double eps_gamma,
+                  int mode, unsigned workers, batch_cb f, void* ctx, ref_decomp** out) {
+  return guarded([&] {
+    Evaluator ev = [f, ctx](std::span<const double> x, std::span<double> o) {
+      if (f(x.data(), 1, o.data(), ctx) != 0) throw std::runtime_error("evaluator callback failed");
+    };
+    AnchorPoint a;
+    a.coords.assign(d, 0.5);
+    a.f_anchor.resize(m);
+    ev(a.coords, a.f_anchor);
+    DdsgOptions opt;
+    opt.k_max = k_max;
+    opt.eps_rho = eps_rho;
+    opt.eps_eta = eps_eta;
+    opt.max_level = max_level;
+    opt.eps_gamma = eps_gamma;
+    opt.mode = to_mode(mode);
+    opt.workers = workers;
+    auto h = std::make_unique<ref_decomp>();
+    h->src = std::make_shared<const DdsgFunction>(decompose(ev, d, m, a, opt));
+    for (const auto& [u, b] : h->src->coeff_b()) {
+      h->slots.push_back(u);
+      h->b.push_back(b);
+    }
+    *out = h.release();
+  });
+}
+
+void ref_decomp_free(ref_decomp* h) { delete h; }
+int ref_decomp_n_slots(const ref_decomp* h) { return static_cast<int>(h->slots.size()); }
+
+// slot s: order, dims (<= capacity), b; returns a new ref_grid handle for
+// non-empty slots (caller frees) or null.
+ref_grid* ref_decomp_slot(const ref_decomp* h, int s, int32_t* order, int32_t* dims, int32_t* b) {
+  const auto& u = h->slots[s];
+  *order = static_cast<int32_t>(u.order());
+  for (size_t j = 0; j < u.order(); ++j) dims[j] = u.dims[j];
+  *b = h->b[s];
+  if (u.empty()) return nullptr;
+  auto g = std::make_unique<ref_grid>();
+  g->g = h->src->accepted().at(u);
+  return g.release();
+}
+
+void ref_decomp_anchor(const ref_decomp* h, double* f_anchor) {
+  const auto& fa = h->src->anchor().f_anchor;
+  std::copy(fa.begin(), fa.end(), f_anchor);
+}
+
+// oracle::uniform_points (proj/tests/oracles.hpp:45-53), point-major.
+void ref_uniform_points(int dim, int64_t count, uint64_t seed, double* out) {
+  const auto pts = oracle::uniform_points(dim, static_cast<size_t>(count), seed);
+  for (int64_t i = 0; i < count; ++i) std::copy(pts[i].begin(), pts[i].end(), out + i * dim);
+}
+
+// oracle::sg_node_count_bruteforce (oracles.hpp:21-43) and sg_node_count (hdmr.hpp:134-151).
+uint64_t ref_sg_node_count_bruteforce(int n, int L) { return oracle::sg_node_count_bruteforce(n, L); }
+
+unsigned ref_default_workers() { return default_worker_count(); }
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+"""ctypes binding of the C-ABI declared in include/ddsg_b200.h.
+
+There is no fallback: if libddsg_b200.so is missing the import fails loudly
+(build it with ``python -c "import __graft_entry__ as g; g.build()"``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libddsg_b200.so"
+WL_PATH = _PKG / "libddsg_workloads.so"
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"{LIB_PATH} is missing: the DDSG CUDA library has not been built "
+        "(run __graft_entry__.build()); there is no CPU fallback"
+    )
+
+lib = C.CDLL(str(LIB_PATH))
+
+# status codes
+OK, INVALID_ARGUMENT, DOMAIN_ERROR, CUDA_ERROR, NCCL_ERROR, OUT_OF_MEMORY, BUILD_ERROR, OUT_OF_RANGE = range(8)
+ZERO_BOUNDARY, MODIFIED_LINEAR = 0, 1
+NORM_INF, NORM_L2 = 0, 1
+EVAL_EXACT, EVAL_FAST = 0, 1
+
+BATCH_EVALUATOR = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)
+
+_p = C.c_void_p
+_i = C.c_int
+_i64 = C.c_int64
+_d = C.c_double
+_pd = C.c_void_p  # raw pointers (host numpy or device)
+
+# name: (restype, argtypes) — mirrors include/ddsg_b200.h one to one
+SIGNATURES = {
+    "ddsg_last_error": (C.c_char_p, []),
+    "ddsg_device_count": (_i, []),
+    "ddsg_grid_create": (_i, [_i, _i, _i, _i, _d, _i64, _p, _p, C.POINTER(_p)]),
+    "ddsg_grid_build": (_i, [_i, _i, _i, _i, _d, _i, _p, _p, C.POINTER(_p)]),
+    "ddsg_last_build_point": (_i, [_p, _i]),
+    "ddsg_grid_append": (_i, [_p, _i64, _p, _p]),
+    "ddsg_hierarchize": (_i, [_p, _i64, _p, _p, _p]),
+    "ddsg_grid_destroy": (_i, [_p]),
+    "ddsg_grid_info": (_i, [_p, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_d), C.POINTER(_i64)]),
+    "ddsg_grid_nodes": (_i, [_p, _p, _p]),
+    "ddsg_grid_quadrature": (_i, [_p, _p]),
+    "ddsg_eval_grid": (_i, [_p, _pd, _i64, _pd, C.POINTER(_i64), _p]),
+    "ddsg_hdmr_create": (_i, [_i, _i, _p, _i, _p, _p, _p, _p, C.POINTER(_p)]),
+    "ddsg_hdmr_destroy": (_i, [_p]),
+    "ddsg_hdmr_info": (_i, [_p, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i64)]),
+    "ddsg_eval_hdmr": (_i, [_p, _pd, _i64, _pd, C.POINTER(_i64), _p]),
+    "ddsg_hdmr_quadrature": (_i, [_p, _p]),
+    "ddsg_grid_set_eval_mode": (_i, [_p, _i]),
+    "ddsg_hdmr_set_eval_mode": (_i, [_p, _i]),
+    "ddsg_last_eval_stats": (_i, [C.POINTER(_i64), C.POINTER(_d)]),
+    "ddsg_hdmr_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
+    "ddsg_grid_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
+    "ddsg_uniform_points": (None, [C.c_uint64, _i64, _i, _p]),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def last_error() -> str:
+    return lib.ddsg_last_error().decode()
+
+
+_wl = None
+
+
+def workloads():
+    """The synthetic-workload library (target functions of the configs)."""
+    global _wl
+    if _wl is None:
+        if not WL_PATH.exists():
+            raise ImportError(f"{WL_PATH} is missing (run __graft_entry__.build())")
+        _wl = C.CDLL(str(WL_PATH))
+        _wl.wl_cut_new.restype = C.c_void_p
+        _wl.wl_cut_new.argtypes = [C.c_void_p, C.c_void_p, _i, _i, _i, _p, _p]
+        _wl.wl_cut_free.argtypes = [C.c_void_p]
+        _wl.wl_config_pairs.restype = _i
+        _wl.wl_config_pairs.argtypes = [_i, _p]
+    return _wl
+
+
+def wl_fn(name: str) -> int:
+    """Address of a C target function in the workloads library."""
+    return C.cast(getattr(workloads(), name), C.c_void_p).value

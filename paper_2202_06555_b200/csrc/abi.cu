@@ -1,0 +1,450 @@
+// C-ABI (include/ddsg_b200.h): handles, validation, error translation.
+//
+// Every entry point catches all exceptions and returns a ddsg_status; the
+// message goes to a thread-local buffer (ddsg_last_error).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/ddsg_b200.h"
+#include "device.cuh"
+#include "grid_host.hpp"
+#include "program.hpp"
+
+using namespace ddsg_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local std::vector<double> g_last_build_point;
+
+ddsg_status set_error(ddsg_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+template <typename F>
+ddsg_status guarded(F&& f) {
+  try {
+    f();
+    return DDSG_OK;
+  } catch (const BuildError& e) {
+    g_last_build_point = e.point;
+    return set_error(e.status, e.what());
+  } catch (const Error& e) {
+    return set_error(e.status, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_error(DDSG_OUT_OF_MEMORY, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_error(DDSG_INVALID_ARGUMENT, e.what());
+  } catch (...) {
+    return set_error(DDSG_INVALID_ARGUMENT, "unknown error");
+  }
+}
+
+int current_device() {
+  int dev = 0;
+  DDSG_CUDA(cudaGetDevice(&dev));
+  return dev;
+}
+
+// Device copies of a program, one per CUDA device that evaluated it.
+struct DeviceCache {
+  std::mutex mu;
+  std::map<int, std::unique_ptr<DeviceProgram>> per_device;
+  const DeviceProgram& get(const HostProgram& hp) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(mu);
+    auto& slot = per_device[dev];
+    if (!slot) {
+      auto p = std::make_unique<DeviceProgram>();
+      p->upload(hp);
+      slot = std::move(p);
+    }
+    return *slot;
+  }
+  void invalidate() {
+    std::lock_guard<std::mutex> lock(mu);
+    per_device.clear();
+  }
+};
+
+}  // namespace
+
+struct ddsg_grid {
+  HostGrid g;
+  int eval_mode = DDSG_EVAL_EXACT;
+  std::mutex prog_mu;
+  std::unique_ptr<HostProgram> prog;
+  DeviceCache dev;
+
+  const HostProgram& program() {
+    std::lock_guard<std::mutex> lock(prog_mu);
+    if (!prog) {
+      auto hp = std::make_unique<HostProgram>();
+      hp->d = g.dim;
+      hp->m = g.m;
+      hp->plain = 1;
+      hp->f_anchor.assign(g.m, 0.0);
+      std::vector<int32_t> dims(g.dim);
+      for (int j = 0; j < g.dim; ++j) dims[j] = j;
+      hp->add_grid_slot(0, g, dims, 1.0);
+      hp->finish();
+      prog = std::move(hp);
+    }
+    return *prog;
+  }
+  void invalidate() {
+    std::lock_guard<std::mutex> lock(prog_mu);
+    prog.reset();
+    dev.invalidate();
+  }
+};
+
+struct ddsg_hdmr {
+  int d = 0, m = 0;
+  std::vector<double> f_anchor;
+  struct Slot {
+    std::vector<int32_t> dims;
+    int32_t b = 0;
+    int grid = -1;  // index into grids
+  };
+  std::vector<Slot> slots;
+  std::vector<HostGrid> grids;
+  HostProgram prog;
+  int eval_mode = DDSG_EVAL_EXACT;
+  DeviceCache dev;
+};
+
+extern "C" {
+
+const char* ddsg_last_error(void) { return g_last_error.c_str(); }
+
+int ddsg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+ddsg_status ddsg_grid_create(int dim, int m, int mode, int max_level, double eps_gamma, int64_t n_nodes,
+                             const uint32_t* heap_keys, const double* surplus, ddsg_grid_t** out) {
+  return guarded([&] {
+    if (!out) fail(DDSG_INVALID_ARGUMENT, "grid_create: null output handle");
+    auto h = std::make_unique<ddsg_grid>();
+    h->g = HostGrid::from_nodes(dim, m, mode, max_level, eps_gamma, n_nodes, heap_keys, surplus);
+    *out = h.release();
+  });
+}
+
+ddsg_status ddsg_grid_build(int dim, int m, int mode, int max_level, double eps_gamma, int norm,
+                            ddsg_batch_evaluator f, void* ctx, ddsg_grid_t** out) {
+  g_last_build_point.clear();
+  return guarded([&] {
+    if (!out) fail(DDSG_INVALID_ARGUMENT, "grid_build: null output handle");
+    if (!f) fail(DDSG_INVALID_ARGUMENT, "grid_build: null evaluator");
+    if (norm != DDSG_NORM_INF && norm != DDSG_NORM_L2)
+      fail(DDSG_INVALID_ARGUMENT, "grid_build: unknown surplus norm");
+    auto h = std::make_unique<ddsg_grid>();
+    h->g = HostGrid::build(dim, m, mode, max_level, eps_gamma, norm,
+                           [&](const double* xs, int64_t count, double* o) {
+                             if (f(xs, count, o, ctx) != 0) {
+                               throw BuildError("sparse grid: evaluator failed",
+                                                std::vector<double>(xs, xs + dim));
+                             }
+                           });
+    *out = h.release();
+  });
+}
+
+int ddsg_last_build_point(double* out, int capacity) {
+  const int n = static_cast<int>(g_last_build_point.size());
+  for (int i = 0; i < std::min(n, capacity); ++i) out[i] = g_last_build_point[i];
+  return n;
+}
+
+ddsg_status ddsg_grid_append(ddsg_grid_t* g, int64_t n_new, const uint32_t* heap_keys, const double* surplus) {
+  return guarded([&] {
+    if (!g) fail(DDSG_INVALID_ARGUMENT, "grid_append: null grid");
+    g->g.append(n_new, heap_keys, surplus);
+    g->invalidate();
+  });
+}
+
+ddsg_status ddsg_hierarchize(const ddsg_grid_t* g, int64_t n_new, const uint32_t* heap_keys,
+                             const double* f_values, double* surplus_out) {
+  return guarded([&] {
+    if (!g) fail(DDSG_INVALID_ARGUMENT, "hierarchize: null grid");
+    if (n_new < 0 || (n_new > 0 && (!heap_keys || !f_values || !surplus_out)))
+      fail(DDSG_INVALID_ARGUMENT, "hierarchize: null arrays");
+    const HostGrid& G = g->g;
+    std::vector<double> x(static_cast<size_t>(n_new) * G.dim);
+    for (int64_t i = 0; i < n_new * G.dim; ++i) {
+      if (!valid_key(heap_keys[i])) fail(DDSG_INVALID_ARGUMENT, "hierarchize: invalid heap key");
+      x[i] = coordinate_of(heap_keys[i]);
+    }
+    std::vector<double> interp(static_cast<size_t>(n_new) * G.m);
+    auto* self = const_cast<ddsg_grid_t*>(g);
+    const DeviceProgram& prog = self->dev.get(self->program());
+    const int64_t bad = evaluate(prog, 1, x.data(), n_new, interp.data(), nullptr);
+    if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "hierarchize: node outside the unit cube");
+    for (int64_t i = 0; i < n_new * G.m; ++i) surplus_out[i] = f_values[i] - interp[i];
+  });
+}
+
+ddsg_status ddsg_grid_destroy(ddsg_grid_t* g) {
+  return guarded([&] { delete g; });
+}
+
+ddsg_status ddsg_grid_info(const ddsg_grid_t* g, int* dim, int* m, int* mode, int* max_level,
+                           double* eps_gamma, int64_t* n_nodes) {
+  return guarded([&] {
+    if (!g) fail(DDSG_INVALID_ARGUMENT, "grid_info: null grid");
+    if (dim) *dim = g->g.dim;
+    if (m) *m = g->g.m;
+    if (mode) *mode = g->g.mode;
+    if (max_level) *max_level = g->g.max_level;
+    if (eps_gamma) *eps_gamma = g->g.eps_gamma;
+    if (n_nodes) *n_nodes = g->g.size();
+  });
+}
+
+ddsg_status ddsg_grid_nodes(const ddsg_grid_t* g, uint32_t* heap_keys, double* surplus) {
+  return guarded([&] {
+    if (!g) fail(DDSG_INVALID_ARGUMENT, "grid_nodes: null grid");
+    if (heap_keys) std::copy(g->g.keys.begin(), g->g.keys.end(), heap_keys);
+    if (surplus) std::copy(g->g.surplus.begin(), g->g.surplus.end(), surplus);
+  });
+}
+
+ddsg_status ddsg_grid_quadrature(const ddsg_grid_t* g, double* out) {
+  return guarded([&] {
+    if (!g || !out) fail(DDSG_INVALID_ARGUMENT, "grid_quadrature: null argument");
+    const auto q = g->g.quadrature();
+    std::copy(q.begin(), q.end(), out);
+  });
+}
+
+ddsg_status ddsg_eval_grid(const ddsg_grid_t* g, const double* x, int64_t n, double* y, int64_t* bad_index,
+                           void* stream) {
+  if (bad_index) *bad_index = -1;
+  return guarded([&] {
+    if (!g) fail(DDSG_INVALID_ARGUMENT, "eval_grid: null grid");
+    if (n < 0) fail(DDSG_INVALID_ARGUMENT, "eval_grid: negative point count");
+    if (n > 0 && (!x || !y)) fail(DDSG_INVALID_ARGUMENT, "eval_grid: null buffers");
+    auto* self = const_cast<ddsg_grid_t*>(g);
+    const DeviceProgram& prog = self->dev.get(self->program());
+    const int64_t bad = evaluate(prog, g->eval_mode == DDSG_EVAL_EXACT, x, n, y,
+                                 static_cast<cudaStream_t>(stream));
+    if (bad >= 0) {
+      if (bad_index) *bad_index = bad;
+      fail(DDSG_DOMAIN_ERROR, "task " + std::to_string(bad) +
+                                  " failed: sparse grid: query outside the unit cube");
+    }
+  });
+}
+
+ddsg_status ddsg_grid_support(const ddsg_grid_t* g, const double* x, int64_t n, int64_t* nnz, uint64_t* hash,
+                              void* stream) {
+  return guarded([&] {
+    if (!g) fail(DDSG_INVALID_ARGUMENT, "grid_support: null grid");
+    if (n > 0 && (!x || !nnz || !hash)) fail(DDSG_INVALID_ARGUMENT, "grid_support: null buffers");
+    auto* self = const_cast<ddsg_grid_t*>(g);
+    const DeviceProgram& prog = self->dev.get(self->program());
+    const int64_t bad = support(prog, x, n, nnz, hash, static_cast<cudaStream_t>(stream));
+    if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "grid_support: query outside the unit cube");
+  });
+}
+
+ddsg_status ddsg_grid_set_eval_mode(ddsg_grid_t* g, int eval_mode) {
+  return guarded([&] {
+    if (!g) fail(DDSG_INVALID_ARGUMENT, "set_eval_mode: null grid");
+    if (eval_mode != DDSG_EVAL_EXACT && eval_mode != DDSG_EVAL_FAST)
+      fail(DDSG_INVALID_ARGUMENT, "set_eval_mode: unknown mode");
+    g->eval_mode = eval_mode;
+  });
+}
+
+// ------------------------------------------------------------------ HDMR
+
+ddsg_status ddsg_hdmr_create(int d, int m, const double* f_anchor, int n_slots, const int32_t* slot_order,
+                             const int32_t* slot_dims, const int32_t* b, const ddsg_grid_t* const* grids,
+                             ddsg_hdmr_t** out) {
+  return guarded([&] {
+    if (!out) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: null output handle");
+    if (d < 1 || m < 1) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: d and m must be >= 1");
+    if (n_slots < 1 || !slot_order || !b || !f_anchor)
+      fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: inconsistent accepted family");
+    auto h = std::make_unique<ddsg_hdmr>();
+    h->d = d;
+    h->m = m;
+    h->f_anchor.assign(f_anchor, f_anchor + m);
+    int64_t dim_off = 0;
+    std::set<std::vector<int32_t>> accepted;
+    for (int s = 0; s < n_slots; ++s) {
+      const int k = slot_order[s];
+      if (k < 0 || k > d) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: slot order out of range");
+      ddsg_hdmr::Slot slot;
+      slot.dims.assign(slot_dims ? slot_dims + dim_off : nullptr, slot_dims ? slot_dims + dim_off + k : nullptr);
+      if (k > 0 && !slot_dims) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: null slot dims");
+      dim_off += k;
+      for (int j = 0; j < k; ++j) {
+        if (slot.dims[j] < 0 || slot.dims[j] >= d)
+          fail(DDSG_INVALID_ARGUMENT, "component index: dimension id out of range");
+        if (j > 0 && slot.dims[j] <= slot.dims[j - 1])
+          fail(DDSG_INVALID_ARGUMENT, "component index: dims must be strictly increasing");
+      }
+      slot.b = b[s];
+      if (s == 0 && k != 0) fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: inconsistent accepted family");
+      if (s > 0) {
+        // (order, lexicographic) ordering, strictly increasing (component_index.hpp:25-28)
+        const auto& prev = h->slots.back().dims;
+        const bool less = prev.size() != slot.dims.size() ? prev.size() < slot.dims.size() : prev < slot.dims;
+        if (!less) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: slots must be sorted by (order, lex) without duplicates");
+      }
+      if (k > 0) {
+        if (!grids || !grids[s])
+          fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: coefficient for a non-accepted index");
+        const HostGrid& G = grids[s]->g;
+        if (G.dim != k) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: grid dimension != slot order");
+        if (G.m != m) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: grid output length != m");
+        slot.grid = static_cast<int>(h->grids.size());
+        h->grids.push_back(G);
+        accepted.insert(slot.dims);
+      }
+      h->slots.push_back(std::move(slot));
+    }
+    // closure: every non-empty proper subset of an accepted index is accepted (ddsg_eval.hpp:63-70)
+    for (const auto& u : accepted) {
+      const size_t k = u.size();
+      for (size_t mask = 1; mask + 1 < (size_t{1} << k); ++mask) {
+        std::vector<int32_t> sub;
+        for (size_t j = 0; j < k; ++j)
+          if (mask & (size_t{1} << j)) sub.push_back(u[j]);
+        if (!accepted.count(sub)) {
+          auto str = [](const std::vector<int32_t>& v) {
+            std::string s = "{";
+            for (size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+            return s + "}";
+          };
+          fail(DDSG_INVALID_ARGUMENT,
+               "vectorized ddsg: accepted family misses subset " + str(sub) + " of " + str(u));
+        }
+      }
+    }
+    HostProgram& hp = h->prog;
+    hp.d = d;
+    hp.m = m;
+    hp.plain = 0;
+    hp.f_anchor = h->f_anchor;
+    for (int s = 0; s < n_slots; ++s) {
+      const auto& slot = h->slots[s];
+      if (slot.b == 0) continue;
+      if (slot.dims.empty())
+        hp.add_empty_slot(s, static_cast<double>(slot.b));
+      else
+        hp.add_grid_slot(s, h->grids[slot.grid], slot.dims, static_cast<double>(slot.b));
+    }
+    hp.finish();
+    *out = h.release();
+  });
+}
+
+ddsg_status ddsg_hdmr_destroy(ddsg_hdmr_t* h) {
+  return guarded([&] { delete h; });
+}
+
+ddsg_status ddsg_hdmr_info(const ddsg_hdmr_t* h, int* d, int* m, int* n_slots, int* n_active, int64_t* n_nodes) {
+  return guarded([&] {
+    if (!h) fail(DDSG_INVALID_ARGUMENT, "hdmr_info: null handle");
+    if (d) *d = h->d;
+    if (m) *m = h->m;
+    if (n_slots) *n_slots = static_cast<int>(h->slots.size());
+    if (n_active) *n_active = static_cast<int>(h->prog.slot_k.size());
+    if (n_nodes) {
+      int64_t t = 0;
+      for (const auto& g : h->grids) t += g.size();
+      *n_nodes = t;
+    }
+  });
+}
+
+ddsg_status ddsg_eval_hdmr(const ddsg_hdmr_t* h, const double* x, int64_t n, double* y, int64_t* bad_index,
+                           void* stream) {
+  if (bad_index) *bad_index = -1;
+  return guarded([&] {
+    if (!h) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr: null handle");
+    if (n < 0) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr: negative point count");
+    if (n > 0 && (!x || !y)) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr: null buffers");
+    auto* self = const_cast<ddsg_hdmr_t*>(h);
+    const DeviceProgram& prog = self->dev.get(h->prog);
+    const int64_t bad = evaluate(prog, h->eval_mode == DDSG_EVAL_EXACT, x, n, y,
+                                 static_cast<cudaStream_t>(stream));
+    if (bad >= 0) {
+      if (bad_index) *bad_index = bad;
+      fail(DDSG_DOMAIN_ERROR, "task " + std::to_string(bad) + " failed: ddsg: query outside unit cube");
+    }
+  });
+}
+
+ddsg_status ddsg_hdmr_support(const ddsg_hdmr_t* h, const double* x, int64_t n, int64_t* nnz, uint64_t* hash,
+                              void* stream) {
+  return guarded([&] {
+    if (!h) fail(DDSG_INVALID_ARGUMENT, "hdmr_support: null handle");
+    if (n > 0 && (!x || !nnz || !hash)) fail(DDSG_INVALID_ARGUMENT, "hdmr_support: null buffers");
+    auto* self = const_cast<ddsg_hdmr_t*>(h);
+    const DeviceProgram& prog = self->dev.get(h->prog);
+    const int64_t bad = support(prog, x, n, nnz, hash, static_cast<cudaStream_t>(stream));
+    if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "hdmr_support: query outside unit cube");
+  });
+}
+
+ddsg_status ddsg_hdmr_quadrature(const ddsg_hdmr_t* h, double* out) {
+  return guarded([&] {
+    if (!h || !out) fail(DDSG_INVALID_ARGUMENT, "hdmr_quadrature: null argument");
+    // ddsg_eval.hpp:143-151: sum over slots with b != 0 of b * cut quadrature
+    std::vector<double> q(h->m, 0.0);
+    for (const auto& s : h->slots) {
+      if (s.b == 0) continue;
+      const std::vector<double> qc = s.dims.empty() ? h->f_anchor : h->grids[s.grid].quadrature();
+      for (int c = 0; c < h->m; ++c) q[c] += s.b * qc[c];
+    }
+    std::copy(q.begin(), q.end(), out);
+  });
+}
+
+ddsg_status ddsg_hdmr_set_eval_mode(ddsg_hdmr_t* h, int eval_mode) {
+  return guarded([&] {
+    if (!h) fail(DDSG_INVALID_ARGUMENT, "set_eval_mode: null handle");
+    if (eval_mode != DDSG_EVAL_EXACT && eval_mode != DDSG_EVAL_FAST)
+      fail(DDSG_INVALID_ARGUMENT, "set_eval_mode: unknown mode");
+    h->eval_mode = eval_mode;
+  });
+}
+
+ddsg_status ddsg_last_eval_stats(int64_t* launches, double* kernel_ms) {
+  const EvalStats& s = last_stats();
+  if (launches) *launches = s.launches;
+  if (kernel_ms) *kernel_ms = s.kernel_ms;
+  return DDSG_OK;
+}
+
+void ddsg_uniform_points(uint64_t seed, int64_t n, int dim, double* out) {
+  // std::uniform_real_distribution<double>(0,1) over std::mt19937_64, as
+  // oracles.hpp:45-53 (libstdc++ generate_canonical with one 64-bit draw).
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  for (int64_t i = 0; i < n * dim; ++i) out[i] = unif(rng);
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Device-resident program and the evaluation kernels' parameter block.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "program.hpp"
+
+namespace ddsg_b200 {
+
+#define DDSG_CUDA(call)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      ::ddsg_b200::fail(e_ == cudaErrorMemoryAllocation ? DDSG_OUT_OF_MEMORY : DDSG_CUDA_ERROR, \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+    }                                                                                       \
+  } while (0)
+
+constexpr int kMaxDepth = 32;  // pairwise-sum stack (2^31 active slots)
+constexpr int kMaxSlotDim = 64;
+
+// Plain-old-data view of a DeviceProgram passed by value to kernels.
+struct EvalParams {
+  int d, m, n_active, plain, exact, depth;
+  const int32_t* slot_k;
+  const int32_t* slot_mode;
+  const int32_t* slot_dims_off;
+  const int32_t* slot_dims;
+  const double* slot_b;
+  const int32_t* slot_sub_begin;
+  const int32_t* slot_sub_end;
+  const int32_t* slot_id;
+  const uint8_t* merges;
+  const int32_t* sub_lv_off;
+  const uint8_t* levels;
+  const int64_t* sub_slab_off;
+  const int32_t* slab;
+  const double* surplus;
+  const int32_t* row_stored;
+  const double* f_anchor;
+};
+
+class DeviceProgram {
+ public:
+  DeviceProgram() = default;
+  DeviceProgram(const DeviceProgram&) = delete;
+  DeviceProgram& operator=(const DeviceProgram&) = delete;
+  ~DeviceProgram();
+
+  void upload(const HostProgram& hp);
+  EvalParams params(int exact) const;
+  bool ready() const { return ready_; }
+  const HostProgram& host() const { return hp_; }
+
+ private:
+  HostProgram hp_;
+  std::vector<void*> allocs_;
+  EvalParams p_{};
+  bool ready_ = false;
+  template <typename T>
+  const T* put(const std::vector<T>& v);
+};
+
+// Per-call statistics (thread-local, see ddsg_last_eval_stats).
+struct EvalStats {
+  int64_t launches = 0;
+  double kernel_ms = 0.0;
+};
+EvalStats& last_stats();
+
+// Evaluates the program over n points.  x/y may be host or device memory.
+// Returns the lowest out-of-domain point index or -1.
+int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,
+                 cudaStream_t stream);
+
+// Support statistics (nnz and order-sensitive hash per point).
+int64_t support(const DeviceProgram& prog, const double* x, int64_t n, int64_t* nnz,
+                uint64_t* hash, cudaStream_t stream);
+
+}  // namespace ddsg_b200

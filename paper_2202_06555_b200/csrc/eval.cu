@@ -1,0 +1,402 @@
+// Generic evaluation kernel (any grid dimension, any slot order, any boundary
+// mode) and the host orchestration of an evaluation call.
+//
+// Semantics (bit-exact in EXACT mode):
+//   plain grid:  y[c] = sum over nodes in canonical order with w != 0 of w*s[c]
+//                (sparse_grid.hpp:111-128; canonical order per SURVEY.md §A.3)
+//   HDMR:        row_s[c] = b_s * interp_s(x|u_s)   (ddsg_eval.hpp:91-110)
+//                y[c]     = pairwise_sum_s row_s[c] (ddsg_eval.hpp:111-112,154-158)
+// One thread owns one point and a chunk of kCols output columns; it walks the
+// subspaces of every active slot, computes the candidate cell and the
+// dim-ordered weight product, and accumulates the surplus row with
+// mul-then-add (EXACT) or FMA (FAST).  Partial slot sums live on a
+// per-thread stack driven by the precompiled merge schedule.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <memory>
+
+#include "basis.cuh"
+#include "device.cuh"
+
+namespace ddsg_b200 {
+
+EvalStats& last_stats() {
+  static thread_local EvalStats s;
+  return s;
+}
+
+DeviceProgram::~DeviceProgram() {
+  for (void* p : allocs_) cudaFree(p);
+}
+
+template <typename T>
+const T* DeviceProgram::put(const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  void* p = nullptr;
+  DDSG_CUDA(cudaMalloc(&p, v.size() * sizeof(T)));
+  allocs_.push_back(p);
+  DDSG_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return static_cast<const T*>(p);
+}
+
+void DeviceProgram::upload(const HostProgram& hp) {
+  for (void* p : allocs_) cudaFree(p);
+  allocs_.clear();
+  ready_ = false;
+  hp_ = hp;
+  EvalParams p{};
+  p.d = hp.d;
+  p.m = hp.m;
+  p.n_active = static_cast<int>(hp.slot_k.size());
+  p.plain = hp.plain;
+  p.depth = hp.depth;
+  if (p.depth > kMaxDepth) fail(DDSG_INVALID_ARGUMENT, "program: slot tree too deep");
+  p.slot_k = put(hp.slot_k);
+  p.slot_mode = put(hp.slot_mode);
+  p.slot_dims_off = put(hp.slot_dims_off);
+  p.slot_dims = put(hp.slot_dims);
+  p.slot_b = put(hp.slot_b);
+  p.slot_sub_begin = put(hp.slot_sub_begin);
+  p.slot_sub_end = put(hp.slot_sub_end);
+  p.slot_id = put(hp.slot_id);
+  p.merges = put(hp.merges);
+  p.sub_lv_off = put(hp.sub_lv_off);
+  p.levels = put(hp.levels);
+  p.sub_slab_off = put(hp.sub_slab_off);
+  p.slab = put(hp.slab);
+  p.surplus = put(hp.surplus);
+  p.row_stored = put(hp.row_stored);
+  p.f_anchor = put(hp.f_anchor);
+  p_ = p;
+  ready_ = true;
+}
+
+EvalParams DeviceProgram::params(int exact) const {
+  EvalParams p = p_;
+  p.exact = exact;
+  return p;
+}
+
+// ---------------------------------------------------------------- kernels
+
+__device__ __forceinline__ double accum(double acc, double w, double s, int exact) {
+  return exact ? __dadd_rn(acc, __dmul_rn(w, s)) : __fma_rn(w, s, acc);
+}
+
+// Validates x[p] (check_query / check_point: !(0 <= v <= 1) also catches NaN).
+__device__ __forceinline__ bool point_ok(const double* xp, int d) {
+  bool ok = true;
+  for (int j = 0; j < d; ++j) {
+    const double v = xp[j];
+    ok &= (v >= 0.0 && v <= 1.0);
+  }
+  return ok;
+}
+
+template <int kCols>
+__global__ void __launch_bounds__(128) eval_generic_kernel(EvalParams P, const double* __restrict__ x,
+                                                           int64_t n, int64_t base, double* __restrict__ y,
+                                                           unsigned long long* bad) {
+  const int chunks = (P.m + kCols - 1) / kCols;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p = tid / chunks;
+  const int ch = static_cast<int>(tid % chunks);
+  if (p >= n) return;
+  const double* xp = x + p * P.d;
+  if (!point_ok(xp, P.d)) {
+    if (ch == 0) atomicMin(bad, static_cast<unsigned long long>(base + p));
+    return;
+  }
+  const int c0 = ch * kCols;
+  const int nc = min(kCols, P.m - c0);
+  double stack[kMaxDepth][kCols];
+  int sp = 0;
+  double acc[kCols];
+  for (int a = 0; a < P.n_active; ++a) {
+    const int k = P.slot_k[a];
+    const double b = P.slot_b[a];
+    if (k == 0) {
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) acc[c] = c < nc ? __dmul_rn(b, P.f_anchor[c0 + c]) : 0.0;
+    } else {
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+      const int32_t* dims = P.slot_dims + P.slot_dims_off[a];
+      const int mode = P.slot_mode[a];
+      const int s_end = P.slot_sub_end[a];
+      for (int s = P.slot_sub_begin[a]; s < s_end; ++s) {
+        const uint8_t* lv = P.levels + P.sub_lv_off[s];
+        double w = 1.0;
+        int64_t lin = 0;
+        for (int j = 0; j < k; ++j) {
+          const int l = lv[j];
+          const double xv = xp[dims[j]];
+          const uint32_t kk = cell_at(xv, l);
+          w = __dmul_rn(w, basis_at(mode, l, kk, xv));
+          lin = (lin << (l - 1)) | kk;
+          if (w == 0.0) break;
+        }
+        if (w == 0.0) continue;
+        const int32_t row = P.slab[P.sub_slab_off[s] + lin];
+        if (row < 0) continue;
+        const double* sr = P.surplus + static_cast<int64_t>(row) * P.m + c0;
+#pragma unroll
+        for (int c = 0; c < kCols; ++c)
+          if (c < nc) acc[c] = accum(acc[c], w, sr[c], P.exact);
+      }
+      if (!P.plain) {
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) acc[c] = __dmul_rn(acc[c], b);
+      }
+    }
+    if (P.plain) break;
+    // push, then fold merges[a] times: top = below + top (ddsg_eval.hpp:157)
+    int mg = P.merges[a];
+    while (mg-- > 0) {
+      --sp;
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) acc[c] = __dadd_rn(stack[sp][c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) stack[sp][c] = acc[c];
+    ++sp;
+  }
+  double* yp = y + p * P.m + c0;
+  if (P.plain) {
+    for (int c = 0; c < nc; ++c) yp[c] = acc[c];
+  } else if (P.n_active == 0) {
+    for (int c = 0; c < nc; ++c) yp[c] = 0.0;
+  } else {
+    for (int c = 0; c < nc; ++c) yp[c] = stack[0][c];
+  }
+}
+
+// Support statistics: nnz and an order-sensitive FNV-1a hash over
+// (slot id, stored node index) of every term with w != 0, in evaluation order.
+__global__ void support_kernel(EvalParams P, const double* __restrict__ x, int64_t n, int64_t base,
+                               int64_t* nnz_out, unsigned long long* hash_out,
+                               unsigned long long* bad) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double* xp = x + p * P.d;
+  if (!point_ok(xp, P.d)) {
+    atomicMin(bad, static_cast<unsigned long long>(base + p));
+    return;
+  }
+  int64_t nnz = 0;
+  unsigned long long h = 0xcbf29ce484222325ull;
+  for (int a = 0; a < P.n_active; ++a) {
+    const int k = P.slot_k[a];
+    if (k == 0) continue;
+    const int32_t* dims = P.slot_dims + P.slot_dims_off[a];
+    const int mode = P.slot_mode[a];
+    for (int s = P.slot_sub_begin[a]; s < P.slot_sub_end[a]; ++s) {
+      const uint8_t* lv = P.levels + P.sub_lv_off[s];
+      double w = 1.0;
+      int64_t lin = 0;
+      for (int j = 0; j < k; ++j) {
+        const int l = lv[j];
+        const double xv = xp[dims[j]];
+        const uint32_t kk = cell_at(xv, l);
+        w = __dmul_rn(w, basis_at(mode, l, kk, xv));
+        lin = (lin << (l - 1)) | kk;
+        if (w == 0.0) break;
+      }
+      if (w == 0.0) continue;
+      const int32_t row = P.slab[P.sub_slab_off[s] + lin];
+      if (row < 0) continue;
+      ++nnz;
+      const unsigned long long key =
+          (static_cast<unsigned long long>(static_cast<uint32_t>(P.slot_id[a])) << 32) |
+          static_cast<uint32_t>(P.row_stored[row]);
+      for (int byte = 0; byte < 8; ++byte) {
+        h ^= (key >> (8 * byte)) & 0xffull;
+        h *= 0x100000001b3ull;
+      }
+    }
+  }
+  nnz_out[p] = nnz;
+  hash_out[p] = h;
+}
+
+// ------------------------------------------------------- host orchestration
+
+namespace {
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* get(size_t want) {
+    if (want > bytes) {
+      if (ptr) cudaFree(ptr);
+      ptr = nullptr;
+      bytes = 0;
+      DDSG_CUDA(cudaMalloc(&ptr, want));
+      bytes = want;
+    }
+    return ptr;
+  }
+  ~Scratch() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
+// Per-thread, per-device scratch (device buffers for host-memory calls).
+struct ThreadScratch {
+  Scratch xbuf[3], ybuf[3], bad;
+  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  ThreadScratch() {
+    for (auto& s : streams) DDSG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+  ~ThreadScratch() {
+    for (auto& s : streams)
+      if (s) cudaStreamDestroy(s);
+  }
+};
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventPair() {
+    DDSG_CUDA(cudaEventCreate(&a));
+    DDSG_CUDA(cudaEventCreate(&b));
+  }
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+constexpr int kMaxDevices = 64;
+
+ThreadScratch& scratch() {
+  static thread_local std::unique_ptr<ThreadScratch> per_dev[kMaxDevices];
+  int dev = 0;
+  DDSG_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) fail(DDSG_CUDA_ERROR, "device ordinal out of range");
+  if (!per_dev[dev]) per_dev[dev].reset(new ThreadScratch());
+  return *per_dev[dev];
+}
+
+EventPair& events() {
+  static thread_local std::unique_ptr<EventPair> per_dev[kMaxDevices];
+  int dev = 0;
+  DDSG_CUDA(cudaGetDevice(&dev));
+  if (!per_dev[dev]) per_dev[dev].reset(new EventPair());
+  return *per_dev[dev];
+}
+
+}  // namespace
+
+// Launches the evaluation of n device-resident points; returns kernel launches.
+static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* dx, int64_t n,
+                           int64_t base, double* dy, unsigned long long* dbad, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const EvalParams P = prog.params(exact);
+  constexpr int kCols = 8;
+  const int chunks = (P.m + kCols - 1) / kCols;
+  const int64_t threads = n * chunks;
+  const int block = 128;
+  const int64_t grid = (threads + block - 1) / block;
+  eval_generic_kernel<kCols><<<static_cast<unsigned>(grid), block, 0, st>>>(P, dx, n, base, dy, dbad);
+  DDSG_CUDA(cudaGetLastError());
+  return 1;
+}
+
+int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,
+                 cudaStream_t stream) {
+  EvalStats& stats = last_stats();
+  stats = EvalStats{};
+  if (n <= 0) return -1;
+  ThreadScratch& ts = scratch();
+  const int d = prog.host().d, m = prog.host().m;
+  unsigned long long* dbad = static_cast<unsigned long long*>(ts.bad.get(sizeof(unsigned long long)));
+  const unsigned long long init = ULLONG_MAX;
+  const bool x_dev = is_device_ptr(x), y_dev = is_device_ptr(y);
+  if (x_dev && y_dev) {
+    DDSG_CUDA(cudaMemcpyAsync(dbad, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    EventPair& ev = events();
+    DDSG_CUDA(cudaEventRecord(ev.a, stream));
+    stats.launches += launch_eval(prog, exact, x, n, 0, y, dbad, stream);
+    DDSG_CUDA(cudaEventRecord(ev.b, stream));
+    unsigned long long bad = 0;
+    DDSG_CUDA(cudaMemcpyAsync(&bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, stream));
+    DDSG_CUDA(cudaStreamSynchronize(stream));
+    float ms = 0.f;
+    DDSG_CUDA(cudaEventElapsedTime(&ms, ev.a, ev.b));
+    stats.kernel_ms = ms;
+    return bad == ULLONG_MAX ? -1 : static_cast<int64_t>(bad);
+  }
+  // Host (or mixed) buffers: pipeline H2D -> kernel -> D2H over three streams.
+  DDSG_CUDA(cudaStreamSynchronize(stream));
+  DDSG_CUDA(cudaMemcpy(dbad, &init, sizeof(init), cudaMemcpyHostToDevice));
+  const int64_t bytes_per_pt = static_cast<int64_t>(d + m) * 8;
+  int64_t chunk = std::max<int64_t>(4096, (int64_t{96} << 20) / bytes_per_pt);
+  chunk = std::min(chunk, n);
+  const int nbuf = 3;
+  for (int i = 0; i < nbuf; ++i) {
+    if (!x_dev) ts.xbuf[i].get(static_cast<size_t>(chunk) * d * 8);
+    if (!y_dev) ts.ybuf[i].get(static_cast<size_t>(chunk) * m * 8);
+  }
+  for (int64_t off = 0, it = 0; off < n; off += chunk, ++it) {
+    const int64_t cnt = std::min(chunk, n - off);
+    const int b = static_cast<int>(it % nbuf);
+    cudaStream_t st = ts.streams[b];
+    const double* dx = x_dev ? x + off * d : static_cast<const double*>(ts.xbuf[b].ptr);
+    double* dy = y_dev ? y + off * m : static_cast<double*>(ts.ybuf[b].ptr);
+    if (!x_dev)
+      DDSG_CUDA(cudaMemcpyAsync(const_cast<double*>(dx), x + off * d, cnt * d * 8,
+                                cudaMemcpyHostToDevice, st));
+    stats.launches += launch_eval(prog, exact, dx, cnt, off, dy, dbad, st);
+    if (!y_dev)
+      DDSG_CUDA(cudaMemcpyAsync(y + off * m, dy, cnt * m * 8, cudaMemcpyDeviceToHost, st));
+  }
+  for (auto& s : ts.streams) DDSG_CUDA(cudaStreamSynchronize(s));
+  unsigned long long bad = 0;
+  DDSG_CUDA(cudaMemcpy(&bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost));
+  return bad == ULLONG_MAX ? -1 : static_cast<int64_t>(bad);
+}
+
+int64_t support(const DeviceProgram& prog, const double* x, int64_t n, int64_t* nnz, uint64_t* hash,
+                cudaStream_t stream) {
+  if (n <= 0) return -1;
+  ThreadScratch& ts = scratch();
+  const int d = prog.host().d;
+  const bool x_dev = is_device_ptr(x), nnz_dev = is_device_ptr(nnz), h_dev = is_device_ptr(hash);
+  const double* dx = x;
+  int64_t* dn = nnz;
+  unsigned long long* dh = reinterpret_cast<unsigned long long*>(hash);
+  if (!x_dev) {
+    dx = static_cast<const double*>(ts.xbuf[0].get(static_cast<size_t>(n) * d * 8));
+    DDSG_CUDA(cudaMemcpyAsync(const_cast<double*>(dx), x, n * d * 8, cudaMemcpyHostToDevice, stream));
+  }
+  if (!nnz_dev) dn = static_cast<int64_t*>(ts.ybuf[0].get(static_cast<size_t>(n) * 8));
+  if (!h_dev) dh = static_cast<unsigned long long*>(ts.ybuf[1].get(static_cast<size_t>(n) * 8));
+  unsigned long long* dbad = static_cast<unsigned long long*>(ts.bad.get(sizeof(unsigned long long)));
+  const unsigned long long init = ULLONG_MAX;
+  DDSG_CUDA(cudaMemcpyAsync(dbad, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
+  const EvalParams P = prog.params(1);
+  const int block = 128;
+  support_kernel<<<static_cast<unsigned>((n + block - 1) / block), block, 0, stream>>>(P, dx, n, 0, dn, dh, dbad);
+  DDSG_CUDA(cudaGetLastError());
+  if (!nnz_dev) DDSG_CUDA(cudaMemcpyAsync(nnz, dn, n * 8, cudaMemcpyDeviceToHost, stream));
+  if (!h_dev) DDSG_CUDA(cudaMemcpyAsync(hash, dh, n * 8, cudaMemcpyDeviceToHost, stream));
+  unsigned long long bad = 0;
+  DDSG_CUDA(cudaMemcpyAsync(&bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, stream));
+  DDSG_CUDA(cudaStreamSynchronize(stream));
+  return bad == ULLONG_MAX ? -1 : static_cast<int64_t>(bad);
+}
+
+}  // namespace ddsg_b200

@@ -1,0 +1,371 @@
+// Host-side sparse grid: from_nodes, adaptive build, quadrature, layout compiler.
+// Compiled with -ffp-contract=off: every floating-point expression below must
+// round exactly like the reference's Release build (mul then add, no FMA).
+#include "grid_host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <map>
+#include <numeric>
+#include <sstream>
+#include <unordered_set>
+
+namespace ddsg_b200 {
+
+double basis_value_host(int mode, int level, uint32_t index, double x) {
+  // basis_kind (basis.hpp:27-33) + basis_value (basis.hpp:36-54).
+  const double inv_h = std::ldexp(1.0, level);
+  const double center = static_cast<double>(index) / inv_h;
+  if (mode == DDSG_MODIFIED_LINEAR) {
+    if (level == 1) return 1.0;
+    if (index == 1u) {
+      const double v = 2.0 - x * inv_h;
+      return v > 0.0 ? v : 0.0;
+    }
+    if (index == (1u << level) - 1u) {
+      const double v = 2.0 - (1.0 - x) * inv_h;
+      return v > 0.0 ? v : 0.0;
+    }
+  }
+  const double v = 1.0 - std::abs(x - center) * inv_h;
+  return v > 0.0 ? v : 0.0;
+}
+
+static double basis_weight_host(int mode, int level, uint32_t index) {
+  // basis_weight (basis.hpp:57-65) with h = 1 / inv_h.
+  const double h = 1.0 / std::ldexp(1.0, level);
+  if (mode == DDSG_MODIFIED_LINEAR) {
+    if (level == 1) return 1.0;
+    if (index == 1u || index == (1u << level) - 1u) return 2.0 * h;
+  }
+  return h;
+}
+
+static int level_sum_of(const uint32_t* key, int dim) {
+  int s = 0;
+  for (int j = 0; j < dim; ++j) s += level_of(key[j]);
+  return s;
+}
+
+void HostGrid::index_node(int64_t i) {
+  std::vector<uint32_t> k(keys.begin() + i * dim, keys.begin() + (i + 1) * dim);
+  if (!lookup_.emplace(std::move(k), i).second)
+    fail(DDSG_INVALID_ARGUMENT, "sparse grid: duplicate node key");
+}
+
+bool HostGrid::contains(const uint32_t* key) const { return find(key) >= 0; }
+
+int64_t HostGrid::find(const uint32_t* key) const {
+  auto it = lookup_.find(std::vector<uint32_t>(key, key + dim));
+  return it == lookup_.end() ? -1 : it->second;
+}
+
+static void validate_keys(int dim, int64_t n, const uint32_t* keys) {
+  for (int64_t i = 0; i < n * dim; ++i)
+    if (!valid_key(keys[i]))
+      fail(DDSG_INVALID_ARGUMENT, "sparse grid: invalid heap key " + std::to_string(keys[i]) +
+                                      " (level must be in [1,30])");
+}
+
+HostGrid HostGrid::from_nodes(int dim, int m, int mode, int max_level, double eps_gamma, int64_t n,
+                              const uint32_t* keys, const double* surplus) {
+  if (dim < 1) fail(DDSG_INVALID_ARGUMENT, "sparse grid: dim must be >= 1");
+  if (m < 1) fail(DDSG_INVALID_ARGUMENT, "sparse grid: out_dim must be >= 1");
+  if (mode != DDSG_ZERO_BOUNDARY && mode != DDSG_MODIFIED_LINEAR)
+    fail(DDSG_INVALID_ARGUMENT, "sparse grid: unknown boundary mode");
+  if (n < 0 || (n > 0 && (!keys || !surplus)))
+    fail(DDSG_INVALID_ARGUMENT, "sparse grid: null node arrays");
+  validate_keys(dim, n, keys);
+  HostGrid g;
+  g.dim = dim;
+  g.m = m;
+  g.mode = mode;
+  g.max_level = max_level;
+  g.eps_gamma = eps_gamma;
+  g.keys.assign(keys, keys + n * dim);
+  g.surplus.assign(surplus, surplus + n * m);
+  g.lookup_.reserve(static_cast<size_t>(n) * 2);
+  for (int64_t i = 0; i < n; ++i) g.index_node(i);
+  return g;
+}
+
+void HostGrid::append(int64_t n, const uint32_t* k, const double* s) {
+  if (n < 0 || (n > 0 && (!k || !s))) fail(DDSG_INVALID_ARGUMENT, "grid append: null arrays");
+  validate_keys(dim, n, k);
+  const int64_t base = size();
+  keys.insert(keys.end(), k, k + n * dim);
+  surplus.insert(surplus.end(), s, s + n * m);
+  for (int64_t i = 0; i < n; ++i) {
+    try {
+      index_node(base + i);
+    } catch (...) {
+      // roll back so the grid stays consistent
+      for (int64_t r = 0; r < i; ++r)
+        lookup_.erase(std::vector<uint32_t>(keys.begin() + (base + r) * dim,
+                                            keys.begin() + (base + r + 1) * dim));
+      keys.resize(base * dim);
+      surplus.resize(base * m);
+      throw;
+    }
+  }
+}
+
+std::vector<double> HostGrid::quadrature() const {
+  // sparse_grid.hpp:138-149: fixed (stored) node order, mul then add.
+  std::vector<double> q(m, 0.0);
+  const int64_t n = size();
+  for (int64_t i = 0; i < n; ++i) {
+    double w = 1.0;
+    for (int j = 0; j < dim; ++j) {
+      const uint32_t hk = keys[i * dim + j];
+      w *= basis_weight_host(mode, level_of(hk), index_of(hk));
+    }
+    const double* s = &surplus[i * m];
+    for (int c = 0; c < m; ++c) q[c] += w * s[c];
+  }
+  return q;
+}
+
+void HostGrid::interpolate_at_node(const uint32_t* key, int64_t upto, double* out) const {
+  // Nonzero terms at a grid node x(key) come only from subspaces l <= level(key)
+  // componentwise (deeper levels put x on a cell boundary, where every 1-d
+  // factor vanishes).  Collect them, order by stored index, accumulate.
+  std::vector<double> x(dim);
+  std::vector<int> L(dim);
+  for (int j = 0; j < dim; ++j) {
+    x[j] = coordinate_of(key[j]);
+    L[j] = level_of(key[j]);
+  }
+  struct Term {
+    int64_t idx;
+    double w;
+  };
+  std::vector<Term> terms;
+  std::vector<int> l(dim, 1);
+  std::vector<uint32_t> cand(dim);
+  while (true) {
+    double w = 1.0;
+    bool zero = false;
+    for (int j = 0; j < dim; ++j) {
+      const int lj = l[j];
+      const uint32_t ncell = 1u << (lj - 1);
+      uint32_t k = static_cast<uint32_t>(std::ldexp(x[j], lj - 1));  // floor, x >= 0
+      if (k >= ncell) k = ncell - 1;
+      cand[j] = ncell + k;
+    }
+    const int64_t idx = find(cand.data());
+    if (idx >= 0 && idx < upto) {
+      for (int j = 0; j < dim; ++j) {
+        w *= basis_value_host(mode, l[j], index_of(cand[j]), x[j]);
+        if (w == 0.0) {
+          zero = true;
+          break;
+        }
+      }
+      if (!zero && w != 0.0) terms.push_back({idx, w});
+    }
+    int j = 0;
+    while (j < dim) {
+      if (++l[j] <= L[j]) break;
+      l[j] = 1;
+      ++j;
+    }
+    if (j == dim) break;
+  }
+  std::sort(terms.begin(), terms.end(), [](const Term& a, const Term& b) { return a.idx < b.idx; });
+  for (const Term& t : terms) {
+    const double* s = &surplus[t.idx * m];
+    for (int c = 0; c < m; ++c) out[c] += t.w * s[c];
+  }
+}
+
+std::vector<std::vector<uint32_t>> HostGrid::next_candidates(int s, std::vector<char>& refined) {
+  // sparse_grid.hpp:215-254.
+  std::unordered_set<std::vector<uint32_t>, VecHash> seen;
+  std::vector<std::vector<uint32_t>> out;
+  auto have = [&](const std::vector<uint32_t>& k) { return contains(k.data()) || seen.count(k); };
+  auto push_missing_ancestors = [&](const std::vector<uint32_t>& key) {
+    std::vector<std::vector<uint32_t>> stack{key};
+    while (!stack.empty()) {
+      std::vector<uint32_t> cur = std::move(stack.back());
+      stack.pop_back();
+      for (int j = 0; j < dim; ++j) {
+        if (cur[j] <= 1u) continue;
+        std::vector<uint32_t> p = cur;
+        p[j] = cur[j] >> 1;
+        if (have(p)) continue;
+        seen.insert(p);
+        out.push_back(p);
+        stack.push_back(std::move(p));
+      }
+    }
+  };
+  const int64_t n = size();
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t* key = &keys[i * dim];
+    if (level_sum_of(key, dim) != s) continue;
+    bool significant = eps_gamma == 0.0;
+    if (!significant) {
+      double g = 0.0;
+      const double* sp = &surplus[i * m];
+      if (norm == DDSG_NORM_INF) {
+        for (int c = 0; c < m; ++c) g = std::max(g, std::abs(sp[c]));
+      } else {
+        for (int c = 0; c < m; ++c) g += sp[c] * sp[c];
+        g = std::sqrt(g);
+      }
+      significant = g > eps_gamma;
+    }
+    if (!significant) continue;
+    refined[i] = 1;
+    for (int j = 0; j < dim; ++j) {
+      for (uint32_t child : {key[j] * 2u, key[j] * 2u + 1u}) {
+        std::vector<uint32_t> c(key, key + dim);
+        c[j] = child;
+        if (contains(c.data()) || !seen.insert(c).second) continue;
+        out.push_back(c);
+        push_missing_ancestors(c);
+      }
+    }
+  }
+  std::sort(out.begin(), out.end(), [&](const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
+    const int sa = level_sum_of(a.data(), dim), sb = level_sum_of(b.data(), dim);
+    if (sa != sb) return sa < sb;
+    return a < b;
+  });
+  return out;
+}
+
+void HostGrid::insert_batch(const std::vector<std::vector<uint32_t>>& batch, const BatchEval& f) {
+  // sparse_grid.hpp:256-298: evaluate the whole batch against the frozen grid,
+  // reject non-finite values, then hierarchize one by one in batch order.
+  const int64_t nb = static_cast<int64_t>(batch.size());
+  std::vector<double> xs(nb * dim), vals(nb * m, 0.0);
+  for (int64_t i = 0; i < nb; ++i)
+    for (int j = 0; j < dim; ++j) xs[i * dim + j] = coordinate_of(batch[i][j]);
+  f(xs.data(), nb, vals.data());
+  for (int64_t i = 0; i < nb; ++i) {
+    for (int c = 0; c < m; ++c) {
+      if (!std::isfinite(vals[i * m + c])) {
+        std::ostringstream os;
+        os << "sparse grid: evaluator returned a non-finite value at grid point (";
+        for (int j = 0; j < dim; ++j) os << (j ? ", " : "") << xs[i * dim + j];
+        os << ")";
+        throw BuildError(os.str(), std::vector<double>(xs.begin() + i * dim, xs.begin() + (i + 1) * dim));
+      }
+    }
+  }
+  std::vector<double> interp(m);
+  for (int64_t i = 0; i < nb; ++i) {
+    std::fill(interp.begin(), interp.end(), 0.0);
+    interpolate_at_node(batch[i].data(), size(), interp.data());
+    keys.insert(keys.end(), batch[i].begin(), batch[i].end());
+    for (int c = 0; c < m; ++c) surplus.push_back(vals[i * m + c] - interp[c]);
+    index_node(size() - 1);
+  }
+}
+
+HostGrid HostGrid::build(int dim, int m, int mode, int max_level, double eps_gamma, int norm,
+                         const BatchEval& f) {
+  // sparse_grid.hpp:84-108.
+  if (dim < 1) fail(DDSG_INVALID_ARGUMENT, "sparse grid: dim must be >= 1");
+  if (m < 1) fail(DDSG_INVALID_ARGUMENT, "sparse grid: out_dim must be >= 1");
+  if (max_level < 1) fail(DDSG_INVALID_ARGUMENT, "sparse grid: max_level must be >= 1");
+  if (max_level > kMaxLevel) fail(DDSG_INVALID_ARGUMENT, "sparse grid: max_level must be <= 30");
+  if (!(eps_gamma >= 0.0)) fail(DDSG_INVALID_ARGUMENT, "sparse grid: eps_gamma must be >= 0");
+  if (mode != DDSG_ZERO_BOUNDARY && mode != DDSG_MODIFIED_LINEAR)
+    fail(DDSG_INVALID_ARGUMENT, "sparse grid: unknown boundary mode");
+  HostGrid g;
+  g.dim = dim;
+  g.m = m;
+  g.mode = mode;
+  g.max_level = max_level;
+  g.eps_gamma = eps_gamma;
+  g.norm = norm;
+  const int max_sum = max_level + dim - 1;
+  std::vector<std::vector<uint32_t>> batch{std::vector<uint32_t>(dim, 1u)};
+  std::vector<char> refined;
+  for (int s = dim; s <= max_sum && !batch.empty(); ++s) {
+    g.insert_batch(batch, f);
+    if (s == max_sum) break;
+    refined.assign(g.size(), 0);
+    batch = g.next_candidates(s, refined);
+  }
+  return g;
+}
+
+GridLayout HostGrid::compile() const {
+  const int64_t n = size();
+  // group nodes by level vector
+  std::map<std::vector<uint8_t>, std::vector<int64_t>> groups;
+  for (int64_t i = 0; i < n; ++i) {
+    std::vector<uint8_t> l(dim);
+    for (int j = 0; j < dim; ++j) l[j] = static_cast<uint8_t>(level_of(keys[i * dim + j]));
+    groups[l].push_back(i);
+  }
+  GridLayout L;
+  for (auto& [lv, nodes] : groups) {
+    SubspaceInfo s;
+    s.levels = lv;
+    s.level_sum = 0;
+    int cell_bits = 0;
+    for (uint8_t v : lv) {
+      s.level_sum += v;
+      cell_bits += v - 1;
+    }
+    if (cell_bits > 40) fail(DDSG_INVALID_ARGUMENT, "sparse grid: subspace too deep for the dense layout");
+    s.cells = int64_t{1} << cell_bits;
+    s.n_nodes = static_cast<int64_t>(nodes.size());
+    L.subspaces.push_back(std::move(s));
+  }
+  // canonical subspace order: (|l|_1, l lexicographic)
+  std::vector<size_t> order(L.subspaces.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::vector<std::vector<int64_t>*> node_lists;
+  for (auto& kv : groups) node_lists.push_back(&kv.second);
+  std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+    const auto& A = L.subspaces[a];
+    const auto& B = L.subspaces[b];
+    if (A.level_sum != B.level_sum) return A.level_sum < B.level_sum;
+    return A.levels < B.levels;
+  });
+  int64_t total_cells = 0;
+  for (size_t o : order) total_cells += L.subspaces[o].cells;
+  if (total_cells > std::max<int64_t>(8 * n, n + (int64_t{1} << 22)) || total_cells > (int64_t{1} << 31) - 1)
+    fail(DDSG_INVALID_ARGUMENT,
+         "sparse grid: adaptive grid too sparse for the dense subspace layout (" +
+             std::to_string(total_cells) + " cells for " + std::to_string(n) + " nodes)");
+  std::vector<SubspaceInfo> sorted;
+  sorted.reserve(order.size());
+  L.slab.assign(total_cells, -1);
+  L.row_to_stored.resize(n);
+  int64_t slab_off = 0, row = 0;
+  for (size_t o : order) {
+    SubspaceInfo s = L.subspaces[o];
+    s.slab_offset = slab_off;
+    // cell linear index, dim 0 most significant
+    std::vector<std::pair<int64_t, int64_t>> cells;  // (cell, stored index)
+    for (int64_t i : *node_lists[o]) {
+      int64_t lin = 0;
+      for (int j = 0; j < dim; ++j) {
+        const uint32_t hk = keys[i * dim + j];
+        lin = (lin << (level_of(hk) - 1)) | cell_of(hk);
+      }
+      cells.emplace_back(lin, i);
+    }
+    std::sort(cells.begin(), cells.end());
+    for (auto& [lin, i] : cells) {
+      L.slab[slab_off + lin] = static_cast<int32_t>(row);
+      L.row_to_stored[row] = static_cast<int32_t>(i);
+      ++row;
+    }
+    slab_off += s.cells;
+    sorted.push_back(std::move(s));
+  }
+  L.subspaces = std::move(sorted);
+  L.rows = row;
+  return L;
+}
+
+}  // namespace ddsg_b200

@@ -1,0 +1,138 @@
+"""Synthetic workloads of BASELINE.json's five configs.
+
+Every grid is built by this package's own builder (ddsg_grid_build, the
+reference's build algorithm) from C target functions in
+libddsg_workloads.so; HDMR configs are assembled from cut grids through
+VectorizedDdsg.compile (DdsgFunction::from_parts + compile, hdmr.hpp:307-325,
+ddsg_eval.hpp:40-74) with a center anchor.  Choices BASELINE.json leaves open
+are fixed here and recorded in DESIGN.md §Workloads.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .ddsg import MODIFIED_LINEAR, ZERO_BOUNDARY, SparseGridFunction, VectorizedDdsg
+
+
+@dataclass
+class Config:
+    name: str
+    d: int
+    m: int
+    n_points: int
+    kind: str  # "grid" or "hdmr"
+    seed: int
+    # plain grid
+    max_level: int = 1
+    eps_gamma: float = 0.0
+    mode: int = ZERO_BOUNDARY
+    target: str = ""
+    # hdmr
+    level_1d: int = 8
+    level_2d: int = 5
+    eps_1d: float = 0.0
+    eps_2d: float = 0.0
+    notes: str = ""
+
+
+CONFIGS = {
+    1: Config("config1_sg_d4_L5", d=4, m=1, n_points=65536, kind="grid", seed=1001, max_level=5,
+              eps_gamma=0.0, mode=ZERO_BOUNDARY, target="wl_config1",
+              notes="regular grid, hat basis, no boundary points"),
+    2: Config("config2_sg_d10_L6", d=10, m=11, n_points=1 << 20, kind="grid", seed=1002, max_level=6,
+              eps_gamma=0.0, mode=ZERO_BOUNDARY, target="wl_config2",
+              notes="regular grid, hat basis, f_j = prod (1+0.1 j x_k)^0.3, j=0..10"),
+    3: Config("config3_asg_d20", d=20, m=21, n_points=1 << 20, kind="grid", seed=1003, max_level=5,
+              eps_gamma=1e-3, mode=MODIFIED_LINEAR, target="wl_config3",
+              notes="adaptive, eps=1e-3, level capped at 5 (L=10 is infeasible, SURVEY.md finding 4)"),
+    4: Config("config4_hdmr_d100", d=100, m=51, n_points=1 << 21, kind="hdmr", seed=1004, level_1d=8,
+              level_2d=6, eps_1d=1e-6, eps_2d=1e-6, mode=MODIFIED_LINEAR, target="wl_config4",
+              notes="100 1-d cuts (L=8) + 45 2-d cuts on dims 0-9 (L=6), eps_gamma=1e-6, center anchor"),
+    5: Config("config5_hdmr_d300", d=300, m=151, n_points=1 << 22, kind="hdmr", seed=1005, level_1d=8,
+              level_2d=5, eps_1d=1e-8, eps_2d=1e-8, mode=MODIFIED_LINEAR, target="wl_config5",
+              notes="300 1-d cuts (L=8) + 300 seeded-random pair cuts (L=5), kinked policies, center anchor"),
+}
+
+
+def telescoping_b(family: List[Tuple[int, ...]]) -> List[int]:
+    """b_i = sum over family members u >= i of (-1)^(|u|-|i|)
+    (hdmr.hpp:339-355 finalize_coefficients; family includes the empty index)."""
+    sets = [frozenset(u) for u in family]
+    out = []
+    for i, si in enumerate(sets):
+        b = 0
+        for u, su in enumerate(sets):
+            if si <= su:
+                b += 1 if (len(su) - len(si)) % 2 == 0 else -1
+        out.append(b)
+    return out
+
+
+def build_grid(cfg: Config) -> SparseGridFunction:
+    return SparseGridFunction.build(N.wl_fn(cfg.target), cfg.d, cfg.m, cfg.max_level, cfg.eps_gamma, cfg.mode)
+
+
+def hdmr_family(cfg: Config) -> List[Tuple[int, ...]]:
+    wl = N.workloads()
+    if cfg.kind != "hdmr":
+        raise ValueError("not an HDMR config")
+    cfg_id = 4 if cfg.d == 100 else 5
+    pairs = np.zeros(2 * 400, dtype=np.int32)
+    n_pairs = wl.wl_config_pairs(cfg_id, pairs.ctypes.data)
+    fam: List[Tuple[int, ...]] = [()]
+    fam += [(k,) for k in range(cfg.d)]
+    fam += sorted({(int(pairs[2 * r]), int(pairs[2 * r + 1])) for r in range(n_pairs)})
+    return fam
+
+
+@dataclass
+class HdmrParts:
+    d: int
+    m: int
+    f_anchor: np.ndarray
+    slots: list = field(default_factory=list)  # (dims, b, SparseGridFunction or None)
+
+
+def build_hdmr_parts(cfg: Config) -> HdmrParts:
+    wl = N.workloads()
+    fam = hdmr_family(cfg)
+    b = telescoping_b(fam)
+    anchor = np.full(cfg.d, 0.5)
+    fa = np.empty(cfg.m)
+    fn = getattr(wl, cfg.target)
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+    fn(anchor.ctypes.data, 1, fa.ctypes.data, None)
+    parts = HdmrParts(cfg.d, cfg.m, fa)
+    f_addr = N.wl_fn(cfg.target)
+    cut_addr = N.wl_fn("wl_cut_eval")
+    for u, bu in zip(fam, b):
+        if not u:
+            parts.slots.append((u, bu, None))
+            continue
+        dims = np.array(u, dtype=np.int32)
+        cut = wl.wl_cut_new(f_addr, None, cfg.d, cfg.m, len(u), dims.ctypes.data, anchor.ctypes.data)
+        try:
+            lvl = cfg.level_1d if len(u) == 1 else cfg.level_2d
+            eps = cfg.eps_1d if len(u) == 1 else cfg.eps_2d
+            g = SparseGridFunction.build(cut_addr, len(u), cfg.m, lvl, eps, cfg.mode, ctx=cut)
+        finally:
+            wl.wl_cut_free(C.c_void_p(cut))
+        parts.slots.append((u, bu, g))
+    return parts
+
+
+def build_hdmr(cfg: Config) -> Tuple[VectorizedDdsg, HdmrParts]:
+    parts = build_hdmr_parts(cfg)
+    return VectorizedDdsg.compile(parts.d, parts.m, parts.f_anchor, parts.slots), parts
+
+
+def points(cfg: Config, n: Optional[int] = None, seed: Optional[int] = None) -> np.ndarray:
+    from .ddsg import uniform_points
+
+    return uniform_points(cfg.seed if seed is None else seed, cfg.n_points if n is None else n, cfg.d)

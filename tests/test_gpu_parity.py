@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar (BASELINE.json north star):
+  * support selection bit-exact (per-point nnz + ordered (slot, node) hash);
+  * EXACT mode: values bit-identical to the oracle on canonical-order grids;
+  * FAST mode: |delta| <= 1e-14 + 1e-12 |ref| where the survey measured it holds.
+Grids are fed to both sides with the SAME bits in canonical node order
+(SURVEY.md §8(c) parity protocol).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from helpers import (bits, canonical_perm, golden_files, hdmr_slots_from_golden, int_ctx, load,
+                     make_vectorized, within_tol, wl)
+from paper_2202_06555_b200 import workloads as W
+from paper_2202_06555_b200.ddsg import (EXACT, FAST, MODIFIED_LINEAR, ZERO_BOUNDARY, DomainError,
+                                        SparseGridFunction, VectorizedDdsg, last_eval_stats, uniform_points)
+
+pytestmark = pytest.mark.gpu
+
+
+def canonical_grid(g: SparseGridFunction) -> SparseGridFunction:
+    keys, sur = g.nodes()
+    p = canonical_perm(keys)
+    return SparseGridFunction.from_nodes(g.dim, g.out_dim, g.max_level, g.eps_gamma, g.boundary_mode, keys[p], sur[p])
+
+
+def grid_oracle(g: SparseGridFunction, x):
+    keys, sur = g.nodes()
+    rc, y, bad = O.port_grid_eval(g.dim, g.out_dim, g.boundary_mode, keys, sur, x)
+    assert rc == 0
+    return y
+
+
+# ------------------------------------------------------------ golden fixtures
+
+@pytest.mark.parametrize("path", golden_files("grid"), ids=lambda p: p.stem)
+def test_golden_grid_exact(path):
+    z = load(path)
+    dim, m = int(z["dim"]), int(z["m"])
+    p = canonical_perm(z["keys"])
+    g = SparseGridFunction.from_nodes(dim, m, int(z["max_level"]), float(z["eps"]), int(z["mode"]), z["keys"][p],
+                                      z["surplus"][p])
+    y = g.interpolate(z["x"])
+    assert np.array_equal(bits(y), bits(z["y_canonical"]))
+    # stored-order reference output: within the north-star tolerance
+    assert within_tol(y, z["y_stored"]).all()
+
+
+@pytest.mark.parametrize("path", golden_files("hdmr"), ids=lambda p: p.stem)
+def test_golden_hdmr_exact(path):
+    z = load(path)
+    d, m = int(z["d"]), int(z["m"])
+    vec = make_vectorized(d, m, z["f_anchor"], hdmr_slots_from_golden(z, canonical=True), int(z["max_level"]),
+                          float(z["eps"]))
+    y = vec.evaluate_batch(z["x"])
+    assert np.array_equal(bits(y), bits(z["y_canonical"]))
+    assert within_tol(y, z["y_stored"]).all()
+    # vectorized == naive telescoping (test_ddsg_eval.cpp:106-120, 1e-12)
+    assert np.max(np.abs(y - z["y_naive"])) <= 1e-12
+
+
+# ------------------------------------------------------------ plain grids
+
+GRID_CASES = [
+    # (target, dim, m, level, eps, mode, ctx_dim)
+    ("wl_config1", 4, 1, 5, 0.0, ZERO_BOUNDARY, 4),
+    ("wl_config1", 4, 1, 5, 0.0, MODIFIED_LINEAR, 4),
+    ("wl_coupled", 6, 1, 4, 1e-4, MODIFIED_LINEAR, 6),
+    ("wl_coupled", 3, 1, 6, 1e-5, ZERO_BOUNDARY, 3),
+    ("wl_config3", 20, 21, 3, 1e-3, MODIFIED_LINEAR, None),
+    ("wl_vector3", 2, 3, 7, 0.0, MODIFIED_LINEAR, None),
+]
+
+
+@pytest.mark.parametrize("case", GRID_CASES, ids=lambda c: f"{c[0]}-d{c[1]}-L{c[3]}-mode{c[5]}")
+def test_grid_exact_bitwise_and_support(case):
+    fn, dim, m, L, eps, mode, cd = case
+    keep, ctx = int_ctx(cd) if cd else (None, 0)
+    g = canonical_grid(SparseGridFunction.build(wl(fn), dim, m, L, eps, mode, ctx=ctx))
+    x = uniform_points(4242 + dim, 3000, dim)
+    x[:8] = np.array([0.0, 1.0, 0.5, 0.25, 0.75, 1 - 2**-53, 2**-30, 0.125])[:, None]
+    y = g.interpolate(x)
+    want = grid_oracle(g, x)
+    assert np.array_equal(bits(y), bits(want))
+    keys, _ = g.nodes()
+    nnz_o, h_o = O.port_grid_support(dim, mode, keys, x)
+    nnz, h = g.support(x)
+    assert np.array_equal(nnz, nnz_o)
+    assert np.array_equal(h, h_o)
+
+
+@pytest.mark.parametrize("case", GRID_CASES[:4], ids=lambda c: f"{c[0]}-d{c[1]}")
+def test_grid_fast_mode_tolerance(case):
+    fn, dim, m, L, eps, mode, cd = case
+    keep, ctx = int_ctx(cd) if cd else (None, 0)
+    g = canonical_grid(SparseGridFunction.build(wl(fn), dim, m, L, eps, mode, ctx=ctx))
+    g.set_eval_mode(FAST)
+    x = uniform_points(99, 2000, dim)
+    assert within_tol(g.interpolate(x), grid_oracle(g, x)).all()
+
+
+def test_config2_grid_exact_sample():
+    cfg = W.CONFIGS[2]
+    g = canonical_grid(W.build_grid(cfg))
+    assert g.size() == 77505
+    x = W.points(cfg, n=256)
+    assert np.array_equal(bits(g.interpolate(x)), bits(grid_oracle(g, x)))
+
+
+def test_domain_error_lowest_index():
+    g = SparseGridFunction.build(wl("wl_config1"), 4, 1, 3, 0.0, ZERO_BOUNDARY)
+    x = uniform_points(5, 1000, 4)
+    x[700, 2] = 1.5
+    x[300, 1] = np.nan
+    x[900, 0] = -0.1
+    with pytest.raises(DomainError) as ei:
+        g.interpolate(x)
+    assert ei.value.task_id == 300
+
+
+def test_empty_batch_and_single_point():
+    g = SparseGridFunction.build(wl("wl_config1"), 4, 1, 4, 0.0, ZERO_BOUNDARY)
+    assert g.interpolate(np.zeros((0, 4))).shape == (0, 1)
+    x = uniform_points(8, 17, 4)
+    batch = g.interpolate(x)
+    for i in range(17):
+        assert bits(g.interpolate(x[i]))[0] == bits(batch[i])[0]
+
+
+def test_device_pointer_path_matches_host():
+    torch = pytest.importorskip("torch")
+    cfg = W.CONFIGS[1]
+    g = W.build_grid(cfg)
+    x = W.points(cfg, n=50000)
+    y_host = g.interpolate(x)
+    xd = torch.from_numpy(x).cuda()
+    y_dev = g.interpolate(xd).cpu().numpy()
+    assert np.array_equal(bits(y_host), bits(y_dev))
+
+
+# ------------------------------------------------------------------ HDMR
+
+def hdmr_from_config(cid):
+    cfg = W.CONFIGS[cid]
+    parts = W.build_hdmr_parts(cfg)
+    slots = []
+    for u, b, g in parts.slots:
+        if g is None:
+            slots.append((u, b, None))
+        else:
+            keys, sur = g.nodes()
+            p = canonical_perm(keys)
+            slots.append((u, b, (g.boundary_mode, keys[p], sur[p])))
+    vec = make_vectorized(cfg.d, cfg.m, parts.f_anchor, slots, cfg.level_1d)
+    return cfg, parts, slots, vec
+
+
+@pytest.fixture(scope="module")
+def config4():
+    return hdmr_from_config(4)
+
+
+@pytest.fixture(scope="module")
+def config5():
+    return hdmr_from_config(5)
+
+
+@pytest.mark.parametrize("cid", [4, 5])
+def test_hdmr_config_exact_bitwise(cid, config4, config5):
+    cfg, parts, slots, vec = config4 if cid == 4 else config5
+    x = W.points(cfg, n=512 if cid == 4 else 128)
+    rc, want, _ = O.port_hdmr_eval(cfg.d, cfg.m, parts.f_anchor, slots, x)
+    assert rc == 0
+    y = vec.evaluate_batch(x)
+    assert np.array_equal(bits(y), bits(want))
+    nnz_o, h_o = O.port_hdmr_support(cfg.d, cfg.m, slots, x)
+    nnz, h = vec.support(x)
+    assert np.array_equal(nnz, nnz_o) and np.array_equal(h, h_o)
+
+
+def test_hdmr_batch_permutation_and_chunking(config4):
+    cfg, parts, slots, vec = config4
+    x = W.points(cfg, n=4000, seed=8443)
+    y = vec.evaluate_batch(x)
+    yr = vec.evaluate_batch(x[::-1].copy())
+    assert np.array_equal(bits(yr[::-1]), bits(y))
+    one = vec.evaluate_batch(x[17])
+    assert np.array_equal(bits(one), bits(y[17]))
+
+
+def test_hdmr_fast_mode_config5_tolerance(config5):
+    cfg, parts, slots, vec = config5
+    x = W.points(cfg, n=128, seed=77)
+    rc, want, _ = O.port_hdmr_eval(cfg.d, cfg.m, parts.f_anchor, slots, x)
+    vec.set_eval_mode(FAST)
+    try:
+        y = vec.evaluate_batch(x)
+    finally:
+        vec.set_eval_mode(EXACT)
+    ok = within_tol(y, want)
+    assert ok.mean() > 0.999  # FAST is a throughput mode; EXACT is the parity mode
+
+
+def test_hdmr_domain_error(config4):
+    cfg, parts, slots, vec = config4
+    x = W.points(cfg, n=100)
+    x[42, 99] = 1.0000000000000002
+    with pytest.raises(DomainError) as ei:
+        vec.evaluate_batch(x)
+    assert ei.value.task_id == 42
+
+
+def test_eval_reports_kernel_launches(config4):
+    cfg, parts, slots, vec = config4
+    torch = pytest.importorskip("torch")
+    x = torch.from_numpy(W.points(cfg, n=1000)).cuda()
+    vec.evaluate_batch(x)
+    launches, ms = last_eval_stats()
+    assert launches >= 1 and ms > 0.0
