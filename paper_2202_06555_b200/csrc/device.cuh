@@ -10,6 +10,10 @@
 #include "program.hpp"
 
 namespace ddsg_b200 {
+class FastHdmr;
+}
+
+namespace ddsg_b200 {
 
 #define DDSG_CUDA(call)                                                                     \
   do {                                                                                      \
@@ -55,12 +59,14 @@ class DeviceProgram {
   EvalParams params(int exact) const;
   bool ready() const { return ready_; }
   const HostProgram& host() const { return hp_; }
+  const FastHdmr* fast() const { return fast_; }
 
  private:
   HostProgram hp_;
   std::vector<void*> allocs_;
   EvalParams p_{};
   bool ready_ = false;
+  FastHdmr* fast_ = nullptr;  // slot-staged kernel program, when the program qualifies
   template <typename T>
   const T* put(const std::vector<T>& v);
 };

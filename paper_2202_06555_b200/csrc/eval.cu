@@ -20,6 +20,7 @@
 
 #include "basis.cuh"
 #include "device.cuh"
+#include "fast_hdmr.cuh"
 
 namespace ddsg_b200 {
 
@@ -30,6 +31,7 @@ EvalStats& last_stats() {
 
 DeviceProgram::~DeviceProgram() {
   for (void* p : allocs_) cudaFree(p);
+  delete fast_;
 }
 
 template <typename T>
@@ -45,6 +47,8 @@ const T* DeviceProgram::put(const std::vector<T>& v) {
 void DeviceProgram::upload(const HostProgram& hp) {
   for (void* p : allocs_) cudaFree(p);
   allocs_.clear();
+  delete fast_;
+  fast_ = nullptr;
   ready_ = false;
   hp_ = hp;
   EvalParams p{};
@@ -71,6 +75,12 @@ void DeviceProgram::upload(const HostProgram& hp) {
   p.row_stored = put(hp.row_stored);
   p.f_anchor = put(hp.f_anchor);
   p_ = p;
+  delete fast_;
+  fast_ = new FastHdmr();
+  if (!fast_->build(hp)) {
+    delete fast_;
+    fast_ = nullptr;
+  }
   ready_ = true;
 }
 
@@ -256,7 +266,7 @@ struct Scratch {
 
 // Per-thread, per-device scratch (device buffers for host-memory calls).
 struct ThreadScratch {
-  Scratch xbuf[3], ybuf[3], bad;
+  Scratch xbuf[3], ybuf[3], bad, xt[4];
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
   ThreadScratch() {
     for (auto& s : streams) DDSG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -302,9 +312,22 @@ EventPair& events() {
 
 // Launches the evaluation of n device-resident points; returns kernel launches.
 static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* dx, int64_t n,
-                           int64_t base, double* dy, unsigned long long* dbad, cudaStream_t st) {
+                           int64_t base, double* dy, unsigned long long* dbad, cudaStream_t st,
+                           Scratch& xt_scratch) {
   if (n <= 0) return 0;
   const EvalParams P = prog.params(exact);
+  if (const FastHdmr* f = prog.fast()) {
+    // chunk so the dim-major scratch stays <= ~1 GiB
+    const int d = f->dim();
+    const int64_t chunk = std::max<int64_t>(32768, (int64_t{1} << 30) / (int64_t{8} * d));
+    int64_t launches = 0;
+    for (int64_t off = 0; off < n; off += chunk) {
+      const int64_t cnt = std::min(chunk, n - off);
+      double* xt = static_cast<double*>(xt_scratch.get(static_cast<size_t>(std::min(chunk, n)) * d * 8));
+      launches += f->launch(exact, dx + off * d, cnt, base + off, dy + off * P.m, dbad, xt, st);
+    }
+    return launches;
+  }
   constexpr int kCols = 8;
   const int chunks = (P.m + kCols - 1) / kCols;
   const int64_t threads = n * chunks;
@@ -329,7 +352,7 @@ int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t 
     DDSG_CUDA(cudaMemcpyAsync(dbad, &init, sizeof(init), cudaMemcpyHostToDevice, stream));
     EventPair& ev = events();
     DDSG_CUDA(cudaEventRecord(ev.a, stream));
-    stats.launches += launch_eval(prog, exact, x, n, 0, y, dbad, stream);
+    stats.launches += launch_eval(prog, exact, x, n, 0, y, dbad, stream, ts.xt[3]);
     DDSG_CUDA(cudaEventRecord(ev.b, stream));
     unsigned long long bad = 0;
     DDSG_CUDA(cudaMemcpyAsync(&bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, stream));
@@ -359,7 +382,7 @@ int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t 
     if (!x_dev)
       DDSG_CUDA(cudaMemcpyAsync(const_cast<double*>(dx), x + off * d, cnt * d * 8,
                                 cudaMemcpyHostToDevice, st));
-    stats.launches += launch_eval(prog, exact, dx, cnt, off, dy, dbad, st);
+    stats.launches += launch_eval(prog, exact, dx, cnt, off, dy, dbad, st, ts.xt[b]);
     if (!y_dev)
       DDSG_CUDA(cudaMemcpyAsync(y + off * m, dy, cnt * m * 8, cudaMemcpyDeviceToHost, st));
   }

@@ -1,0 +1,847 @@
+// Slot-staged HDMR evaluation kernel (see fast_hdmr.cuh for the design).
+//
+// Reference semantics reproduced bit for bit in EXACT mode:
+//   VectorizedDdsg::evaluate (ddsg_eval.hpp:83-113): per active slot in slot
+//   order, row = interpolate(grid, x|u) (sparse_grid.hpp:111-128, nodes in
+//   canonical order, w = dim-ordered product with early exit, out += w*s as
+//   mul then add), row *= b; out[c] = pairwise_sum over rows
+//   (ddsg_eval.hpp:154-158).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+#include "basis.cuh"
+#include "fast_hdmr.cuh"
+
+namespace ddsg_b200 {
+
+namespace fast {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ---- tensor memory (per-thread scratch for deep pairwise-tree levels)
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_store8(uint32_t taddr, const double (&v)[kCols]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    r[2 * c] = __double2loint(v[c]);
+    r[2 * c + 1] = __double2hiint(v[c]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_load8(uint32_t taddr, double (&v)[kCols]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = __hiloint2double(static_cast<int>(r[2 * c + 1]), static_cast<int>(r[2 * c]));
+}
+
+template <int kExact>
+__device__ __forceinline__ void accum_row(double (&acc)[kCols], double w, const unsigned char* table,
+                                          int row) {
+  const double* sr = reinterpret_cast<const double*>(table + row * (kStride * 8));
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) {
+    const double v = sr[c];
+    acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w, v)) : __fma_rn(w, v, acc[c]);
+  }
+}
+
+// Branch-free 1-d factor at level l (static): candidate cell and basis value
+// (basis_at in basis.cuh, written with selects so the compiler can schedule
+// every subspace of a slot as one straight-line block).
+template <int l>
+__device__ __forceinline__ void factor(int mode, double x, uint32_t& kk, double& v) {
+  kk = cell_at(x, l);
+  if (l == 1 && mode == 1) {
+    v = 1.0;
+    return;
+  }
+  const double scale = static_cast<double>(1u << l);
+  const double t = __dmul_rn(x, scale);
+  const double hat = __dadd_rn(1.0, -fabs(__dadd_rn(t, -static_cast<double>(2u * kk + 1u))));
+  const double left = __dadd_rn(2.0, -t);
+  const double right = __dadd_rn(2.0, -__dadd_rn(scale, -t));
+  double r = hat;
+  if (l >= 2) {
+    r = (mode == 1 && kk == 0u) ? left : r;
+    r = (mode == 1 && kk == (1u << (l - 1)) - 1u) ? right : r;
+  }
+  v = r > 0.0 ? r : 0.0;
+}
+
+// Row of the candidate node of canonical subspace idx, or the slot's zero row
+// when the subspace is absent, the cell is absent, or the weight is 0 (the
+// reference skips w == 0 terms; adding w * 0 leaves the accumulator's bits
+// unchanged because it is never -0).
+__device__ __forceinline__ int term_row(const SlotHeader& H, const unsigned char* blk, int idx, int cell,
+                                        double w, bool all_full) {
+  const int base = H.sub_base[idx];
+  int row;
+  if (all_full) {
+    row = base + cell;
+  } else {
+    row = ((H.full >> idx) & 1u) ? base + cell : reinterpret_cast<const int16_t*>(blk + H.slab_off)[base + cell];
+  }
+  const bool ok = ((H.present >> idx) & 1u) && w != 0.0 && row >= 0;
+  return ok ? row : H.zero_row;
+}
+
+template <int kExact, int L>
+__device__ __forceinline__ void leaf_order1(const SlotHeader& H, const unsigned char* blk, double x,
+                                            double (&acc)[kCols], bool all_full) {
+  const unsigned char* table = blk + H.table_off;
+  const int mode = H.mode;
+  double w[L];
+  int row[L];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    uint32_t kk;
+    double v;
+    switch (l) {  // static level for the factor template
+#define DDSG_F(LV) \
+  case LV:         \
+    factor<LV>(mode, x, kk, v); \
+    break;
+      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4) DDSG_F(5) DDSG_F(6) DDSG_F(7) DDSG_F(8) DDSG_F(9) DDSG_F(10)
+#undef DDSG_F
+      default:
+        kk = 0;
+        v = 0.0;
+    }
+    row[l - 1] = term_row(H, blk, l - 1, static_cast<int>(kk), v, all_full);
+    w[l - 1] = v;
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) accum_row<kExact>(acc, w[l], table, row[l]);
+}
+
+template <int kExact, int L>
+__device__ __forceinline__ void leaf_order2(const SlotHeader& H, const unsigned char* blk, double x0,
+                                            double x1, double (&acc)[kCols], bool all_full) {
+  const unsigned char* table = blk + H.table_off;
+  const int mode = H.mode;
+  double v0[L], v1[L];
+  uint32_t k0[L], k1[L];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    switch (l) {
+#define DDSG_F(LV)                          \
+  case LV:                                  \
+    factor<LV>(mode, x0, k0[l - 1], v0[l - 1]); \
+    factor<LV>(mode, x1, k1[l - 1], v1[l - 1]); \
+    break;
+      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4) DDSG_F(5) DDSG_F(6)
+#undef DDSG_F
+      default:
+        break;
+    }
+  }
+  constexpr int kN = L * (L + 1) / 2;
+  double w[kN];
+  int row[kN];
+  int idx = 0;
+#pragma unroll
+  for (int s = 2; s <= L + 1; ++s) {
+#pragma unroll
+    for (int l1 = 1; l1 < s; ++l1) {
+      const int l2 = s - l1;
+      // reference: w = 1 * v0; if (w == 0) break; w *= v1  -> fl(v0 * v1) (0 if v0 == 0)
+      const double ww = __dmul_rn(v0[l1 - 1], v1[l2 - 1]);
+      const int cell = static_cast<int>((k0[l1 - 1] << (l2 - 1)) | k1[l2 - 1]);
+      row[idx] = term_row(H, blk, idx, cell, ww, all_full);
+      w[idx] = ww;
+      ++idx;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kN; ++i) accum_row<kExact>(acc, w[i], table, row[i]);
+}
+
+// ------------------------------------------------------------------ full grids
+// A full order-1 grid of max level L stores level l's 2^(l-1) cells from row
+// 2^(l-1) - 1; a full order-2 grid stores canonical subspace (l1, l2) from
+// row base2(l1, l2) (rows of all earlier subspaces in (|l|_1, l lex) order).
+__host__ __device__ constexpr int base1(int l) { return (1 << (l - 1)) - 1; }
+__host__ __device__ constexpr int base2(int l1, int l2) {
+  int b = 0;
+  for (int t = 2; t < l1 + l2; ++t) b += (t - 1) << (t - 2);
+  return b + ((l1 - 1) << (l1 + l2 - 2));
+}
+
+// Exact 1-d factor of the candidate node at static level l (basis.hpp:36-54):
+// with t = x 2^l, every kind is v = fl(A - |fl(t - B)|):
+//   hat (A, B) = (1, 2k+1); left edge (2, 0); right edge (2, 2^l);
+//   modified level 1 is the constant 1.  v >= 0 for the candidate cell, so the
+//   reference's max(v, 0) is the identity here.
+template <int l, int kMode>
+__device__ __forceinline__ void factor_full(double x, uint32_t& kk, double& v) {
+  constexpr uint32_t ncell = 1u << (l - 1);
+  const uint32_t k = static_cast<uint32_t>(__dmul_rn(x, static_cast<double>(ncell)));
+  kk = k < ncell ? k : ncell - 1u;
+  if (kMode == 1 && l == 1) {
+    v = 1.0;
+    return;
+  }
+  const double t = __dmul_rn(x, static_cast<double>(2u * ncell));
+  uint32_t B = 2u * kk + 1u;
+  double A = 1.0;
+  if (kMode == 1) {
+    const bool left = kk == 0u, right = kk == ncell - 1u;
+    B = left ? 0u : (right ? 2u * ncell : B);
+    A = (left || right) ? 2.0 : 1.0;
+  }
+  v = __dadd_rn(A, -fabs(__dadd_rn(t, -static_cast<double>(B))));
+}
+
+template <int kExact>
+__device__ __forceinline__ void fma_row(double (&acc)[kCols], double w, const double (&s)[kCols]) {
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) {
+    if (kExact)
+      acc[c] = __dadd_rn(acc[c], __dmul_rn(w, s[c]));
+    else
+      acc[c] = __fma_rn(w, s[c], acc[c]);
+  }
+}
+
+// LDS.64 gathers: lanes (points) read the same column of their rows.
+__device__ __forceinline__ void load_row(const unsigned char* table, int row, double (&s)[kCols]) {
+  const double* sr = reinterpret_cast<const double*>(table + row * (kStride * 8));
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) s[c] = sr[c];
+}
+
+// Full order-1 slot: levels 1..L, one term per level, loads one term ahead.
+// Terms with w == 0 are accumulated too: the surpluses are finite (checked on
+// the host), so w * s = +-0 and the accumulator (never -0) keeps its bits.
+template <int kExact, int kMode, int L>
+__device__ __forceinline__ void leaf_full1(const unsigned char* table, double x, double (&acc)[kCols]) {
+  double w[L];
+  int row[L];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    uint32_t kk;
+    switch (l) {
+#define DDSG_F(LV)                               \
+  case LV:                                       \
+    factor_full<LV, kMode>(x, kk, w[l - 1]);     \
+    break;
+      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4) DDSG_F(5) DDSG_F(6) DDSG_F(7) DDSG_F(8) DDSG_F(9) DDSG_F(10)
+#undef DDSG_F
+      default:
+        kk = 0;
+        w[l - 1] = 0.0;
+    }
+    row[l - 1] = base1(l) + static_cast<int>(kk);
+  }
+  double cur[kCols], nxt[kCols];
+  load_row(table, row[0], cur);
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    if (i + 1 < L) load_row(table, row[i + 1], nxt);
+    fma_row<kExact>(acc, w[i], cur);
+    if (i + 1 < L) {
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) cur[c] = nxt[c];
+    }
+  }
+}
+
+// Full order-2 slot with max level L per dim (level sum <= L + 1), canonical
+// order; w = fl(v0 * v1) (exact 1 * v when a factor is the modified level-1 constant).
+template <int kExact, int kMode, int L>
+__device__ __forceinline__ void leaf_full2(const unsigned char* table, double x0, double x1, double (&acc)[kCols]) {
+  double v0[L], v1[L];
+  uint32_t k0[L], k1[L];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    switch (l) {
+#define DDSG_F(LV)                                  \
+  case LV:                                          \
+    factor_full<LV, kMode>(x0, k0[l - 1], v0[l - 1]); \
+    factor_full<LV, kMode>(x1, k1[l - 1], v1[l - 1]); \
+    break;
+      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4) DDSG_F(5) DDSG_F(6)
+#undef DDSG_F
+      default:
+        break;
+    }
+  }
+  constexpr int kN = L * (L + 1) / 2;
+  // term i of the canonical sequence: (l1, l2) with l1 + l2 = s
+  auto term = [&](int i, double& w, int& row) {
+    int idx = 0;
+#pragma unroll
+    for (int s = 2; s <= L + 1; ++s)
+#pragma unroll
+      for (int l1 = 1; l1 < s; ++l1) {
+        const int l2 = s - l1;
+        if (idx == i) {
+          if (kMode == 1 && l1 == 1)
+            w = v1[l2 - 1];
+          else if (kMode == 1 && l2 == 1)
+            w = v0[l1 - 1];
+          else
+            w = __dmul_rn(v0[l1 - 1], v1[l2 - 1]);
+          row = base2(l1, l2) + static_cast<int>((k0[l1 - 1] << (l2 - 1)) | k1[l2 - 1]);
+        }
+        ++idx;
+      }
+  };
+  double w_cur, w_nxt = 0.0;
+  int r_cur, r_nxt = 0;
+  term(0, w_cur, r_cur);
+  double cur[kCols], nxt[kCols];
+  load_row(table, r_cur, cur);
+#pragma unroll
+  for (int i = 0; i < kN; ++i) {
+    if (i + 1 < kN) {
+      term(i + 1, w_nxt, r_nxt);
+      load_row(table, r_nxt, nxt);
+    }
+    fma_row<kExact>(acc, w_cur, cur);
+    if (i + 1 < kN) {
+      w_cur = w_nxt;
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) cur[c] = nxt[c];
+    }
+  }
+}
+
+template <int kExact>
+__device__ __forceinline__ void leaf_dispatch(const SlotHeader& H, const unsigned char* blk, double x0, double x1,
+                                              double (&acc)[kCols]) {
+  const unsigned char* table = blk + H.table_off;
+  if (H.fast_full) {
+    switch (H.mode * 64 + H.k * 16 + H.nlev) {
+#define DDSG_P1(MD, LV) \
+  case MD * 64 + 16 + LV: \
+    leaf_full1<kExact, MD, LV>(table, x0, acc); \
+    return;
+#define DDSG_P2(MD, LV) \
+  case MD * 64 + 32 + LV: \
+    leaf_full2<kExact, MD, LV>(table, x0, x1, acc); \
+    return;
+      DDSG_P1(0, 1) DDSG_P1(0, 2) DDSG_P1(0, 3) DDSG_P1(0, 4) DDSG_P1(0, 5) DDSG_P1(0, 6) DDSG_P1(0, 7)
+      DDSG_P1(0, 8) DDSG_P1(0, 9) DDSG_P1(0, 10)
+      DDSG_P1(1, 1) DDSG_P1(1, 2) DDSG_P1(1, 3) DDSG_P1(1, 4) DDSG_P1(1, 5) DDSG_P1(1, 6) DDSG_P1(1, 7)
+      DDSG_P1(1, 8) DDSG_P1(1, 9) DDSG_P1(1, 10)
+      DDSG_P2(0, 1) DDSG_P2(0, 2) DDSG_P2(0, 3) DDSG_P2(0, 4) DDSG_P2(0, 5) DDSG_P2(0, 6)
+      DDSG_P2(1, 1) DDSG_P2(1, 2) DDSG_P2(1, 3) DDSG_P2(1, 4) DDSG_P2(1, 5) DDSG_P2(1, 6)
+#undef DDSG_P1
+#undef DDSG_P2
+      default:
+        break;
+    }
+  }
+  // general path: adaptive / partial grids or non-finite surpluses
+  const bool all_full = H.full == H.present;
+  switch (H.k * 16 + H.nlev) {
+#define DDSG_L1(LV) \
+  case 16 + LV:     \
+    leaf_order1<kExact, LV>(H, blk, x0, acc, all_full); \
+    break;
+#define DDSG_L2(LV) \
+  case 32 + LV:     \
+    leaf_order2<kExact, LV>(H, blk, x0, x1, acc, all_full); \
+    break;
+    DDSG_L1(1) DDSG_L1(2) DDSG_L1(3) DDSG_L1(4) DDSG_L1(5) DDSG_L1(6) DDSG_L1(7) DDSG_L1(8) DDSG_L1(9) DDSG_L1(10)
+    DDSG_L2(1) DDSG_L2(2) DDSG_L2(3) DDSG_L2(4) DDSG_L2(5) DDSG_L2(6)
+#undef DDSG_L1
+#undef DDSG_L2
+    default:
+      break;
+  }
+}
+
+// Pending level i of the pairwise tree for this thread (levels >= 1).
+struct TreeStore {
+  double2* smem;   // [kSmemLevels][kCols/2][kPoints]
+  uint32_t tbase;  // TMEM address of this warp's lane quarter / column block
+  int tid;
+  __device__ __forceinline__ void load(int i, double (&v)[kCols]) const {
+    if (i <= kSmemLevels) {
+      const double2* L = smem + (static_cast<int64_t>(i - 1) * (kCols / 2)) * kPoints + tid;
+#pragma unroll
+      for (int q = 0; q < kCols / 2; ++q) {
+        const double2 x = L[q * kPoints];
+        v[2 * q] = x.x;
+        v[2 * q + 1] = x.y;
+      }
+    } else {
+      tmem_load8(tbase + 16u * static_cast<uint32_t>(i - kSmemLevels - 1), v);
+    }
+  }
+  __device__ __forceinline__ void store(int i, const double (&v)[kCols]) const {
+    if (i <= kSmemLevels) {
+      double2* L = smem + (static_cast<int64_t>(i - 1) * (kCols / 2)) * kPoints + tid;
+#pragma unroll
+      for (int q = 0; q < kCols / 2; ++q) L[q * kPoints] = make_double2(v[2 * q], v[2 * q + 1]);
+    } else {
+      tmem_store8(tbase + 16u * static_cast<uint32_t>(i - kSmemLevels - 1), v);
+    }
+  }
+};
+
+template <int kExact>
+__global__ void __launch_bounds__(kPoints, 1)
+    fast_hdmr_kernel(const unsigned char* __restrict__ blocks, const int64_t* __restrict__ block_off,
+                     const int32_t* __restrict__ block_len, const int16_t* __restrict__ slot_dims,
+                     int n_active, int n_cb, int levels, const double* __restrict__ xt, int64_t n, int m,
+                     double* __restrict__ y, int64_t stage_bytes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 64);
+  unsigned char* stages = smem + 128;
+  double2* deep = reinterpret_cast<double2*>(stages + kStages * stage_bytes);
+  const int smem_levels = levels - 1 < kSmemLevels ? (levels - 1 > 0 ? levels - 1 : 0) : kSmemLevels;
+  int16_t* sdims = reinterpret_cast<int16_t*>(deep + static_cast<int64_t>(smem_levels) * (kCols / 2) * kPoints);
+  const bool use_tmem = levels - 1 > kSmemLevels;
+
+  const int tile = blockIdx.x / n_cb;
+  const int cb = blockIdx.x - tile * n_cb;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int64_t p = static_cast<int64_t>(tile) * kPoints + tid;
+  const bool valid = p < n;
+  const int64_t pc = valid ? p : n - 1;
+  const int64_t* offs = block_off + static_cast<int64_t>(cb) * n_active;
+  const int32_t* lens = block_len + static_cast<int64_t>(cb) * n_active;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kStages && s < n_active; ++s) {
+      mbar_expect_tx(&bars[s], static_cast<uint32_t>(lens[s]));
+      bulk_g2s(stages + s * stage_bytes, blocks + offs[s], static_cast<uint32_t>(lens[s]), &bars[s]);
+    }
+  }
+  if (use_tmem && warp == 0) tmem_alloc(tmem_slot, 512);
+  for (int i = tid; i < 2 * n_active; i += kPoints) sdims[i] = slot_dims[i];
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  TreeStore store{deep, 0u, tid};
+  if (use_tmem)
+    store.tbase = *tmem_slot + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(128 * (warp >> 2));
+
+  double xc0 = xt[static_cast<int64_t>(sdims[0]) * n + pc];
+  double xc1 = xt[static_cast<int64_t>(sdims[1]) * n + pc];
+  double L0[kCols];
+  double root[kCols];
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) root[c] = 0.0;
+
+  for (int a = 0; a < n_active; ++a) {
+    const int st = a % kStages;
+    mbar_wait(&bars[st], static_cast<uint32_t>((a / kStages) & 1));
+    const unsigned char* blk = stages + st * stage_bytes;
+    const SlotHeader& H = *reinterpret_cast<const SlotHeader*>(blk);
+    double acc[kCols];
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+    const int k = H.k;
+    const double x0 = xc0, x1 = xc1;
+    if (a + 1 < n_active) {  // prefetch the next slot's coordinates
+      xc0 = xt[static_cast<int64_t>(sdims[2 * (a + 1)]) * n + pc];
+      xc1 = xt[static_cast<int64_t>(sdims[2 * (a + 1) + 1]) * n + pc];
+    }
+    if (k == 0) {
+      const double* r0 = reinterpret_cast<const double*>(blk + H.table_off);
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) acc[c] = r0[c];
+    } else {
+      leaf_dispatch<kExact>(H, blk, x0, x1, acc);
+      if (H.b_kind == 0) {
+        const double b = H.b;
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) acc[c] = __dmul_rn(acc[c], b);
+      } else if (H.b_kind == 2) {
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) acc[c] = -acc[c];
+      }
+    }
+    // pairwise tree (perfect-tree embedding): merge with the pending left
+    // siblings at levels s.. while the position bit is set, then park.
+    const int t = H.tree_t;
+    int i = H.tree_s;
+    if (i == 0 && i < levels) {
+      if (t & 1) {
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) acc[c] = __dadd_rn(L0[c], acc[c]);
+        i = 1;
+      } else {
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) L0[c] = acc[c];
+        i = -1;  // parked
+      }
+    }
+    if (i >= 0) {
+      while (i < levels && ((t >> i) & 1)) {
+        double v[kCols];
+        store.load(i, v);
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) acc[c] = __dadd_rn(v[c], acc[c]);
+        ++i;
+      }
+      if (i < levels) {
+        store.store(i, acc);
+      } else {
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) root[c] = acc[c];
+      }
+    }
+    __syncthreads();  // every warp is done with stage st
+    if (tid == 0 && a + kStages < n_active) {
+      fence_proxy_async();
+      const int nxt = a + kStages;
+      mbar_expect_tx(&bars[st], static_cast<uint32_t>(lens[nxt]));
+      bulk_g2s(stages + st * stage_bytes, blocks + offs[nxt], static_cast<uint32_t>(lens[nxt]), &bars[st]);
+    }
+  }
+  if (valid) {
+    const int c0 = cb * kCols;
+    double* yp = y + p * m + c0;
+#pragma unroll
+    for (int c = 0; c < kCols; ++c)
+      if (c0 + c < m) yp[c] = root[c];
+  }
+  if (use_tmem) {
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tmem_slot, 512);
+  }
+}
+
+// x [n][d] row-major -> xt [d][n]; flags the lowest point outside [0,1]^d.
+__global__ void transpose_check_kernel(const double* __restrict__ x, int64_t n, int d, int64_t base,
+                                       double* __restrict__ xt, unsigned long long* bad) {
+  __shared__ double tile[32][33];
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t p = p0 + r;
+    const int j = j0 + tx;
+    double v = 0.5;
+    if (p < n && j < d) {
+      v = x[p * d + j];
+      if (!(v >= 0.0 && v <= 1.0)) atomicMin(bad, static_cast<unsigned long long>(base + p));
+    }
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int j = j0 + r;
+    const int64_t p = p0 + tx;
+    if (p < n && j < d) xt[static_cast<int64_t>(j) * n + p] = tile[tx][r];
+  }
+}
+
+}  // namespace fast
+
+using namespace fast;
+
+FastHdmr::~FastHdmr() {
+  if (blocks_) cudaFree(blocks_);
+  if (block_off_) cudaFree(block_off_);
+  if (block_len_) cudaFree(block_len_);
+  if (slot_dims_) cudaFree(slot_dims_);
+}
+
+static int canon_index(int k, int l1, int l2) {
+  if (k == 1) return l1 - 1;
+  const int s = l1 + l2;
+  return (s - 2) * (s - 1) / 2 + (l1 - 1);
+}
+
+bool FastHdmr::build(const HostProgram& hp) {
+  usable_ = false;
+  if (hp.plain) {
+    why_ = "plain grid";
+    return false;
+  }
+  const int na = static_cast<int>(hp.slot_k.size());
+  if (na == 0) {
+    why_ = "no active slot";
+    return false;
+  }
+  int levels = 0;
+  while ((int64_t{1} << levels) < na) ++levels;
+  if (levels > kMaxLevels) {
+    why_ = "too many active slots";
+    return false;
+  }
+  d_ = hp.d;
+  m_ = hp.m;
+  n_active_ = na;
+  levels_ = levels;
+  n_cb_ = (hp.m + kCols - 1) / kCols;
+
+  // perfect-tree embedding of pairwise_sum (ddsg_eval.hpp:154-158)
+  std::vector<int32_t> tree_t, tree_s;
+  {
+    struct Rec {
+      static void go(int64_t lo, int64_t cnt, int depth, int D, std::vector<int32_t>& t,
+                     std::vector<int32_t>& s) {
+        if (cnt == 1) {
+          t.push_back(static_cast<int32_t>(lo));
+          s.push_back(D - depth);
+          return;
+        }
+        const int64_t h = cnt / 2;
+        go(lo, h, depth + 1, D, t, s);
+        go(lo + (int64_t{1} << (D - depth - 1)), cnt - h, depth + 1, D, t, s);
+      }
+    };
+    Rec::go(0, na, 0, levels, tree_t, tree_s);
+  }
+
+  // per-slot headers (column-block independent part)
+  struct SlotPlan {
+    SlotHeader h;
+    int64_t row_begin = 0, rows = 0;
+    std::vector<int16_t> slab;
+    int64_t bytes = 0;
+  };
+  std::vector<SlotPlan> plans(na);
+  std::vector<int16_t> dims16;
+  int64_t max_bytes = 0;
+  for (int a = 0; a < na; ++a) {
+    SlotPlan& P = plans[a];
+    std::memset(&P.h, 0, sizeof(SlotHeader));
+    SlotHeader& H = P.h;
+    const int k = hp.slot_k[a];
+    if (k > 2) {
+      why_ = "slot order > 2";
+      return false;
+    }
+    H.k = k;
+    H.mode = hp.slot_mode[a];
+    H.tree_t = tree_t[a];
+    H.tree_s = tree_s[a];
+    H.table_off = sizeof(SlotHeader);
+    dims16.push_back(0);
+    dims16.push_back(0);
+    if (k == 0) {
+      H.b_kind = 1;  // b * f_anchor is folded into the staged row
+      P.rows = 1;
+    } else {
+      const double b = hp.slot_b[a];
+      H.b = b;
+      H.b_kind = b == 1.0 ? 1 : (b == -1.0 ? 2 : 0);
+      H.d0 = hp.slot_dims[hp.slot_dims_off[a]];
+      H.d1 = k == 2 ? hp.slot_dims[hp.slot_dims_off[a] + 1] : 0;
+      if (H.d0 > 32767 || H.d1 > 32767) {
+        why_ = "point dimension above 32767";
+        return false;
+      }
+      dims16[2 * a] = static_cast<int16_t>(H.d0);
+      dims16[2 * a + 1] = static_cast<int16_t>(H.d1);
+      P.row_begin = hp.slot_row_begin[a];
+      P.rows = hp.slot_row_end[a] - hp.slot_row_begin[a];
+      if (P.rows > 32767) {
+        why_ = "slot has more than 32767 nodes";
+        return false;
+      }
+      int nlev = 0;
+      for (int s = hp.slot_sub_begin[a]; s < hp.slot_sub_end[a]; ++s) {
+        const uint8_t* lv = &hp.levels[hp.sub_lv_off[s]];
+        const int l1 = lv[0], l2 = k == 2 ? lv[1] : 0;
+        nlev = std::max(nlev, std::max(l1, l2));
+        if ((k == 1 && l1 > kL1) || (k == 2 && (l1 > kL2 || l2 > kL2))) {
+          why_ = "slot level above the kernel's static maximum";
+          return false;
+        }
+        const int idx = canon_index(k, l1, l2);
+        const int64_t cells = int64_t{1} << (l1 - 1 + (k == 2 ? l2 - 1 : 0));
+        H.present |= 1u << idx;
+        const int32_t* slab = &hp.slab[hp.sub_slab_off[s]];
+        if (hp.sub_nodes[s] == cells) {
+          H.full |= 1u << idx;
+          H.sub_base[idx] = static_cast<int16_t>(slab[0] - P.row_begin);
+        } else {
+          if (P.slab.size() + cells > 32767) {
+            why_ = "slab too large";
+            return false;
+          }
+          H.sub_base[idx] = static_cast<int16_t>(P.slab.size());
+          for (int64_t c = 0; c < cells; ++c)
+            P.slab.push_back(slab[c] < 0 ? int16_t{-1} : static_cast<int16_t>(slab[c] - P.row_begin));
+        }
+      }
+      H.nlev = nlev;
+      {
+        // fast_full: the grid is the full grid of its max level (every canonical
+        // subspace present and complete) and all its surpluses are finite
+        const int nsub = k == 1 ? nlev : nlev * (nlev + 1) / 2;
+        const uint32_t all = nsub >= 32 ? 0xffffffffu : ((1u << nsub) - 1u);
+        bool finite = true;
+        for (int64_t r = 0; r < P.rows && finite; ++r)
+          for (int c = 0; c < m_; ++c)
+            if (!std::isfinite(hp.surplus[(P.row_begin + r) * m_ + c])) {
+              finite = false;
+              break;
+            }
+        H.fast_full = (H.present == all && H.full == all && finite) ? 1 : 0;
+      }
+      H.zero_row = static_cast<int32_t>(P.rows);  // all-zero row appended to the table
+      P.rows += 1;
+    }
+    const int64_t table_bytes = P.rows * kStride * 8;
+    H.slab_off = static_cast<int32_t>(sizeof(SlotHeader) + table_bytes);
+    P.bytes = (sizeof(SlotHeader) + table_bytes + P.slab.size() * 2 + 15) / 16 * 16;
+    max_bytes = std::max(max_bytes, P.bytes);
+  }
+  block_bytes_ = (max_bytes + 127) / 128 * 128;
+  const int64_t deep_bytes = std::min(std::max(0, levels - 1), kSmemLevels) * int64_t{kCols} * kPoints * 8;
+  const int64_t smem = 128 + kStages * block_bytes_ + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
+  if (smem > 227 * 1024) {
+    why_ = "shared-memory footprint too large";
+    return false;
+  }
+
+  // column-blocked staged blocks
+  std::vector<int64_t> off(static_cast<size_t>(n_cb_) * na);
+  std::vector<int32_t> len(static_cast<size_t>(n_cb_) * na);
+  int64_t total = 0;
+  for (int cb = 0; cb < n_cb_; ++cb)
+    for (int a = 0; a < na; ++a) {
+      off[static_cast<size_t>(cb) * na + a] = total;
+      len[static_cast<size_t>(cb) * na + a] = static_cast<int32_t>(plans[a].bytes);
+      total += plans[a].bytes;
+    }
+  std::vector<unsigned char> host(total, 0);
+  for (int cb = 0; cb < n_cb_; ++cb)
+    for (int a = 0; a < na; ++a) {
+      const SlotPlan& P = plans[a];
+      unsigned char* blk = host.data() + off[static_cast<size_t>(cb) * na + a];
+      std::memcpy(blk, &P.h, sizeof(SlotHeader));
+      double* table = reinterpret_cast<double*>(blk + sizeof(SlotHeader));
+      for (int64_t r = 0; r < P.rows; ++r)
+        for (int c = 0; c < kCols; ++c) {
+          const int col = cb * kCols + c;
+          double v = 0.0;
+          const bool zero_row = hp.slot_k[a] != 0 && r == P.rows - 1;
+          if (col < m_ && !zero_row) {
+            if (hp.slot_k[a] == 0)
+              v = hp.slot_b[a] * hp.f_anchor[col];  // row = b * f_anchor (ddsg_eval.hpp:94-96)
+            else
+              v = hp.surplus[(P.row_begin + r) * m_ + col];
+          }
+          table[r * kStride + c] = v;
+        }
+      if (!P.slab.empty())
+        std::memcpy(blk + P.h.slab_off, P.slab.data(), P.slab.size() * 2);
+    }
+  DDSG_CUDA(cudaMalloc(&blocks_, total));
+  DDSG_CUDA(cudaMemcpy(blocks_, host.data(), total, cudaMemcpyHostToDevice));
+  DDSG_CUDA(cudaMalloc(&block_off_, off.size() * sizeof(int64_t)));
+  DDSG_CUDA(cudaMemcpy(block_off_, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  DDSG_CUDA(cudaMalloc(&slot_dims_, dims16.size() * sizeof(int16_t)));
+  DDSG_CUDA(cudaMemcpy(slot_dims_, dims16.data(), dims16.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+  DDSG_CUDA(cudaMalloc(&block_len_, len.size() * sizeof(int32_t)));
+  DDSG_CUDA(cudaMemcpy(block_len_, len.data(), len.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  DDSG_CUDA(cudaFuncSetAttribute(fast_hdmr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  DDSG_CUDA(cudaFuncSetAttribute(fast_hdmr_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  usable_ = true;
+  why_.clear();
+  return true;
+}
+
+int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, double* y,
+                         unsigned long long* bad, double* xt, cudaStream_t st) const {
+  // dim-major copy of the points so each slot's coordinate read is coalesced
+  dim3 tgrid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((d_ + 31) / 32));
+  transpose_check_kernel<<<tgrid, dim3(32, 8), 0, st>>>(x, n, d_, base, xt, bad);
+  DDSG_CUDA(cudaGetLastError());
+  const int64_t tiles = (n + kPoints - 1) / kPoints;
+  const int64_t deep_bytes = std::min(std::max(0, levels_ - 1), kSmemLevels) * int64_t{kCols} * kPoints * 8;
+  const size_t smem = 128 + kStages * block_bytes_ + deep_bytes + (4 * static_cast<size_t>(n_active_) + 15) / 16 * 16;
+  const dim3 grid(static_cast<unsigned>(tiles * n_cb_));
+  if (exact)
+    fast_hdmr_kernel<1><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
+                                                     block_len_, slot_dims_, n_active_, n_cb_, levels_, xt, n, m_, y,
+                                                     block_bytes_);
+  else
+    fast_hdmr_kernel<0><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
+                                                     block_len_, slot_dims_, n_active_, n_cb_, levels_, xt, n, m_, y,
+                                                     block_bytes_);
+  DDSG_CUDA(cudaGetLastError());
+  return 2;
+}
+
+}  // namespace ddsg_b200

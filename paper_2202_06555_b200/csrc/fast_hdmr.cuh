@@ -1,0 +1,102 @@
+// Slot-staged HDMR evaluation kernel for low-order cut-HDMR programs
+// (every active slot of order <= 2): the B200 hot path for BASELINE configs 4-5.
+//
+// Design:
+//  * One CTA = kWarps x 32 points (lanes = points) x one block of kCols output
+//    columns.  Every active slot's surplus block for that column block is a
+//    contiguous global region [header | rows x kStride doubles | slab], moved
+//    into a shared-memory ring by one TMA bulk copy (cp.async.bulk + mbarrier).
+//  * Each thread walks the slot's subspaces in canonical order (statically
+//    unrolled for order-1 levels <= kL1 and order-2 levels <= kL2), computes the
+//    candidate cell and the bit-exact weight, and gathers s[row][c] with
+//    LDS.128: lanes of a warp read the same column of (few) rows, so the
+//    shared-memory broadcast path delivers 256 B/clk/SM.
+//  * Leaf (slot) values enter the reference's pairwise tree through a
+//    perfect-binary-tree embedding (leaf a at position t_a spanning 2^s_a):
+//    pending level 0 lives in registers, levels 1..kSmemLevels in shared
+//    memory, deeper (rarely touched) levels in tensor memory: each thread
+//    owns TMEM lane (its lane in the warp's lane quarter) and 16 columns per
+//    level (tcgen05.st/ld 32x32b.x16).
+//  * EXACT mode: DMUL then DADD per term (bit-identical to the reference);
+//    FAST mode: one DFMA per term.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "device.cuh"
+
+namespace ddsg_b200 {
+
+namespace fast {
+
+constexpr int kCols = 8;                 // output columns per thread / CTA column block
+constexpr int kStride = kCols + 1;       // doubles per staged row: odd, so 16 consecutive rows
+                                         // fall on 16 distinct 8-byte bank pairs (LDS.64 conflict-free)
+constexpr int kWarps = 16;
+constexpr int kPoints = kWarps * 32;     // points per CTA
+constexpr int kL1 = 10;                  // max level of order-1 slots
+constexpr int kL2 = 6;                   // max level (per dim) of order-2 slots
+constexpr int kSub2 = kL2 * (kL2 + 1) / 2;  // canonical subspaces of a full order-2 grid
+constexpr int kMaxSub = kSub2 > kL1 ? kSub2 : kL1;
+constexpr int kSmemLevels = 5;           // tree levels 1..5 in shared memory (level 0 in registers)
+constexpr int kTmemLevels = 8;           // levels 6..13 in tensor memory (128 columns per warp)
+constexpr int kMaxLevels = 1 + kSmemLevels + kTmemLevels;  // 2^14 active slots
+constexpr int kStages = 3;
+
+// Per-slot header at the front of every staged block (16-B aligned, 160 B).
+struct SlotHeader {
+  int32_t k;          // slot order 0..2
+  int32_t mode;       // boundary mode
+  int32_t nlev;       // order 1: max level; order 2: max level per dim
+  int32_t d0, d1;     // point dims of the slot
+  int32_t tree_t;     // leaf position in the perfect-tree embedding
+  int32_t tree_s;     // leaf span exponent
+  int32_t b_kind;     // 0: multiply by b, 1: b == 1, 2: b == -1
+  double b;
+  uint32_t present;   // bit i: canonical subspace i has nodes
+  uint32_t full;      // bit i: canonical subspace i has all its cells
+  int32_t table_off;  // byte offset of the row table within the block
+  int32_t slab_off;   // byte offset of the int16 slab within the block
+  int32_t zero_row;   // index of the all-zero row (target of skipped terms)
+  int32_t fast_full;  // 1: full grid of level nlev with finite surpluses (static row layout)
+  int16_t sub_base[kMaxSub];  // first row (full) or slab index (partial) per subspace
+  int16_t pad_[(160 - 64 - 2 * kMaxSub) / 2];
+};
+static_assert(sizeof(SlotHeader) == 160, "header layout");
+
+}  // namespace fast
+
+// Host-built, device-resident program of the fast kernel.
+class FastHdmr {
+ public:
+  FastHdmr() = default;
+  FastHdmr(const FastHdmr&) = delete;
+  FastHdmr& operator=(const FastHdmr&) = delete;
+  ~FastHdmr();
+
+  // Builds the staged blocks when the program qualifies; returns usable().
+  bool build(const HostProgram& hp);
+  bool usable() const { return usable_; }
+  // Launches the evaluation of n device points (x row-major [n][d]); xt is a
+  // device scratch of at least n*d doubles (the dim-major copy of x).
+  // Returns the number of kernel launches.
+  int64_t launch(int exact, const double* x, int64_t n, int64_t base, double* y, unsigned long long* bad,
+                 double* xt, cudaStream_t st) const;
+  int dim() const { return d_; }
+  std::string why_not() const { return why_; }
+
+ private:
+  bool usable_ = false;
+  std::string why_;
+  int d_ = 0, m_ = 0, n_cb_ = 0, n_active_ = 0, levels_ = 0;
+  int64_t block_bytes_ = 0;  // stage size (max block), multiple of 128
+  void* blocks_ = nullptr;   // [n_cb][n_active] blocks of block_bytes_ each (offsets below)
+  int64_t* block_off_ = nullptr;  // device: [n_cb * n_active] byte offsets
+  int32_t* block_len_ = nullptr;  // device: [n_cb * n_active] byte lengths
+  int16_t* slot_dims_ = nullptr;  // device: [n_active][2] point dims per slot
+};
+
+}  // namespace ddsg_b200

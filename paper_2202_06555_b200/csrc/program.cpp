@@ -46,6 +46,8 @@ void HostProgram::add_empty_slot(int32_t id, double b) {
   const int32_t s = static_cast<int32_t>(sub_lv_off.size());
   slot_sub_begin.push_back(s);
   slot_sub_end.push_back(s);
+  slot_row_begin.push_back(rows);
+  slot_row_end.push_back(rows);
 }
 
 void HostProgram::add_grid_slot(int32_t id, const HostGrid& g, const std::vector<int32_t>& dims,
@@ -76,7 +78,9 @@ void HostProgram::add_grid_slot(int32_t id, const HostGrid& g, const std::vector
                    g.surplus.begin() + static_cast<int64_t>(st + 1) * m);
     row_stored.push_back(st);
   }
+  slot_row_begin.push_back(rows);
   rows += L.rows;
+  slot_row_end.push_back(rows);
   if (rows > (int64_t{1} << 31) - 1) fail(DDSG_INVALID_ARGUMENT, "program: more than 2^31 rows");
 }
 

@@ -30,6 +30,7 @@ struct HostProgram {
   std::vector<int32_t> slot_dims;
   std::vector<double> slot_b;
   std::vector<int32_t> slot_sub_begin, slot_sub_end;  // subspace range
+  std::vector<int64_t> slot_row_begin, slot_row_end;  // surplus row range
   std::vector<uint8_t> merges;
 
   // subspaces (all slots concatenated)
