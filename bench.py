@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py — batched DDSG interpolant evaluation on B200 (the hot path of
+arXiv 2202.06555, BASELINE.json).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 5] [--points n] [--mode exact|fast]
+
+A step evaluates the HDMR interpolant of the chosen BASELINE config (default:
+config 5, d=300, m=151, 519 active slots, 115,198 nodes) at n points:
+value = points x outputs per second over the whole job (strong scaling:
+n = 2^22 points split across the ranks, grids replicated).  Inputs are
+device-resident for `value`; `e2e` repeats the measurement through the same
+public API with pinned host buffers (H2D of x and D2H of y inside every step).
+One JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "interpolant evals/sec (points x outputs)"
+UNIT = "evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--points", type=int, default=0, help="total points (default: the config's n)")
+    ap.add_argument("--mode", choices=["exact", "fast"], default="exact")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sms, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm = float(parts[1])
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            if sm > 0:
+                sms.append(sm)
+            for nm, v in zip(names, parts[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        if not sms:
+            return None
+        sms.sort()
+        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ----------------------------------------------------------- CPU baseline
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def build_reference_hdmr(cfg, parts, use_reference_build: bool):
+    """The reference's VectorizedDdsg over the config's component grids.
+
+    use_reference_build: build every cut grid with the reference's own
+    SparseGridFunction::build (sparse_grid.hpp:84) from the same C target;
+    otherwise inject our grids through from_nodes (same bits)."""
+    import ctypes as C
+
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    from paper_2202_06555_b200 import _native as N
+
+    grids = []
+    wl = N.workloads()
+    anchor = np.full(cfg.d, 0.5)
+    for u, b, g in parts.slots:
+        if g is None:
+            grids.append(None)
+            continue
+        if use_reference_build:
+            dims = np.array(u, dtype=np.int32)
+            cut = wl.wl_cut_new(N.wl_fn(cfg.target), None, cfg.d, cfg.m, len(u), dims.ctypes.data, anchor.ctypes.data)
+            lvl = cfg.level_1d if len(u) == 1 else cfg.level_2d
+            eps = cfg.eps_1d if len(u) == 1 else cfg.eps_2d
+            rc, rg = O.ref_build(len(u), cfg.m, cfg.mode, lvl, eps, N.wl_fn("wl_cut_eval"), C.c_void_p(cut))
+            wl.wl_cut_free(C.c_void_p(cut))
+            if rc != 0:
+                raise RuntimeError(f"reference build failed: {rg}")
+            grids.append(rg)
+        else:
+            keys, sur = g.nodes()
+            grids.append(O.ref_from_nodes(len(u), cfg.m, g.boundary_mode, g.max_level, g.eps_gamma, keys, sur))
+    return O.RefHdmr(cfg.d, cfg.m, parts.f_anchor, [(u, b) for u, b, _ in parts.slots], grids)
+
+
+def time_reference(ref_hdmr, cfg, x_sample, target_s: float, workers: int):
+    """VectorizedDdsg::evaluate_batch (ddsg_eval.hpp:130-139) on a growing
+    prefix of the sample until one call takes >= target_s."""
+    n = min(256, x_sample.shape[0])
+    while True:
+        t0 = time.perf_counter()
+        rc, _ = ref_hdmr.eval(x_sample[:n], workers=workers, flat=False)
+        dt = time.perf_counter() - t0
+        if rc != 0:
+            raise RuntimeError("reference evaluate_batch failed")
+        if dt >= target_s or n >= x_sample.shape[0]:
+            return n, dt
+        n = min(x_sample.shape[0], max(n * 2, int(n * target_s / max(dt, 1e-3) * 1.1)))
+
+
+def reference_variants():
+    """The generic Release build and the x86-64-v3 build of oracle/_ref."""
+    out = [ROOT / "oracle" / "_ref" / "libddsg_ref.so"]
+    v3 = ROOT / "oracle" / "_ref" / "libddsg_ref_v3.so"
+    try:
+        flags = open("/proc/cpuinfo").read()
+        if v3.exists() and " avx2 " in flags and " fma " in flags:
+            out.append(v3)
+    except Exception:
+        pass
+    return [p for p in out if p.exists()]
+
+
+def cpu_baseline(cfg, parts, target_s: float, use_reference_build: bool):
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    from paper_2202_06555_b200.ddsg import uniform_points
+
+    workers = cpu_cores()
+    x = uniform_points(cfg.seed, 1 << 16, cfg.d)
+    best = None
+    for lib in reference_variants():
+        O._ref = None
+        O.REF_PATH = lib
+        ref = build_reference_hdmr(cfg, parts, use_reference_build)
+        time_reference(ref, cfg, x, 0.5, workers)  # warm
+        n, dt = time_reference(ref, cfg, x, target_s, workers)
+        rate = n * cfg.m / dt
+        if best is None or rate > best[0]:
+            best = (rate, n, dt, lib.name)
+        del ref
+    if best is None:
+        return None
+    rate, n, dt, name = best
+    return {"value": rate, "unit": UNIT, "cores": workers, "kind": "reference",
+            "sample": f"first {n} seeded points of {cfg.name} through the reference's "
+                      f"VectorizedDdsg::evaluate_batch(workers={workers}) ({name}, {dt:.1f} s)"}
+
+
+# -------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank, dist):
+    import numpy as np
+    import torch
+
+    from paper_2202_06555_b200 import workloads as W
+    from paper_2202_06555_b200.ddsg import EXACT, FAST, last_eval_stats, measure_fp64_peak
+
+    torch.cuda.set_device(local_rank)
+    cfg = W.CONFIGS[args.config]
+    n_total = args.points or cfg.n_points
+    n_local = n_total // world + (1 if rank < n_total % world else 0)
+    t0 = time.time()
+    if cfg.kind == "hdmr":
+        obj, parts = W.build_hdmr(cfg)
+        evaluate = obj.evaluate_batch
+    else:
+        obj, parts = W.build_grid(cfg), None
+        evaluate = obj.interpolate
+    obj.set_eval_mode(EXACT if args.mode == "exact" else FAST)
+    build_s = time.time() - t0
+
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(cfg.seed * 1000 + rank)
+    x = torch.rand((n_local, cfg.d), dtype=torch.float64, device="cuda", generator=gen)
+    y = torch.empty((n_local, cfg.m), dtype=torch.float64, device="cuda")
+
+    # exact algorithmic work: NNZ_total = sum over points of (slot, node) pairs with w != 0
+    nnz, _ = obj.support(x)
+    nnz_total = int(np.asarray(nnz).sum())
+    dfma, dmma = measure_fp64_peak()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        evaluate(x, out=y)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    main_ms = 0.0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        evaluate(x, out=y)
+        l, _, mk = last_eval_stats()
+        launches += l
+        main_ms += mk
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([elapsed_ms, main_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms, main_ms_max = float(t[0]), float(t[1])
+    ms_per_step = elapsed_ms / args.steps
+    value = n_total * cfg.m / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (the slot kernel): algorithmic FLOPs = 2 m NNZ
+    kernel_ms = main_ms / args.steps
+    flops = 2.0 * cfg.m * nnz_total
+    achieved = flops / (kernel_ms / 1e3) / 1e12
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": dfma, "unit": "TFLOP/s",
+                "frac": achieved / dfma, "traffic": None,
+                "peak_source": "DFMA issue-rate microbenchmark measured live on this GPU "
+                               "(MEASURED_PEAKS.json has no FP64 entry); DMMA peak %.1f TFLOP/s" % dmma,
+                "kernel_ms": kernel_ms, "kernel_share": kernel_ms / ms_per_step,
+                "flops_per_step": flops, "nnz_per_point": nnz_total / n_local,
+                "exact_mode_cap_frac": 0.5}
+
+    # e2e through the same API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        try:
+            xh = torch.empty((n_local, cfg.d), dtype=torch.float64, pin_memory=True)
+            xh.copy_(x)
+            yh = torch.empty((n_local, cfg.m), dtype=torch.float64, pin_memory=True)
+            evaluate(xh, out=yh)
+            barrier()
+            t1 = time.perf_counter()
+            for _ in range(args.steps):
+                evaluate(xh, out=yh)
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device="cuda")
+            if dist is not None:
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            e2e_s = float(dt[0]) / args.steps
+            if not torch.equal(yh, y.cpu()):
+                raise RuntimeError("e2e result differs from the device-resident result")
+            e2e = {"value": n_total * cfg.m / e2e_s, "unit": UNIT,
+                   "h2d_bytes_per_step": n_total * cfg.d * 8, "d2h_bytes_per_step": n_total * cfg.m * 8,
+                   "s_per_step": e2e_s, "timing": "wall clock around the synchronous C-ABI call"}
+            del xh, yh
+        except RuntimeError as e:  # e.g. pinned allocation failure
+            e2e = {"value": None, "unit": UNIT, "error": str(e)[:200]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.kind == "hdmr":
+        try:
+            cpu = cpu_baseline(cfg, parts, args.cpu_seconds, use_reference_build=False)
+        except Exception as e:
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "d": cfg.d, "m": cfg.m, "points_total": n_total,
+                       "points_per_gpu": n_local, "active_slots": obj.info()["n_active"] if parts else 1,
+                       "nodes": obj.info()["n_nodes"] if parts else obj.size(),
+                       "eval_mode": args.mode, "parallelism": f"points sharded over {world} GPU(s), grids replicated",
+                       "l2": f"inputs {n_local * cfg.d * 8 / 1e9:.1f} GB per GPU, larger than L2 (no flush needed)",
+                       "build_s": round(build_s, 1)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2202_06555_b200 import workloads as W
+    from paper_2202_06555_b200.ddsg import uniform_points
+
+    cfg = W.CONFIGS[args.config]
+    if cfg.kind != "hdmr":
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for the HDMR configs"}))
+        return
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+
+    if not reference_variants():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libddsg_ref.so was not built"}))
+        return
+    parts = W.build_hdmr_parts(cfg)
+    workers = cpu_cores()
+    lib = reference_variants()[-1]
+    O._ref = None
+    O.REF_PATH = lib
+    ref = build_reference_hdmr(cfg, parts, use_reference_build=True)
+    x = uniform_points(cfg.seed, 1 << 14, cfg.d)
+    # size one step to ~ (a few minutes / steps) of CPU work
+    n, dt = time_reference(ref, cfg, x, 2.0, workers)
+    for _ in range(args.warmup):
+        ref.eval(x[:n], workers=workers, flat=False)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ref.eval(x[:n], workers=workers, flat=False)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = n * cfg.m / dt
+    sample = (f"{n} seeded points of {cfg.name} per step through VectorizedDdsg::evaluate_batch"
+              f"(workers={workers}); grids built by the reference's SparseGridFunction::build ({lib.name})")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "d": cfg.d, "m": cfg.m, "points_per_step": n},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    try:
+        run_ours(args, rank, world, local_rank, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

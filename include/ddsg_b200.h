@@ -166,9 +166,18 @@ ddsg_status ddsg_grid_set_eval_mode(ddsg_grid_t* g, int eval_mode);
 ddsg_status ddsg_hdmr_set_eval_mode(ddsg_hdmr_t* h, int eval_mode);
 
 /* Kernel statistics of the last evaluation on this thread: number of kernel
- * launches issued and the device time (ms) of the evaluation kernels alone,
- * measured with CUDA events on the launching stream. */
-ddsg_status ddsg_last_eval_stats(int64_t* launches, double* kernel_ms);
+ * launches issued, the device time (ms) of the whole evaluation (device-
+ * resident calls; 0 for host-buffer calls) and of the dominant evaluation
+ * kernel alone, measured with CUDA events on the launching stream(s). */
+ddsg_status ddsg_last_eval_stats(int64_t* launches, double* kernel_ms, double* main_kernel_ms);
+
+/* 1 if the HDMR evaluates on the slot-staged kernel (all active slots of
+ * order <= 2 within its static level limits), 0 for the generic kernel. */
+ddsg_status ddsg_hdmr_kernel_path(const ddsg_hdmr_t* h, int* fast_path);
+
+/* Measures the FP64 DFMA and DMMA (mma.sync f64) peaks of the current device
+ * in TFLOP/s (roofline denominators; microbenchmark, ~0.1 s). */
+ddsg_status ddsg_measure_fp64_peak(double* dfma_tflops, double* dmma_tflops);
 
 /* Support statistics (test / roofline helper, computed on the device):
  * nnz[i] = number of (slot, node) pairs with w != 0 at x[i]; hash[i] = an

@@ -55,7 +55,9 @@ SIGNATURES = {
     "ddsg_hdmr_quadrature": (_i, [_p, _p]),
     "ddsg_grid_set_eval_mode": (_i, [_p, _i]),
     "ddsg_hdmr_set_eval_mode": (_i, [_p, _i]),
-    "ddsg_last_eval_stats": (_i, [C.POINTER(_i64), C.POINTER(_d)]),
+    "ddsg_last_eval_stats": (_i, [C.POINTER(_i64), C.POINTER(_d), C.POINTER(_d)]),
+    "ddsg_hdmr_kernel_path": (_i, [_p, C.POINTER(_i)]),
+    "ddsg_measure_fp64_peak": (_i, [C.POINTER(_d), C.POINTER(_d)]),
     "ddsg_hdmr_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
     "ddsg_grid_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
     "ddsg_uniform_points": (None, [C.c_uint64, _i64, _i, _p]),

@@ -432,11 +432,20 @@ ddsg_status ddsg_hdmr_set_eval_mode(ddsg_hdmr_t* h, int eval_mode) {
   });
 }
 
-ddsg_status ddsg_last_eval_stats(int64_t* launches, double* kernel_ms) {
+ddsg_status ddsg_last_eval_stats(int64_t* launches, double* kernel_ms, double* main_kernel_ms) {
   const EvalStats& s = last_stats();
   if (launches) *launches = s.launches;
   if (kernel_ms) *kernel_ms = s.kernel_ms;
+  if (main_kernel_ms) *main_kernel_ms = s.main_ms;
   return DDSG_OK;
+}
+
+ddsg_status ddsg_hdmr_kernel_path(const ddsg_hdmr_t* h, int* fast_path) {
+  return guarded([&] {
+    if (!h || !fast_path) fail(DDSG_INVALID_ARGUMENT, "hdmr_kernel_path: null argument");
+    auto* self = const_cast<ddsg_hdmr_t*>(h);
+    *fast_path = self->dev.get(h->prog).fast() != nullptr ? 1 : 0;
+  });
 }
 
 void ddsg_uniform_points(uint64_t seed, int64_t n, int dim, double* out) {

@@ -74,9 +74,19 @@ class DeviceProgram {
 // Per-call statistics (thread-local, see ddsg_last_eval_stats).
 struct EvalStats {
   int64_t launches = 0;
-  double kernel_ms = 0.0;
+  double kernel_ms = 0.0;  // device time of the whole evaluation (device-resident calls)
+  double main_ms = 0.0;    // device time of the dominant (slot) kernel launches
 };
 EvalStats& last_stats();
+
+// Interval timer for the dominant kernel: begin()/end() record CUDA events on
+// the launching stream; collect() sums the intervals after a synchronize.
+struct KernelTimer {
+  void begin(cudaStream_t st);
+  void end(cudaStream_t st);
+  double collect();  // ms; resets
+};
+KernelTimer& kernel_timer();
 
 // Evaluates the program over n points.  x/y may be host or device memory.
 // Returns the lowest out-of-domain point index or -1.

@@ -29,6 +29,41 @@ EvalStats& last_stats() {
   return s;
 }
 
+namespace {
+struct TimerState {
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  ~TimerState() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      DDSG_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+thread_local TimerState g_timer;
+}  // namespace
+
+void KernelTimer::begin(cudaStream_t st) { DDSG_CUDA(cudaEventRecord(g_timer.next(), st)); }
+void KernelTimer::end(cudaStream_t st) { DDSG_CUDA(cudaEventRecord(g_timer.next(), st)); }
+double KernelTimer::collect() {
+  double total = 0.0;
+  for (size_t i = 0; i + 1 < g_timer.used; i += 2) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, g_timer.pool[i], g_timer.pool[i + 1]) == cudaSuccess) total += ms;
+  }
+  g_timer.used = 0;
+  return total;
+}
+KernelTimer& kernel_timer() {
+  static thread_local KernelTimer t;
+  return t;
+}
+
 DeviceProgram::~DeviceProgram() {
   for (void* p : allocs_) cudaFree(p);
   delete fast_;
@@ -333,7 +368,9 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
   const int64_t threads = n * chunks;
   const int block = 128;
   const int64_t grid = (threads + block - 1) / block;
+  kernel_timer().begin(st);
   eval_generic_kernel<kCols><<<static_cast<unsigned>(grid), block, 0, st>>>(P, dx, n, base, dy, dbad);
+  kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());
   return 1;
 }
@@ -342,6 +379,7 @@ int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t 
                  cudaStream_t stream) {
   EvalStats& stats = last_stats();
   stats = EvalStats{};
+  kernel_timer().collect();  // drop stale intervals
   if (n <= 0) return -1;
   ThreadScratch& ts = scratch();
   const int d = prog.host().d, m = prog.host().m;
@@ -360,6 +398,7 @@ int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t 
     float ms = 0.f;
     DDSG_CUDA(cudaEventElapsedTime(&ms, ev.a, ev.b));
     stats.kernel_ms = ms;
+    stats.main_ms = kernel_timer().collect();
     return bad == ULLONG_MAX ? -1 : static_cast<int64_t>(bad);
   }
   // Host (or mixed) buffers: pipeline H2D -> kernel -> D2H over three streams.
@@ -387,6 +426,7 @@ int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t 
       DDSG_CUDA(cudaMemcpyAsync(y + off * m, dy, cnt * m * 8, cudaMemcpyDeviceToHost, st));
   }
   for (auto& s : ts.streams) DDSG_CUDA(cudaStreamSynchronize(s));
+  stats.main_ms = kernel_timer().collect();
   unsigned long long bad = 0;
   DDSG_CUDA(cudaMemcpy(&bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost));
   return bad == ULLONG_MAX ? -1 : static_cast<int64_t>(bad);

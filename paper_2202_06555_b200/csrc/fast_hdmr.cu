@@ -45,6 +45,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -304,16 +308,12 @@ __device__ __forceinline__ void leaf_full1(const unsigned char* table, double x,
     }
     row[l - 1] = base1(l) + static_cast<int>(kk);
   }
-  double cur[kCols], nxt[kCols];
-  load_row(table, row[0], cur);
+  double buf[2][kCols];  // static ping-pong: term i+1 loads while term i accumulates
+  load_row(table, row[0], buf[0]);
 #pragma unroll
   for (int i = 0; i < L; ++i) {
-    if (i + 1 < L) load_row(table, row[i + 1], nxt);
-    fma_row<kExact>(acc, w[i], cur);
-    if (i + 1 < L) {
-#pragma unroll
-      for (int c = 0; c < kCols; ++c) cur[c] = nxt[c];
-    }
+    if (i + 1 < L) load_row(table, row[i + 1], buf[(i + 1) & 1]);
+    fma_row<kExact>(acc, w[i], buf[i & 1]);
   }
 }
 
@@ -358,23 +358,18 @@ __device__ __forceinline__ void leaf_full2(const unsigned char* table, double x0
         ++idx;
       }
   };
-  double w_cur, w_nxt = 0.0;
-  int r_cur, r_nxt = 0;
-  term(0, w_cur, r_cur);
-  double cur[kCols], nxt[kCols];
-  load_row(table, r_cur, cur);
+  double wb[2];
+  int rb[2];
+  term(0, wb[0], rb[0]);
+  double buf[2][kCols];  // static ping-pong
+  load_row(table, rb[0], buf[0]);
 #pragma unroll
   for (int i = 0; i < kN; ++i) {
     if (i + 1 < kN) {
-      term(i + 1, w_nxt, r_nxt);
-      load_row(table, r_nxt, nxt);
+      term(i + 1, wb[(i + 1) & 1], rb[(i + 1) & 1]);
+      load_row(table, rb[(i + 1) & 1], buf[(i + 1) & 1]);
     }
-    fma_row<kExact>(acc, w_cur, cur);
-    if (i + 1 < kN) {
-      w_cur = w_nxt;
-#pragma unroll
-      for (int c = 0; c < kCols; ++c) cur[c] = nxt[c];
-    }
+    fma_row<kExact>(acc, wb[i & 1], buf[i & 1]);
   }
 }
 
@@ -460,9 +455,10 @@ __global__ void __launch_bounds__(kPoints, 1)
                      int n_active, int n_cb, int levels, const double* __restrict__ xt, int64_t n, int m,
                      double* __restrict__ y, int64_t stage_bytes) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 64);
-  unsigned char* stages = smem + 128;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [kStages] full, [kStages] empty
+  uint64_t* empty = bars + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kStages);
+  unsigned char* stages = smem + kHeaderBytes;
   double2* deep = reinterpret_cast<double2*>(stages + kStages * stage_bytes);
   const int smem_levels = levels - 1 < kSmemLevels ? (levels - 1 > 0 ? levels - 1 : 0) : kSmemLevels;
   int16_t* sdims = reinterpret_cast<int16_t*>(deep + static_cast<int64_t>(smem_levels) * (kCols / 2) * kPoints);
@@ -479,7 +475,10 @@ __global__ void __launch_bounds__(kPoints, 1)
   const int32_t* lens = block_len + static_cast<int64_t>(cb) * n_active;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bars[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
     fence_mbar_init();
     for (int s = 0; s < kStages && s < n_active; ++s) {
       mbar_expect_tx(&bars[s], static_cast<uint32_t>(lens[s]));
@@ -504,6 +503,14 @@ __global__ void __launch_bounds__(kPoints, 1)
 
   for (int a = 0; a < n_active; ++a) {
     const int st = a % kStages;
+    if (tid == 0 && a >= 1 && a - 1 + kStages < n_active) {
+      // refill the stage released by slot a-1 (all warps arrived on its empty barrier)
+      const int b = a - 1, sb = b % kStages, nxt = b + kStages;
+      mbar_wait(&empty[sb], static_cast<uint32_t>((b / kStages) & 1));
+      fence_proxy_async();
+      mbar_expect_tx(&bars[sb], static_cast<uint32_t>(lens[nxt]));
+      bulk_g2s(stages + sb * stage_bytes, blocks + offs[nxt], static_cast<uint32_t>(lens[nxt]), &bars[sb]);
+    }
     mbar_wait(&bars[st], static_cast<uint32_t>((a / kStages) & 1));
     const unsigned char* blk = stages + st * stage_bytes;
     const SlotHeader& H = *reinterpret_cast<const SlotHeader*>(blk);
@@ -561,13 +568,8 @@ __global__ void __launch_bounds__(kPoints, 1)
         for (int c = 0; c < kCols; ++c) root[c] = acc[c];
       }
     }
-    __syncthreads();  // every warp is done with stage st
-    if (tid == 0 && a + kStages < n_active) {
-      fence_proxy_async();
-      const int nxt = a + kStages;
-      mbar_expect_tx(&bars[st], static_cast<uint32_t>(lens[nxt]));
-      bulk_g2s(stages + st * stage_bytes, blocks + offs[nxt], static_cast<uint32_t>(lens[nxt]), &bars[st]);
-    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
   }
   if (valid) {
     const int c0 = cb * kCols;
@@ -766,7 +768,7 @@ bool FastHdmr::build(const HostProgram& hp) {
   }
   block_bytes_ = (max_bytes + 127) / 128 * 128;
   const int64_t deep_bytes = std::min(std::max(0, levels - 1), kSmemLevels) * int64_t{kCols} * kPoints * 8;
-  const int64_t smem = 128 + kStages * block_bytes_ + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
+  const int64_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
   if (smem > 227 * 1024) {
     why_ = "shared-memory footprint too large";
     return false;
@@ -830,8 +832,9 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   DDSG_CUDA(cudaGetLastError());
   const int64_t tiles = (n + kPoints - 1) / kPoints;
   const int64_t deep_bytes = std::min(std::max(0, levels_ - 1), kSmemLevels) * int64_t{kCols} * kPoints * 8;
-  const size_t smem = 128 + kStages * block_bytes_ + deep_bytes + (4 * static_cast<size_t>(n_active_) + 15) / 16 * 16;
+  const size_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * static_cast<size_t>(n_active_) + 15) / 16 * 16;
   const dim3 grid(static_cast<unsigned>(tiles * n_cb_));
+  kernel_timer().begin(st);
   if (exact)
     fast_hdmr_kernel<1><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
                                                      block_len_, slot_dims_, n_active_, n_cb_, levels_, xt, n, m_, y,
@@ -840,6 +843,7 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
     fast_hdmr_kernel<0><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
                                                      block_len_, slot_dims_, n_active_, n_cb_, levels_, xt, n, m_, y,
                                                      block_bytes_);
+  kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());
   return 2;
 }

@@ -41,10 +41,11 @@ constexpr int kL1 = 10;                  // max level of order-1 slots
 constexpr int kL2 = 6;                   // max level (per dim) of order-2 slots
 constexpr int kSub2 = kL2 * (kL2 + 1) / 2;  // canonical subspaces of a full order-2 grid
 constexpr int kMaxSub = kSub2 > kL1 ? kSub2 : kL1;
-constexpr int kSmemLevels = 5;           // tree levels 1..5 in shared memory (level 0 in registers)
-constexpr int kTmemLevels = 8;           // levels 6..13 in tensor memory (128 columns per warp)
+constexpr int kSmemLevels = 4;           // tree levels 1..4 in shared memory (level 0 in registers)
+constexpr int kTmemLevels = 8;           // levels 5..12 in tensor memory (128 columns per warp)
 constexpr int kMaxLevels = 1 + kSmemLevels + kTmemLevels;  // 2^14 active slots
-constexpr int kStages = 3;
+constexpr int kStages = 4;
+constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
 
 // Per-slot header at the front of every staged block (16-B aligned, 160 B).
 struct SlotHeader {

@@ -141,7 +141,7 @@ class SparseGridFunction:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and N is not None and N.lib is not None:
             N.lib.ddsg_grid_destroy(h)
             self._h = C.c_void_p(0)
 
@@ -260,7 +260,7 @@ class VectorizedDdsg:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and N is not None and N.lib is not None:
             N.lib.ddsg_hdmr_destroy(h)
             self._h = C.c_void_p(0)
 
@@ -294,11 +294,24 @@ class VectorizedDdsg:
         _check(N.lib.ddsg_hdmr_quadrature(self._h, _ptr(q)))
         return q
 
+    def uses_slot_kernel(self) -> bool:
+        v = C.c_int()
+        _check(N.lib.ddsg_hdmr_kernel_path(self._h, C.byref(v)))
+        return bool(v.value)
+
 
 def last_eval_stats():
-    launches, ms = C.c_int64(), C.c_double()
-    N.lib.ddsg_last_eval_stats(C.byref(launches), C.byref(ms))
-    return launches.value, ms.value
+    """(kernel launches, device ms of the whole evaluation, device ms of the dominant kernel)."""
+    launches, ms, main = C.c_int64(), C.c_double(), C.c_double()
+    N.lib.ddsg_last_eval_stats(C.byref(launches), C.byref(ms), C.byref(main))
+    return launches.value, ms.value, main.value
+
+
+def measure_fp64_peak():
+    """(DFMA TFLOP/s, DMMA TFLOP/s) measured on the current device."""
+    a, b = C.c_double(), C.c_double()
+    _check(N.lib.ddsg_measure_fp64_peak(C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 def uniform_points(seed: int, n: int, dim: int) -> np.ndarray:

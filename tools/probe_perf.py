@@ -21,7 +21,7 @@ def run(cid, n, modes=(EXACT,)):
         ms = []
         for _ in range(3):
             ev(x, out=y)
-            ms.append(last_eval_stats()[1])
+            ms.append(last_eval_stats()[2])
         kms = min(ms)
         flops = 2.0 * cfg.m * nnz.mean() * n
         print(f"config{cid} n={n} mode={'exact' if mode==EXACT else 'fast'} build={tb:.1f}s kernel={kms:.2f}ms "
