@@ -188,7 +188,7 @@ def cpu_baseline(cfg, parts, target_s: float, use_reference_build: bool):
     from paper_2202_06555_b200.ddsg import uniform_points
 
     workers = cpu_cores()
-    x = uniform_points(cfg.seed, 1 << 16, cfg.d)
+    x = uniform_points(cfg.seed, 1 << 18, cfg.d)
     best = None
     for lib in reference_variants():
         O._ref = None

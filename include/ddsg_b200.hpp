@@ -1,0 +1,405 @@
+// ddsg_b200.hpp — C++20 drop-in for the reference's interpolation API, over
+// the C-ABI of include/ddsg_b200.h (header-only; link libddsg_b200.so).
+//
+// Class and member names, argument meaning and exception types mirror
+// /root/reference/proj/include/ddsg/ (cited per member), so a caller of the
+// reference switches by replacing `ddsg::` with `ddsg_b200::`.  Evaluation
+// runs on the GPU; every batched call is one C-ABI call.
+//
+//   SparseGridFunction   sparse_grid.hpp:72-351
+//   DdsgFunction         hdmr.hpp:195-356   (from_parts only; decompose is out of scope)
+//   VectorizedDdsg       ddsg_eval.hpp:28-165
+//   build_error          sparse_grid.hpp:40-48
+//   task_error           runtime.hpp:71-92
+#pragma once
+
+#include <cstdint>
+#include <exception>
+#include <functional>
+#include <map>
+#include <memory>
+#include <new>
+#include <set>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ddsg_b200.h"
+
+namespace ddsg_b200 {
+
+using HeapKey = std::uint32_t;            // grid_index.hpp:19
+using NodeKey = std::vector<HeapKey>;     // grid_index.hpp:22
+
+enum class BoundaryMode { zero_boundary, modified_linear };  // basis.hpp:22
+enum class SurplusNorm { inf, l2 };                          // sparse_grid.hpp:53
+
+class build_error : public std::runtime_error {  // sparse_grid.hpp:40-48
+ public:
+  build_error(std::string msg, std::vector<double> point)
+      : std::runtime_error(std::move(msg)), point_(std::move(point)) {}
+  const std::vector<double>& point() const { return point_; }
+
+ private:
+  std::vector<double> point_;
+};
+
+class task_error : public std::runtime_error {  // runtime.hpp:71-92
+ public:
+  task_error(std::size_t task_id, std::exception_ptr cause, const std::string& what)
+      : std::runtime_error(what), task_id_(task_id), cause_(std::move(cause)) {}
+  std::size_t task_id() const { return task_id_; }
+  [[noreturn]] void rethrow_cause() const { std::rethrow_exception(cause_); }
+
+ private:
+  std::size_t task_id_;
+  std::exception_ptr cause_;
+};
+
+namespace detail {
+
+// Status -> the reference's exception types.  `batch` selects the
+// evaluate_batch convention (domain errors wrapped in task_error with the
+// lowest offending point, runtime.hpp:133-136).
+[[noreturn]] inline void raise(ddsg_status s, bool batch = false, int64_t bad = -1) {
+  const std::string msg = ddsg_last_error();
+  switch (s) {
+    case DDSG_INVALID_ARGUMENT:
+      throw std::invalid_argument(msg);
+    case DDSG_DOMAIN_ERROR:
+      if (batch && bad >= 0)
+        throw task_error(static_cast<std::size_t>(bad), std::make_exception_ptr(std::domain_error(msg)), msg);
+      throw std::domain_error(msg);
+    case DDSG_BUILD_ERROR: {
+      std::vector<double> p(64);
+      const int n = ddsg_last_build_point(p.data(), 64);
+      p.resize(static_cast<std::size_t>(n < 64 ? n : 64));
+      throw build_error(msg, std::move(p));
+    }
+    case DDSG_OUT_OF_RANGE:
+      throw std::out_of_range(msg);
+    case DDSG_OUT_OF_MEMORY:
+      throw std::bad_alloc();
+    default:
+      throw std::runtime_error("ddsg_b200: " + msg);
+  }
+}
+
+inline void check(ddsg_status s) {
+  if (s != DDSG_OK) raise(s);
+}
+
+}  // namespace detail
+
+struct GridNode {  // sparse_grid.hpp:55-59
+  NodeKey key;
+  std::vector<double> surplus;
+  bool refined = false;
+};
+
+struct SgBuildOptions {  // sparse_grid.hpp:61-67
+  int max_level = 1;
+  double eps_gamma = 0.0;
+  BoundaryMode mode = BoundaryMode::zero_boundary;
+  SurplusNorm norm = SurplusNorm::inf;
+  unsigned workers = 1;  // accepted for source compatibility; evaluation runs on the GPU
+};
+
+using GridEvaluator = std::function<void(std::span<const double>, std::span<double>)>;  // sparse_grid.hpp:70
+
+class SparseGridFunction {
+ public:
+  SparseGridFunction() = default;
+
+  int dim() const { return dim_; }
+  int out_dim() const { return out_dim_; }
+  int max_level() const { return max_level_; }
+  double eps_gamma() const { return eps_gamma_; }
+  BoundaryMode boundary_mode() const { return mode_; }
+  std::size_t size() const {
+    int64_t n = 0;
+    detail::check(ddsg_grid_info(h_.get(), nullptr, nullptr, nullptr, nullptr, nullptr, &n));
+    return static_cast<std::size_t>(n);
+  }
+
+  // sparse_grid.hpp:84-108
+  static SparseGridFunction build(const GridEvaluator& f, int dim, int out_dim, const SgBuildOptions& opt) {
+    struct Ctx {
+      const GridEvaluator* f;
+      int dim, m;
+      std::exception_ptr err;
+    } ctx{&f, dim, out_dim, nullptr};
+    auto tramp = [](const double* xs, int64_t count, double* out, void* c) -> int {
+      auto* cx = static_cast<Ctx*>(c);
+      try {
+        for (int64_t i = 0; i < count; ++i)
+          (*cx->f)(std::span<const double>(xs + i * cx->dim, static_cast<std::size_t>(cx->dim)),
+                   std::span<double>(out + i * cx->m, static_cast<std::size_t>(cx->m)));
+        return 0;
+      } catch (...) {
+        cx->err = std::current_exception();
+        return 1;
+      }
+    };
+    ddsg_grid_t* g = nullptr;
+    const ddsg_status s =
+        ddsg_grid_build(dim, out_dim, static_cast<int>(opt.mode), opt.max_level, opt.eps_gamma,
+                        static_cast<int>(opt.norm), tramp, &ctx, &g);
+    if (ctx.err) std::rethrow_exception(ctx.err);  // the evaluator's own error type (sparse_grid.hpp:259-262)
+    detail::check(s);
+    return SparseGridFunction(g);
+  }
+
+  // sparse_grid.hpp:160-179
+  static SparseGridFunction from_nodes(int dim, int out_dim, int max_level, double eps_gamma, BoundaryMode mode,
+                                       const std::vector<GridNode>& nodes) {
+    std::vector<uint32_t> keys;
+    std::vector<double> sur;
+    keys.reserve(nodes.size() * static_cast<std::size_t>(dim > 0 ? dim : 0));
+    sur.reserve(nodes.size() * static_cast<std::size_t>(out_dim > 0 ? out_dim : 0));
+    for (const auto& n : nodes) {
+      if (n.key.size() != static_cast<std::size_t>(dim))
+        throw std::invalid_argument("sparse grid: node key dimension mismatch");
+      if (n.surplus.size() != static_cast<std::size_t>(out_dim))
+        throw std::invalid_argument("sparse grid: node surplus length mismatch");
+      keys.insert(keys.end(), n.key.begin(), n.key.end());
+      sur.insert(sur.end(), n.surplus.begin(), n.surplus.end());
+    }
+    ddsg_grid_t* g = nullptr;
+    detail::check(ddsg_grid_create(dim, out_dim, static_cast<int>(mode), max_level, eps_gamma,
+                                   static_cast<int64_t>(nodes.size()), keys.data(), sur.data(), &g));
+    return SparseGridFunction(g);
+  }
+
+  // sparse_grid.hpp:81 (stored order)
+  std::vector<GridNode> nodes() const {
+    const std::size_t n = size();
+    std::vector<uint32_t> keys(n * static_cast<std::size_t>(dim_));
+    std::vector<double> sur(n * static_cast<std::size_t>(out_dim_));
+    detail::check(ddsg_grid_nodes(h_.get(), keys.data(), sur.data()));
+    std::vector<GridNode> out(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      out[i].key.assign(keys.begin() + static_cast<std::ptrdiff_t>(i * dim_),
+                        keys.begin() + static_cast<std::ptrdiff_t>((i + 1) * dim_));
+      out[i].surplus.assign(sur.begin() + static_cast<std::ptrdiff_t>(i * out_dim_),
+                            sur.begin() + static_cast<std::ptrdiff_t>((i + 1) * out_dim_));
+    }
+    return out;
+  }
+
+  // sparse_grid.hpp:111-128 (one point; std::domain_error outside [0,1]^dim)
+  void interpolate(std::span<const double> x, std::span<double> out) const {
+    if (x.size() != static_cast<std::size_t>(dim_))
+      throw std::invalid_argument("sparse grid: query dimension mismatch");
+    if (out.size() != static_cast<std::size_t>(out_dim_))
+      throw std::invalid_argument("sparse grid: output length mismatch");
+    int64_t bad = -1;
+    const ddsg_status s = ddsg_eval_grid(h_.get(), x.data(), 1, out.data(), &bad, nullptr);
+    if (s != DDSG_OK) detail::raise(s);
+  }
+  std::vector<double> interpolate(std::span<const double> x) const {  // sparse_grid.hpp:130-134
+    std::vector<double> out(static_cast<std::size_t>(out_dim_));
+    interpolate(x, out);
+    return out;
+  }
+  // Batched form (x [n][dim], y [n][m]; host or device pointers); failures
+  // follow for_each_index: task_error with the lowest failing point.
+  void interpolate_batch(const double* x, int64_t n, double* y, void* stream = nullptr) const {
+    int64_t bad = -1;
+    const ddsg_status s = ddsg_eval_grid(h_.get(), x, n, y, &bad, stream);
+    if (s != DDSG_OK) detail::raise(s, true, bad);
+  }
+
+  std::vector<double> quadrature() const {  // sparse_grid.hpp:138-149
+    std::vector<double> q(static_cast<std::size_t>(out_dim_));
+    detail::check(ddsg_grid_quadrature(h_.get(), q.data()));
+    return q;
+  }
+
+  bool contains(const NodeKey& key) const {
+    for (const auto& n : nodes())
+      if (n.key == key) return true;
+    return false;
+  }
+
+  const ddsg_grid_t* handle() const { return h_.get(); }
+
+ private:
+  struct Del {
+    void operator()(ddsg_grid_t* g) const { ddsg_grid_destroy(g); }
+  };
+  std::shared_ptr<ddsg_grid_t> h_;
+  int dim_ = 0, out_dim_ = 0, max_level_ = 0;
+  double eps_gamma_ = 0.0;
+  BoundaryMode mode_ = BoundaryMode::zero_boundary;
+
+  explicit SparseGridFunction(ddsg_grid_t* g) : h_(g, Del{}) {
+    int dim = 0, m = 0, mode = 0, lvl = 0;
+    double eps = 0.0;
+    int64_t n = 0;
+    detail::check(ddsg_grid_info(g, &dim, &m, &mode, &lvl, &eps, &n));
+    dim_ = dim;
+    out_dim_ = m;
+    max_level_ = lvl;
+    eps_gamma_ = eps;
+    mode_ = mode == DDSG_MODIFIED_LINEAR ? BoundaryMode::modified_linear : BoundaryMode::zero_boundary;
+  }
+};
+
+struct ComponentIndex {  // component_index.hpp:16-54
+  std::vector<int> dims;
+  std::size_t order() const { return dims.size(); }
+  bool empty() const { return dims.empty(); }
+  bool operator==(const ComponentIndex& o) const { return dims == o.dims; }
+  bool operator<(const ComponentIndex& o) const {
+    if (dims.size() != o.dims.size()) return dims.size() < o.dims.size();
+    return dims < o.dims;
+  }
+};
+
+struct AnchorPoint {  // hdmr.hpp:27-30
+  std::vector<double> coords;
+  std::vector<double> f_anchor;
+};
+
+struct DdsgOptions {  // hdmr.hpp:166-175 (only the fields evaluation uses matter here)
+  int k_max = 1;
+  double eps_rho = 0.0, eps_eta = 0.0;
+  int max_level = 1;
+  double eps_gamma = 0.0;
+  BoundaryMode mode = BoundaryMode::modified_linear;
+  bool exact_cuts = false;
+  unsigned workers = 1;
+};
+
+class DdsgFunction {  // hdmr.hpp:195-356
+ public:
+  int dim() const { return dim_; }
+  int out_dim() const { return out_dim_; }
+  const AnchorPoint& anchor() const { return anchor_; }
+  const std::map<ComponentIndex, SparseGridFunction>& accepted() const { return accepted_; }
+  const std::map<ComponentIndex, int>& coeff_b() const { return coeff_b_; }
+
+  // hdmr.hpp:307-325
+  static DdsgFunction from_parts(int dim, int out_dim, DdsgOptions opt, AnchorPoint anchor,
+                                 std::map<ComponentIndex, SparseGridFunction> accepted,
+                                 std::set<ComponentIndex> rejected, std::map<ComponentIndex, int> coeff_b,
+                                 std::map<ComponentIndex, std::vector<double>> cut_quadratures) {
+    (void)rejected;
+    (void)cut_quadratures;  // recomputed from the grids (bit-identical to decompose's)
+    DdsgFunction f;
+    f.dim_ = dim;
+    f.out_dim_ = out_dim;
+    f.opt_ = opt;
+    f.opt_.exact_cuts = false;
+    f.anchor_ = std::move(anchor);
+    f.accepted_ = std::move(accepted);
+    f.coeff_b_ = std::move(coeff_b);
+    return f;
+  }
+
+ private:
+  int dim_ = 0, out_dim_ = 0;
+  DdsgOptions opt_;
+  AnchorPoint anchor_;
+  std::map<ComponentIndex, SparseGridFunction> accepted_;
+  std::map<ComponentIndex, int> coeff_b_;
+};
+
+class VectorizedDdsg {  // ddsg_eval.hpp:28-165
+ public:
+  VectorizedDdsg() = default;
+
+  // ddsg_eval.hpp:40-74 — same validation (null source, non-accepted
+  // coefficient, missing subsets) through ddsg_hdmr_create.
+  static VectorizedDdsg compile(std::shared_ptr<const DdsgFunction> source) {
+    if (!source) throw std::invalid_argument("vectorized ddsg: null source");
+    VectorizedDdsg v;
+    v.source_ = source;
+    v.dim_ = source->dim();
+    v.out_dim_ = source->out_dim();
+    std::vector<int32_t> order, dims, b;
+    std::vector<const ddsg_grid_t*> grids;
+    for (const auto& [u, bu] : source->coeff_b()) {
+      order.push_back(static_cast<int32_t>(u.order()));
+      for (int dd : u.dims) dims.push_back(dd);
+      b.push_back(bu);
+      if (u.empty()) {
+        grids.push_back(nullptr);
+      } else {
+        auto it = source->accepted().find(u);
+        if (it == source->accepted().end())
+          throw std::invalid_argument("vectorized ddsg: coefficient for a non-accepted index");
+        grids.push_back(it->second.handle());
+      }
+    }
+    ddsg_hdmr_t* h = nullptr;
+    detail::check(ddsg_hdmr_create(v.dim_, v.out_dim_, source->anchor().f_anchor.data(),
+                                   static_cast<int>(order.size()), order.data(), dims.data(), b.data(),
+                                   grids.data(), &h));
+    v.h_.reset(h, [](ddsg_hdmr_t* p) { ddsg_hdmr_destroy(p); });
+    return v;
+  }
+
+  int dim() const { return dim_; }
+  int out_dim() const { return out_dim_; }
+  const DdsgFunction& source() const { return *source_; }
+
+  // ddsg_eval.hpp:83-113 (one point)
+  void evaluate(std::span<const double> x, std::span<double> out) const {
+    if (x.size() != static_cast<std::size_t>(dim_)) throw std::invalid_argument("ddsg: query dimension mismatch");
+    if (out.size() != static_cast<std::size_t>(out_dim_))
+      throw std::invalid_argument("vectorized ddsg: output length mismatch");
+    int64_t bad = -1;
+    const ddsg_status s = ddsg_eval_hdmr(h_.get(), x.data(), 1, out.data(), &bad, nullptr);
+    if (s != DDSG_OK) detail::raise(s);
+  }
+  std::vector<double> evaluate(std::span<const double> x) const {
+    std::vector<double> out(static_cast<std::size_t>(out_dim_));
+    evaluate(x, out);
+    return out;
+  }
+
+  // ddsg_eval.hpp:130-139: elementwise equal to evaluate, independent of
+  // `workers`; a bad point raises task_error with the lowest index.
+  std::vector<std::vector<double>> evaluate_batch(const std::vector<std::vector<double>>& xs,
+                                                  unsigned workers = 1) const {
+    (void)workers;
+    const std::size_t n = xs.size();
+    std::vector<double> flat(n * static_cast<std::size_t>(dim_));
+    for (std::size_t i = 0; i < n; ++i) {
+      if (xs[i].size() != static_cast<std::size_t>(dim_))
+        throw task_error(i, std::make_exception_ptr(std::invalid_argument("ddsg: query dimension mismatch")),
+                         "task " + std::to_string(i) + " failed: ddsg: query dimension mismatch");
+      std::copy(xs[i].begin(), xs[i].end(), flat.begin() + static_cast<std::ptrdiff_t>(i * dim_));
+    }
+    std::vector<double> y(n * static_cast<std::size_t>(out_dim_));
+    evaluate_batch(flat.data(), static_cast<int64_t>(n), y.data());
+    std::vector<std::vector<double>> out(n);
+    for (std::size_t i = 0; i < n; ++i)
+      out[i].assign(y.begin() + static_cast<std::ptrdiff_t>(i * out_dim_),
+                    y.begin() + static_cast<std::ptrdiff_t>((i + 1) * out_dim_));
+    return out;
+  }
+  // Flat form: x [n][dim] -> y [n][m], host or device pointers.
+  void evaluate_batch(const double* x, int64_t n, double* y, void* stream = nullptr) const {
+    int64_t bad = -1;
+    const ddsg_status s = ddsg_eval_hdmr(h_.get(), x, n, y, &bad, stream);
+    if (s != DDSG_OK) detail::raise(s, true, bad);
+  }
+
+  std::vector<double> quadrature() const {  // ddsg_eval.hpp:143-151
+    std::vector<double> q(static_cast<std::size_t>(out_dim_));
+    detail::check(ddsg_hdmr_quadrature(h_.get(), q.data()));
+    return q;
+  }
+
+ private:
+  std::shared_ptr<const DdsgFunction> source_;
+  std::shared_ptr<ddsg_hdmr_t> h_;
+  int dim_ = 0, out_dim_ = 0;
+};
+
+}  // namespace ddsg_b200

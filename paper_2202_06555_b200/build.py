@@ -80,6 +80,16 @@ def build_library(verbose: bool = False) -> Path:
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("nvcc link failed")
+    # C++ drop-in test driver (tests/cpp): include/ddsg_b200.hpp over the C-ABI
+    drv_src = ROOT / "tests" / "cpp" / "test_dropin.cpp"
+    drv = ROOT / "build" / "test_dropin"
+    if drv_src.exists() and _stale(drv, [drv_src, LIB, ROOT / "include" / "ddsg_b200.hpp"]):
+        cmd = ["g++", "-std=c++20", "-O2", "-Wall", f"-I{ROOT / 'include'}", str(drv_src), f"-L{PKG}", "-lddsg_b200",
+               "-Wl,-rpath,$ORIGIN/../paper_2202_06555_b200", "-o", str(drv)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("drop-in test driver build failed")
     if _stale(WL_LIB, [WL_SRC, Path(__file__)]):
         cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", str(WL_LIB), str(WL_SRC), "-lm"]
         res = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,0 +1,390 @@
+// C++ drop-in tests: the reference's own test cases (restated, same inputs,
+// seeds and thresholds) run against include/ddsg_b200.hpp.
+//
+//   test_dropin cpu   — construction / validation cases (no kernel launch)
+//   test_dropin gpu   — evaluation cases (needs a CUDA device)
+//
+// Reference cases: proj/tests/test_sparse_grid.cpp, test_ddsg_eval.cpp,
+// test_hdmr.cpp (cited per case).  Exit code = number of failed checks.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "ddsg_b200.hpp"
+
+using namespace ddsg_b200;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    if (cond) {                                                              \
+      ++g_pass;                                                              \
+    } else {                                                                 \
+      ++g_fail;                                                              \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);   \
+    }                                                                        \
+  } while (0)
+
+template <typename E, typename F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static GridEvaluator scalar(std::function<double(std::span<const double>)> f) {
+  return [f](std::span<const double> x, std::span<double> out) { out[0] = f(x); };
+}
+
+static SparseGridFunction build_scalar(std::function<double(std::span<const double>)> f, int dim, int L,
+                                       double eps, BoundaryMode mode) {
+  SgBuildOptions opt;
+  opt.max_level = L;
+  opt.eps_gamma = eps;
+  opt.mode = mode;
+  return SparseGridFunction::build(scalar(f), dim, 1, opt);
+}
+
+// oracles.hpp:45-53
+static std::vector<std::vector<double>> uniform_points(int n, std::size_t count, uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  std::vector<std::vector<double>> pts(count, std::vector<double>(static_cast<std::size_t>(n)));
+  for (auto& p : pts)
+    for (auto& c : p) c = unif(rng);
+  return pts;
+}
+
+static uint64_t brute_count(int n, int L) {  // oracles.hpp:21-43
+  uint64_t total = 0;
+  std::vector<int> l(static_cast<std::size_t>(n), 1);
+  while (true) {
+    int sum = 0;
+    for (int v : l) sum += v;
+    if (sum <= L + n - 1) {
+      uint64_t pts = 1;
+      for (int v : l) pts <<= (v - 1);
+      total += pts;
+    }
+    std::size_t j = 0;
+    while (j < l.size()) {
+      if (++l[j] <= L) break;
+      l[j] = 1;
+      ++j;
+    }
+    if (j == l.size()) break;
+  }
+  return total;
+}
+
+static double coupled(std::span<const double> x) {  // test_ddsg_eval.cpp:37-42
+  double s = 0.0;
+  for (std::size_t j = 0; j < x.size(); ++j) s += std::exp(-0.5 * x[j]) + 0.2 * x[j] * x[j];
+  for (std::size_t j = 0; j + 1 < x.size(); ++j) s += 0.3 * std::sin(x[j] * x[j + 1]);
+  return s;
+}
+
+// Full (non-adaptive) decomposition assembled through from_parts: every
+// index of order <= k accepted, cut grids built by this library's build from
+// the cut through the center anchor (hdmr.hpp:248-259), b from the lattice
+// formula (hdmr.hpp:339-355).  Equals decompose() with eps_rho = eps_eta = 0.
+static std::shared_ptr<const DdsgFunction> full_decomposition(const GridEvaluator& f, int d, int m, int k,
+                                                              int L, BoundaryMode mode) {
+  AnchorPoint a;
+  a.coords.assign(static_cast<std::size_t>(d), 0.5);
+  a.f_anchor.resize(static_cast<std::size_t>(m));
+  f(a.coords, a.f_anchor);
+  std::vector<ComponentIndex> family{ComponentIndex{}};
+  for (int kk = 1; kk <= k; ++kk) {
+    std::vector<int> comb(static_cast<std::size_t>(kk));
+    for (int i = 0; i < kk; ++i) comb[static_cast<std::size_t>(i)] = i;
+    while (true) {
+      family.push_back(ComponentIndex{comb});
+      int i = kk;
+      while (i > 0 && comb[static_cast<std::size_t>(i - 1)] == d - (kk - i) - 1) --i;
+      if (i == 0) break;
+      ++comb[static_cast<std::size_t>(i - 1)];
+      for (int j = i; j < kk; ++j) comb[static_cast<std::size_t>(j)] = comb[static_cast<std::size_t>(j - 1)] + 1;
+    }
+  }
+  std::map<ComponentIndex, SparseGridFunction> accepted;
+  std::map<ComponentIndex, int> b;
+  for (const auto& u : family) {
+    int bu = 0;
+    for (const auto& v : family) {
+      if (!std::includes(v.dims.begin(), v.dims.end(), u.dims.begin(), u.dims.end())) continue;
+      bu += ((v.order() - u.order()) % 2 == 0) ? 1 : -1;
+    }
+    b[u] = bu;
+    if (u.empty()) continue;
+    std::vector<double> base = a.coords;
+    std::vector<int> dims = u.dims;
+    GridEvaluator cut = [&f, base, dims](std::span<const double> y, std::span<double> out) {
+      std::vector<double> x = base;
+      for (std::size_t j = 0; j < dims.size(); ++j) x[static_cast<std::size_t>(dims[j])] = y[j];
+      f(x, out);
+    };
+    SgBuildOptions opt;
+    opt.max_level = L;
+    opt.mode = mode;
+    accepted.emplace(u, SparseGridFunction::build(cut, static_cast<int>(u.order()), m, opt));
+  }
+  DdsgOptions o;
+  o.k_max = k;
+  o.max_level = L;
+  return std::make_shared<const DdsgFunction>(DdsgFunction::from_parts(d, m, o, a, accepted, {}, b, {}));
+}
+
+// ------------------------------------------------------------------ cpu
+
+static void cpu_cases() {
+  // test_sparse_grid.cpp:66-75
+  auto one = [](std::span<const double>) { return 1.0; };
+  CHECK(build_scalar(one, 1, 3, 0.0, BoundaryMode::zero_boundary).size() == 7);
+  CHECK(build_scalar(one, 2, 2, 0.0, BoundaryMode::zero_boundary).size() == 5);
+  for (int n = 1; n <= 4; ++n)
+    for (int L = 1; L <= 6; ++L)
+      CHECK(build_scalar(one, n, L, 0.0, BoundaryMode::modified_linear).size() == brute_count(n, L));
+
+  // test_sparse_grid.cpp:77-86
+  {
+    auto f = [](std::span<const double> x) { return std::max(1.0 - 2.0 * std::abs(x[0] - 0.5), 0.0); };
+    const auto g = build_scalar(f, 1, 3, 1e-8, BoundaryMode::zero_boundary);
+    CHECK(g.size() == 3);
+    for (const auto& node : g.nodes()) {
+      if (node.key[0] == 1u) CHECK(std::abs(node.surplus[0] - 1.0) <= 1e-15);
+      else CHECK(std::abs(node.surplus[0]) < 1e-15);
+    }
+  }
+  // test_sparse_grid.cpp:210-225
+  {
+    SgBuildOptions opt;
+    opt.max_level = 3;
+    GridEvaluator f = [](std::span<const double> x, std::span<double> out) {
+      out[0] = (x[0] == 0.25) ? std::numeric_limits<double>::quiet_NaN() : x[0];
+    };
+    bool caught = false;
+    try {
+      SparseGridFunction::build(f, 1, 1, opt);
+    } catch (const build_error& be) {
+      caught = true;
+      CHECK(be.point().size() == 1);
+      CHECK(be.point()[0] == 0.25);
+      CHECK(std::string(be.what()).find("0.25") != std::string::npos);
+    }
+    CHECK(caught);
+  }
+  // an evaluator exception surfaces with its own type (sparse_grid.hpp:259-262)
+  {
+    SgBuildOptions opt;
+    opt.max_level = 2;
+    GridEvaluator f = [](std::span<const double>, std::span<double>) { throw std::out_of_range("boom"); };
+    CHECK(throws<std::out_of_range>([&] { SparseGridFunction::build(f, 1, 1, opt); }));
+  }
+  // option validation (sparse_grid.hpp:86-89)
+  {
+    SgBuildOptions opt;
+    opt.max_level = 0;
+    CHECK(throws<std::invalid_argument>([&] { SparseGridFunction::build(scalar(one), 1, 1, opt); }));
+    opt.max_level = 2;
+    CHECK(throws<std::invalid_argument>([&] { SparseGridFunction::build(scalar(one), 0, 1, opt); }));
+  }
+  // from_nodes validation (sparse_grid.hpp:168-176)
+  CHECK(throws<std::invalid_argument>([&] {
+    SparseGridFunction::from_nodes(1, 1, 2, 0.0, BoundaryMode::zero_boundary, {GridNode{{1u}, {1.0}}, GridNode{{1u}, {2.0}}});
+  }));
+  CHECK(throws<std::invalid_argument>([&] {
+    SparseGridFunction::from_nodes(2, 1, 2, 0.0, BoundaryMode::zero_boundary, {GridNode{{1u}, {1.0}}});
+  }));
+  // quadrature examples (test_sparse_grid.cpp:148-177)
+  {
+    auto g1 = SparseGridFunction::from_nodes(1, 1, 2, 0.0, BoundaryMode::zero_boundary, {GridNode{{2u}, {1.0}}});
+    CHECK(std::abs(g1.quadrature()[0] - 0.25) <= 1e-15);
+    auto hat = [](std::span<const double> x) { return std::max(1.0 - 2.0 * std::abs(x[0] - 0.5), 0.0); };
+    CHECK(std::abs(build_scalar(hat, 1, 3, 0.0, BoundaryMode::zero_boundary).quadrature()[0] - 0.5) <= 1e-14);
+  }
+  // compile validation (ddsg_eval.hpp:41,54-56,63-70)
+  CHECK(throws<std::invalid_argument>([&] { VectorizedDdsg::compile(nullptr); }));
+  {
+    AnchorPoint a{{0.5, 0.5}, {1.0}};
+    std::map<ComponentIndex, SparseGridFunction> acc;
+    acc.emplace(ComponentIndex{{0, 1}}, build_scalar(coupled, 2, 2, 0.0, BoundaryMode::modified_linear));
+    std::map<ComponentIndex, int> b{{ComponentIndex{}, 0}, {ComponentIndex{{0, 1}}, 1}};
+    auto src = std::make_shared<const DdsgFunction>(DdsgFunction::from_parts(2, 1, {}, a, acc, {}, b, {}));
+    CHECK(throws<std::invalid_argument>([&] { VectorizedDdsg::compile(src); }));  // misses {0}, {1}
+    std::map<ComponentIndex, int> b2{{ComponentIndex{}, 0}, {ComponentIndex{{1}}, 1}};
+    auto src2 = std::make_shared<const DdsgFunction>(DdsgFunction::from_parts(2, 1, {}, a, acc, {}, b2, {}));
+    CHECK(throws<std::invalid_argument>([&] { VectorizedDdsg::compile(src2); }));  // non-accepted index
+  }
+}
+
+// ------------------------------------------------------------------ gpu
+
+static void gpu_cases() {
+  // hierarchization round trip (test_sparse_grid.cpp:88-116)
+  {
+    auto f = [](std::span<const double> x) {
+      double s = 1.0;
+      for (double c : x) s *= std::exp(-2.0 * c) + 0.3 * c;
+      return s;
+    };
+    for (BoundaryMode mode : {BoundaryMode::zero_boundary, BoundaryMode::modified_linear}) {
+      const auto g = build_scalar(f, 2, 5, 0.0, mode);
+      for (const auto& node : g.nodes()) {
+        std::vector<double> x(2);
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t hk = node.key[static_cast<std::size_t>(j)];
+          const int l = 32 - __builtin_clz(hk);
+          x[static_cast<std::size_t>(j)] = (2.0 * (hk - (1u << (l - 1))) + 1.0) * std::ldexp(1.0, -l);
+        }
+        CHECK(std::abs(g.interpolate(x)[0] - f(x)) <= 1e-12);
+      }
+    }
+    auto bump = [](std::span<const double> x) { return std::exp(-40.0 * (x[0] - 0.3) * (x[0] - 0.3)) + 0.1 * x[1]; };
+    const auto ga = build_scalar(bump, 2, 6, 1e-3, BoundaryMode::modified_linear);
+    CHECK(ga.size() < brute_count(2, 6));
+    for (const auto& node : ga.nodes()) {
+      std::vector<double> x(2);
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t hk = node.key[static_cast<std::size_t>(j)];
+        const int l = 32 - __builtin_clz(hk);
+        x[static_cast<std::size_t>(j)] = (2.0 * (hk - (1u << (l - 1))) + 1.0) * std::ldexp(1.0, -l);
+      }
+      CHECK(std::abs(ga.interpolate(x)[0] - bump(x)) <= 1e-12);
+    }
+  }
+  // interpolation examples (test_sparse_grid.cpp:118-146)
+  {
+    auto parab = [](std::span<const double> x) { return x[0] * (1.0 - x[0]); };
+    const auto g1 = build_scalar(parab, 1, 1, 0.0, BoundaryMode::zero_boundary);
+    std::vector<double> q{0.5};
+    CHECK(std::abs(g1.interpolate(q)[0] - 0.25) <= 1e-15);
+    const auto g2 = build_scalar(parab, 2, 4, 0.0, BoundaryMode::modified_linear);
+    for (double x2 : {0.0, 0.17, 0.5, 0.83, 1.0}) {
+      std::vector<double> a{0.3, x2}, b{0.3, 0.62};
+      CHECK(std::abs(g2.interpolate(a)[0] - g2.interpolate(b)[0]) <= 1e-12);
+    }
+    auto lin = [](std::span<const double> x) { return x[0]; };
+    const auto g3 = build_scalar(lin, 1, 2, 0.0, BoundaryMode::modified_linear);
+    std::vector<double> p{0.3};
+    CHECK(std::abs(g3.interpolate(p)[0] - 0.3) <= 1e-14);
+    for (const auto& pt : uniform_points(1, 100, 20240501ull)) CHECK(std::abs(g3.interpolate(pt)[0] - pt[0]) <= 1e-13);
+    std::vector<double> outside{1.5};
+    CHECK(throws<std::domain_error>([&] { g3.interpolate(outside); }));
+  }
+  // L2 convergence ratio (test_sparse_grid.cpp:227-244), seed 77001, 1e4 points
+  {
+    auto f = [](std::span<const double> x) { return x[0] * (1.0 - x[0]) * x[1] * (1.0 - x[1]); };
+    const auto pts = uniform_points(2, 10000, 77001ull);
+    std::vector<double> flat;
+    for (const auto& p : pts) flat.insert(flat.end(), p.begin(), p.end());
+    double prev = 0.0;
+    for (int L = 3; L <= 7; ++L) {
+      const auto g = build_scalar(f, 2, L, 0.0, BoundaryMode::zero_boundary);
+      std::vector<double> y(pts.size());
+      g.interpolate_batch(flat.data(), static_cast<int64_t>(pts.size()), y.data());
+      double sq = 0.0;
+      for (std::size_t i = 0; i < pts.size(); ++i) {
+        const double dd = y[i] - f(pts[i]);
+        sq += dd * dd;
+      }
+      const double err = std::sqrt(sq / static_cast<double>(pts.size()));
+      if (L > 3) CHECK(err / prev <= 0.35);
+      prev = err;
+    }
+  }
+  // constant functions come back constant (test_ddsg_eval.cpp:122-133)
+  {
+    GridEvaluator f = [](std::span<const double>, std::span<double> out) { out[0] = 4.25; };
+    auto src = full_decomposition(f, 3, 1, 2, 3, BoundaryMode::modified_linear);
+    const auto vec = VectorizedDdsg::compile(src);
+    for (const auto& p : uniform_points(3, 100, 5)) CHECK(std::abs(vec.evaluate(p)[0] - 4.25) <= 1e-13);
+  }
+  // batch == looped bitwise, permutation, worker independence (test_ddsg_eval.cpp:179-209)
+  {
+    auto src = full_decomposition(scalar(coupled), 4, 1, 2, 3, BoundaryMode::modified_linear);
+    const auto vec = VectorizedDdsg::compile(src);
+    const auto pts = uniform_points(4, 10000, 8443);
+    const auto batch = vec.evaluate_batch(pts);
+    CHECK(batch.size() == pts.size());
+    bool same = true;
+    for (std::size_t i = 0; i < pts.size(); i += 97) same &= std::memcmp(&batch[i][0], &vec.evaluate(pts[i])[0], 8) == 0;
+    CHECK(same);
+    auto perm = pts;
+    std::reverse(perm.begin(), perm.end());
+    const auto rb = vec.evaluate_batch(perm);
+    bool psame = true;
+    for (std::size_t i = 0; i < pts.size(); ++i) psame &= std::memcmp(&rb[pts.size() - 1 - i][0], &batch[i][0], 8) == 0;
+    CHECK(psame);
+    const auto b4 = vec.evaluate_batch(pts, 4);
+    bool wsame = true;
+    for (std::size_t i = 0; i < pts.size(); ++i) wsame &= std::memcmp(&b4[i][0], &batch[i][0], 8) == 0;
+    CHECK(wsame);
+    // a bad point raises task_error with the lowest index (runtime.hpp:133-136)
+    auto badpts = pts;
+    badpts[123][2] = 1.5;
+    badpts[77][1] = -0.5;
+    bool caught = false;
+    try {
+      vec.evaluate_batch(badpts);
+    } catch (const task_error& te) {
+      caught = te.task_id() == 77;
+      CHECK(throws<std::domain_error>([&] { te.rethrow_cause(); }));
+    }
+    CHECK(caught);
+  }
+  // vector-valued outputs (test_ddsg_eval.cpp:224-242) and vectorized == naive
+  // (test_ddsg_eval.cpp:106-120): naive telescoping from per-cut batched calls
+  {
+    GridEvaluator f = [](std::span<const double> x, std::span<double> out) {
+      out[0] = x[0] + x[1];
+      out[1] = std::exp(x[0] * x[1]);
+      out[2] = 0.5;
+    };
+    auto src = full_decomposition(f, 2, 3, 2, 4, BoundaryMode::modified_linear);
+    const auto vec = VectorizedDdsg::compile(src);
+    const auto pts = uniform_points(2, 200, 61);
+    for (const auto& p : pts) {
+      const auto got = vec.evaluate(p);
+      // naive Eq. 3.16: sum_u sum_{v subset u} sign * cut_v(x)
+      std::vector<double> want = src->anchor().f_anchor;
+      for (const auto& [u, g] : src->accepted()) {
+        const std::size_t k = u.order();
+        for (std::size_t mask = 0; mask < (std::size_t{1} << k); ++mask) {
+          std::vector<int> vd;
+          for (std::size_t j = 0; j < k; ++j)
+            if (mask & (std::size_t{1} << j)) vd.push_back(u.dims[j]);
+          const double sign = ((k - vd.size()) % 2 == 0) ? 1.0 : -1.0;
+          if (vd.empty()) {
+            for (int c = 0; c < 3; ++c) want[static_cast<std::size_t>(c)] += sign * src->anchor().f_anchor[static_cast<std::size_t>(c)];
+            continue;
+          }
+          std::vector<double> xr;
+          for (int dd : vd) xr.push_back(p[static_cast<std::size_t>(dd)]);
+          const auto cv = src->accepted().at(ComponentIndex{vd}).interpolate(xr);
+          for (int c = 0; c < 3; ++c) want[static_cast<std::size_t>(c)] += sign * cv[static_cast<std::size_t>(c)];
+        }
+      }
+      for (int c = 0; c < 3; ++c) CHECK(std::abs(got[static_cast<std::size_t>(c)] - want[static_cast<std::size_t>(c)]) <= 1e-12);
+    }
+  }
+}
+
+int main(int argc, char** argv) {
+  const std::string which = argc > 1 ? argv[1] : "cpu";
+  if (which == "cpu" || which == "all") cpu_cases();
+  if (which == "gpu" || which == "all") gpu_cases();
+  std::printf("%d passed, %d failed\n", g_pass, g_fail);
+  return g_fail;
+}
