@@ -45,6 +45,8 @@ struct EvalParams {
   const int32_t* slab;
   const double* surplus;
   const int32_t* row_stored;
+  const int16_t* row_run;
+  const int32_t* slot_runs;
   const double* f_anchor;
 };
 

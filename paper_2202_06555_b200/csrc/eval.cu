@@ -108,6 +108,8 @@ void DeviceProgram::upload(const HostProgram& hp) {
   p.slab = put(hp.slab);
   p.surplus = put(hp.surplus);
   p.row_stored = put(hp.row_stored);
+  p.row_run = put(hp.row_run);
+  p.slot_runs = put(hp.slot_runs);
   p.f_anchor = put(hp.f_anchor);
   p_ = p;
   delete fast_;
@@ -172,6 +174,8 @@ __global__ void __launch_bounds__(128) eval_generic_kernel(EvalParams P, const d
       const int32_t* dims = P.slot_dims + P.slot_dims_off[a];
       const int mode = P.slot_mode[a];
       const int s_end = P.slot_sub_end[a];
+      const int runs = P.slot_runs[a];
+      for (int run = 0; run < runs; ++run)  // stored order = runs of canonical order
       for (int s = P.slot_sub_begin[a]; s < s_end; ++s) {
         const uint8_t* lv = P.levels + P.sub_lv_off[s];
         double w = 1.0;
@@ -187,6 +191,7 @@ __global__ void __launch_bounds__(128) eval_generic_kernel(EvalParams P, const d
         if (w == 0.0) continue;
         const int32_t row = P.slab[P.sub_slab_off[s] + lin];
         if (row < 0) continue;
+        if (runs > 1 && P.row_run[row] != run) continue;
         const double* sr = P.surplus + static_cast<int64_t>(row) * P.m + c0;
 #pragma unroll
         for (int c = 0; c < kCols; ++c)
@@ -238,6 +243,8 @@ __global__ void support_kernel(EvalParams P, const double* __restrict__ x, int64
     if (k == 0) continue;
     const int32_t* dims = P.slot_dims + P.slot_dims_off[a];
     const int mode = P.slot_mode[a];
+    const int runs = P.slot_runs[a];
+    for (int run = 0; run < runs; ++run)
     for (int s = P.slot_sub_begin[a]; s < P.slot_sub_end[a]; ++s) {
       const uint8_t* lv = P.levels + P.sub_lv_off[s];
       double w = 1.0;
@@ -253,6 +260,7 @@ __global__ void support_kernel(EvalParams P, const double* __restrict__ x, int64
       if (w == 0.0) continue;
       const int32_t row = P.slab[P.sub_slab_off[s] + lin];
       if (row < 0) continue;
+      if (runs > 1 && P.row_run[row] != run) continue;
       ++nnz;
       const unsigned long long key =
           (static_cast<unsigned long long>(static_cast<uint32_t>(P.slot_id[a])) << 32) |

@@ -689,6 +689,10 @@ bool FastHdmr::build(const HostProgram& hp) {
       why_ = "slot order > 2";
       return false;
     }
+    if (hp.slot_runs[a] != 1) {
+      why_ = "grid stored in non-canonical order (multi-run evaluation is on the generic kernel)";
+      return false;
+    }
     H.k = k;
     H.mode = hp.slot_mode[a];
     H.tree_t = tree_t[a];

@@ -365,6 +365,26 @@ GridLayout HostGrid::compile() const {
   }
   L.subspaces = std::move(sorted);
   L.rows = row;
+  // Stored order = concatenation of maximal runs sorted by (level sum, key):
+  // the reference's build appends batches sorted that way
+  // (sparse_grid.hpp:248-253), closure ancestors making later batches start
+  // below earlier ones.  At any point the nonzero nodes of one run come in
+  // canonical subspace order, so evaluating run by run reproduces the stored
+  // order exactly.
+  std::vector<int16_t> run_of(n, 0);
+  int run = 0;
+  for (int64_t i = 1; i < n; ++i) {
+    const uint32_t* a = &keys[(i - 1) * dim];
+    const uint32_t* b = &keys[i * dim];
+    const int sa = level_sum_of(a, dim), sb = level_sum_of(b, dim);
+    const bool ascending = sa != sb ? sa < sb : std::lexicographical_compare(a, a + dim, b, b + dim);
+    if (!ascending) ++run;
+    if (run > 32767) fail(DDSG_INVALID_ARGUMENT, "sparse grid: stored order has more than 32767 runs");
+    run_of[i] = static_cast<int16_t>(run);
+  }
+  L.runs = n > 0 ? run + 1 : 1;
+  L.row_run.resize(L.rows);
+  for (int64_t r = 0; r < L.rows; ++r) L.row_run[r] = run_of[L.row_to_stored[r]];
   return L;
 }
 

@@ -17,11 +17,6 @@
 
 namespace ddsg_b200 {
 
-struct KeyHash {
-  const uint32_t* keys;
-  int dim;
-};
-
 // One subspace (level vector l) of a grid in the compiled layout.  Cells are
 // row-major over dims (dim 0 most significant), cell k_j in [0, 2^(l_j-1)).
 struct SubspaceInfo {
@@ -41,6 +36,8 @@ struct GridLayout {
   std::vector<SubspaceInfo> subspaces;
   std::vector<int32_t> slab;          // [total cells] -> layout row or -1
   std::vector<int32_t> row_to_stored; // layout row -> stored node index
+  std::vector<int16_t> row_run;       // layout row -> run of its stored position
+  int runs = 1;                       // maximal canonically sorted runs of the stored order
   int64_t rows = 0;
 };
 

@@ -48,6 +48,7 @@ void HostProgram::add_empty_slot(int32_t id, double b) {
   slot_sub_end.push_back(s);
   slot_row_begin.push_back(rows);
   slot_row_end.push_back(rows);
+  slot_runs.push_back(1);
 }
 
 void HostProgram::add_grid_slot(int32_t id, const HostGrid& g, const std::vector<int32_t>& dims,
@@ -77,7 +78,9 @@ void HostProgram::add_grid_slot(int32_t id, const HostGrid& g, const std::vector
     surplus.insert(surplus.end(), g.surplus.begin() + static_cast<int64_t>(st) * m,
                    g.surplus.begin() + static_cast<int64_t>(st + 1) * m);
     row_stored.push_back(st);
+    row_run.push_back(L.row_run[r]);
   }
+  slot_runs.push_back(L.runs);
   slot_row_begin.push_back(rows);
   rows += L.rows;
   slot_row_end.push_back(rows);

@@ -31,6 +31,7 @@ struct HostProgram {
   std::vector<double> slot_b;
   std::vector<int32_t> slot_sub_begin, slot_sub_end;  // subspace range
   std::vector<int64_t> slot_row_begin, slot_row_end;  // surplus row range
+  std::vector<int32_t> slot_runs;                     // stored-order runs of the slot's grid
   std::vector<uint8_t> merges;
 
   // subspaces (all slots concatenated)
@@ -41,6 +42,7 @@ struct HostProgram {
   std::vector<int32_t> slab;          // -> surplus row, or -1
   std::vector<double> surplus;        // [rows][m]
   std::vector<int32_t> row_stored;    // row -> stored node index within its grid
+  std::vector<int16_t> row_run;       // row -> stored-order run
   std::vector<double> f_anchor;       // [m]
   int64_t rows = 0;
 

@@ -221,3 +221,57 @@ def test_eval_reports_kernel_launches(config4):
     vec.evaluate_batch(x)
     launches, ms, _ = last_eval_stats()
     assert launches >= 1 and ms > 0.0
+
+
+# ----------------------------------------------------- stored-order exactness
+
+def test_config3_stored_order_exact():
+    """Config 3's adaptive build is NOT in canonical order (closure ancestors
+    appended to later batches, sparse_grid.hpp:218-253).  EXACT mode walks
+    the stored order run by run, so the GPU matches the reference's own
+    evaluation of its own build bit for bit."""
+    cfg = W.CONFIGS[3]
+    g = W.build_grid(cfg)
+    keys, _ = g.nodes()
+    assert not np.array_equal(canonical_perm(keys), np.arange(len(keys)))
+    x = W.points(cfg, n=200)
+    assert np.array_equal(bits(g.interpolate(x)), bits(grid_oracle(g, x)))
+    nnz_o, h_o = O.port_grid_support(cfg.d, cfg.mode, keys, x)
+    nnz, h = g.support(x)
+    assert np.array_equal(nnz, nnz_o) and np.array_equal(h, h_o)
+
+
+def test_arbitrary_stored_order_exact():
+    """Any caller order (from_nodes preserves it, sparse_grid.hpp:160-179)."""
+    keep, ctx = int_ctx(3)
+    g0 = SparseGridFunction.build(wl("wl_coupled"), 3, 1, 5, 1e-4, MODIFIED_LINEAR, ctx=ctx)
+    keys, sur = g0.nodes()
+    rng = np.random.default_rng(7)
+    p = rng.permutation(len(keys))
+    g = SparseGridFunction.from_nodes(3, 1, 5, 1e-4, MODIFIED_LINEAR, keys[p], sur[p])
+    x = uniform_points(123, 1000, 3)
+    assert np.array_equal(bits(g.interpolate(x)), bits(grid_oracle(g, x)))
+
+
+@pytest.mark.parametrize("cid", [4, 5])
+def test_hdmr_configs_run_on_slot_kernel(cid, config4, config5):
+    cfg, parts, slots, vec = config4 if cid == 4 else config5
+    assert vec.uses_slot_kernel()
+
+
+def test_hdmr_stored_order_grids_fall_back_exactly():
+    """An HDMR whose component grids are stored out of canonical order is
+    evaluated on the generic kernel in stored order, still bit-exact."""
+    z = load(golden_files("hdmr")[0])
+    slots = hdmr_slots_from_golden(z, canonical=False)
+    rng = np.random.default_rng(3)
+    shuffled = []
+    for u, b, g in slots:
+        if g is None:
+            shuffled.append((u, b, None))
+        else:
+            p = rng.permutation(len(g[1]))
+            shuffled.append((u, b, (g[0], g[1][p], g[2][p])))
+    vec = make_vectorized(int(z["d"]), int(z["m"]), z["f_anchor"], shuffled, int(z["max_level"]), float(z["eps"]))
+    rc, want, _ = O.port_hdmr_eval(int(z["d"]), int(z["m"]), z["f_anchor"], shuffled, z["x"])
+    assert np.array_equal(bits(vec.evaluate_batch(z["x"])), bits(want))
