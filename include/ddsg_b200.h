@@ -109,6 +109,19 @@ ddsg_status ddsg_grid_append(ddsg_grid_t* g, int64_t n_new, const uint32_t* heap
 ddsg_status ddsg_hierarchize(const ddsg_grid_t* g, int64_t n_new, const uint32_t* heap_keys,
                              const double* f_values, double* surplus_out);
 
+/* Host (CPU) residual hierarchization, bit-identical to the reference's
+ * insert_batch (sparse_grid.hpp:264-276): interpolation at each new node over
+ * the current nodes in stored order.  Used where no GPU is present. */
+ddsg_status ddsg_hierarchize_host(const ddsg_grid_t* g, int64_t n_new, const uint32_t* heap_keys,
+                                  const double* f_values, double* surplus_out);
+
+/* Refinement candidates from level sum s (sparse_grid.hpp:215-254): children
+ * of every node at level sum s whose surplus passes the grid's criterion
+ * (eps_gamma, norm), closed under missing ancestors, sorted by (level sum,
+ * key) — the next batch the reference's build would insert.  Call with
+ * heap_keys == NULL to get the count in *n_out. */
+ddsg_status ddsg_grid_refine_candidates(const ddsg_grid_t* g, int level_sum, int64_t* n_out, uint32_t* heap_keys);
+
 ddsg_status ddsg_grid_destroy(ddsg_grid_t* g);
 
 /* Accessors (sparse_grid.hpp:74-81). */

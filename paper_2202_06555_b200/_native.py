@@ -44,6 +44,8 @@ SIGNATURES = {
     "ddsg_grid_append": (_i, [_p, _i64, _p, _p]),
     "ddsg_hierarchize": (_i, [_p, _i64, _p, _p, _p]),
     "ddsg_grid_destroy": (_i, [_p]),
+    "ddsg_hierarchize_host": (_i, [_p, _i64, _p, _p, _p]),
+    "ddsg_grid_refine_candidates": (_i, [_p, _i, C.POINTER(_i64), _p]),
     "ddsg_grid_info": (_i, [_p, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_d), C.POINTER(_i64)]),
     "ddsg_grid_nodes": (_i, [_p, _p, _p]),
     "ddsg_grid_quadrature": (_i, [_p, _p]),

@@ -202,6 +202,34 @@ ddsg_status ddsg_hierarchize(const ddsg_grid_t* g, int64_t n_new, const uint32_t
   });
 }
 
+ddsg_status ddsg_hierarchize_host(const ddsg_grid_t* g, int64_t n_new, const uint32_t* heap_keys,
+                                  const double* f_values, double* surplus_out) {
+  return guarded([&] {
+    if (!g) fail(DDSG_INVALID_ARGUMENT, "hierarchize: null grid");
+    if (n_new < 0 || (n_new > 0 && (!heap_keys || !f_values || !surplus_out)))
+      fail(DDSG_INVALID_ARGUMENT, "hierarchize: null arrays");
+    const HostGrid& G = g->g;
+    std::vector<double> interp(G.m);
+    for (int64_t i = 0; i < n_new; ++i) {
+      for (int j = 0; j < G.dim; ++j)
+        if (!valid_key(heap_keys[i * G.dim + j])) fail(DDSG_INVALID_ARGUMENT, "hierarchize: invalid heap key");
+      std::fill(interp.begin(), interp.end(), 0.0);
+      G.interpolate_at_node(heap_keys + i * G.dim, G.size(), interp.data());
+      for (int c = 0; c < G.m; ++c) surplus_out[i * G.m + c] = f_values[i * G.m + c] - interp[c];
+    }
+  });
+}
+
+ddsg_status ddsg_grid_refine_candidates(const ddsg_grid_t* g, int level_sum, int64_t* n_out, uint32_t* heap_keys) {
+  return guarded([&] {
+    if (!g || !n_out) fail(DDSG_INVALID_ARGUMENT, "refine_candidates: null argument");
+    const auto c = g->g.refine_candidates(level_sum);
+    *n_out = static_cast<int64_t>(c.size());
+    if (heap_keys)
+      for (size_t i = 0; i < c.size(); ++i) std::copy(c[i].begin(), c[i].end(), heap_keys + i * g->g.dim);
+  });
+}
+
 ddsg_status ddsg_grid_destroy(ddsg_grid_t* g) {
   return guarded([&] { delete g; });
 }

@@ -452,7 +452,8 @@ template <int kExact>
 __global__ void __launch_bounds__(kPoints, 1)
     fast_hdmr_kernel(const unsigned char* __restrict__ blocks, const int64_t* __restrict__ block_off,
                      const int32_t* __restrict__ block_len, const int16_t* __restrict__ slot_dims,
-                     int n_active, int n_cb, int levels, const double* __restrict__ xt, int64_t n, int m,
+                     int n_active, int n_cb, int cb_group, int levels, const double* __restrict__ xt, int64_t n,
+                     int m,
                      double* __restrict__ y, int64_t stage_bytes) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [kStages] full, [kStages] empty
@@ -464,8 +465,17 @@ __global__ void __launch_bounds__(kPoints, 1)
   int16_t* sdims = reinterpret_cast<int16_t*>(deep + static_cast<int64_t>(smem_levels) * (kCols / 2) * kPoints);
   const bool use_tmem = levels - 1 > kSmemLevels;
 
-  const int tile = blockIdx.x / n_cb;
-  const int cb = blockIdx.x - tile * n_cb;
+  // CTA order: column blocks in groups of cb_group; within a group, the
+  // group's column blocks of one point tile are adjacent.  Concurrent CTAs
+  // then share a few column blocks' slot tables (L2-resident) while each
+  // tile's points are re-read only n_cb / cb_group times.
+  const int64_t tiles = (n + kPoints - 1) / kPoints;
+  const int64_t per_group = tiles * cb_group;
+  const int grp = static_cast<int>(blockIdx.x / per_group);
+  const int64_t rem = blockIdx.x - grp * per_group;
+  const int gsize = min(cb_group, n_cb - grp * cb_group);
+  const int64_t tile = rem / gsize;
+  const int cb = grp * cb_group + static_cast<int>(rem - tile * gsize);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int64_t p = static_cast<int64_t>(tile) * kPoints + tid;
@@ -771,6 +781,12 @@ bool FastHdmr::build(const HostProgram& hp) {
     max_bytes = std::max(max_bytes, P.bytes);
   }
   block_bytes_ = (max_bytes + 127) / 128 * 128;
+  {
+    int64_t per_cb = 0;
+    for (const SlotPlan& P : plans) per_cb += P.bytes;
+    const int64_t budget = int64_t{64} << 20;  // staged tables kept L2-resident per CTA wave
+    cb_group_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_cb_, budget / std::max<int64_t>(per_cb, 1))));
+  }
   const int64_t deep_bytes = std::min(std::max(0, levels - 1), kSmemLevels) * int64_t{kCols} * kPoints * 8;
   const int64_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
   if (smem > 227 * 1024) {
@@ -841,11 +857,11 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   kernel_timer().begin(st);
   if (exact)
     fast_hdmr_kernel<1><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
-                                                     block_len_, slot_dims_, n_active_, n_cb_, levels_, xt, n, m_, y,
+                                                     block_len_, slot_dims_, n_active_, n_cb_, cb_group_, levels_, xt, n, m_, y,
                                                      block_bytes_);
   else
     fast_hdmr_kernel<0><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
-                                                     block_len_, slot_dims_, n_active_, n_cb_, levels_, xt, n, m_, y,
+                                                     block_len_, slot_dims_, n_active_, n_cb_, cb_group_, levels_, xt, n, m_, y,
                                                      block_bytes_);
   kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());

@@ -92,7 +92,7 @@ class FastHdmr {
  private:
   bool usable_ = false;
   std::string why_;
-  int d_ = 0, m_ = 0, n_cb_ = 0, n_active_ = 0, levels_ = 0;
+  int d_ = 0, m_ = 0, n_cb_ = 0, cb_group_ = 1, n_active_ = 0, levels_ = 0;
   int64_t block_bytes_ = 0;  // stage size (max block), multiple of 128
   void* blocks_ = nullptr;   // [n_cb][n_active] blocks of block_bytes_ each (offsets below)
   int64_t* block_off_ = nullptr;  // device: [n_cb * n_active] byte offsets

@@ -237,6 +237,11 @@ std::vector<std::vector<uint32_t>> HostGrid::next_candidates(int s, std::vector<
   return out;
 }
 
+std::vector<std::vector<uint32_t>> HostGrid::refine_candidates(int s) const {
+  std::vector<char> refined(size(), 0);
+  return const_cast<HostGrid*>(this)->next_candidates(s, refined);
+}
+
 void HostGrid::insert_batch(const std::vector<std::vector<uint32_t>>& batch, const BatchEval& f) {
   // sparse_grid.hpp:256-298: evaluate the whole batch against the frozen grid,
   // reject non-finite values, then hierarchize one by one in batch order.

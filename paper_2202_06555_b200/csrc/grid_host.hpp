@@ -64,6 +64,10 @@ class HostGrid {
                         const BatchEval& f);
 
   void append(int64_t n, const uint32_t* keys, const double* surplus);
+  // Refinement candidates from level sum s: children of significant nodes,
+  // closed under missing ancestors, sorted by (level sum, key)
+  // (sparse_grid.hpp:215-254).  Does not modify the grid.
+  std::vector<std::vector<uint32_t>> refine_candidates(int s) const;
   std::vector<double> quadrature() const;
   bool contains(const uint32_t* key) const;
   int64_t find(const uint32_t* key) const;

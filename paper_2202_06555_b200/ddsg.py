@@ -206,12 +206,25 @@ class SparseGridFunction:
         surplus = np.ascontiguousarray(surplus, dtype=np.float64).reshape(-1, self.out_dim)
         _check(N.lib.ddsg_grid_append(self._h, keys.shape[0], _ptr(keys), _ptr(surplus)))
 
-    def hierarchize(self, keys: np.ndarray, f_values: np.ndarray) -> np.ndarray:
+    def hierarchize(self, keys: np.ndarray, f_values: np.ndarray, device: bool = True) -> np.ndarray:
+        """surplus = f - interpolate(grid, x(key)) for new nodes (sparse_grid.hpp:264-276);
+        device=True evaluates on the GPU, False on the host (both bit-identical)."""
         keys = np.ascontiguousarray(keys, dtype=np.uint32).reshape(-1, self.dim)
         f_values = np.ascontiguousarray(f_values, dtype=np.float64).reshape(-1, self.out_dim)
         out = np.empty_like(f_values)
-        _check(N.lib.ddsg_hierarchize(self._h, keys.shape[0], _ptr(keys), _ptr(f_values), _ptr(out)))
+        fn = N.lib.ddsg_hierarchize if device else N.lib.ddsg_hierarchize_host
+        _check(fn(self._h, keys.shape[0], _ptr(keys), _ptr(f_values), _ptr(out)))
         return out
+
+    def refine_candidates(self, level_sum: int) -> np.ndarray:
+        """The batch the reference's build would insert after level sum s
+        (sparse_grid.hpp:215-254), as heap keys [n][dim]."""
+        n = C.c_int64()
+        _check(N.lib.ddsg_grid_refine_candidates(self._h, level_sum, C.byref(n), None))
+        keys = np.empty((n.value, self.dim), dtype=np.uint32)
+        if n.value:
+            _check(N.lib.ddsg_grid_refine_candidates(self._h, level_sum, C.byref(n), _ptr(keys)))
+        return keys
 
     def set_eval_mode(self, mode: int) -> None:
         _check(N.lib.ddsg_grid_set_eval_mode(self._h, mode))

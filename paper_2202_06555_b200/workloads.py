@@ -127,6 +127,41 @@ def build_hdmr_parts(cfg: Config) -> HdmrParts:
     return parts
 
 
+class CutTarget:
+    """The config target restricted to the cut through the center anchor along
+    `dims` (hdmr.hpp:248-259), as a C evaluator (address + ctx) and a numpy
+    batch function."""
+
+    def __init__(self, cfg: Config, dims: Tuple[int, ...]):
+        wl = N.workloads()
+        self.cfg, self.dims = cfg, tuple(dims)
+        self._dims = np.array(dims, dtype=np.int32)
+        self._anchor = np.full(cfg.d, 0.5)
+        self.ctx = wl.wl_cut_new(N.wl_fn(cfg.target), None, cfg.d, cfg.m, len(dims), self._dims.ctypes.data,
+                                 self._anchor.ctypes.data)
+        self.addr = N.wl_fn("wl_cut_eval")
+        self._fn = wl.wl_cut_eval
+        self._fn.restype = C.c_int
+        self._fn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+
+    def __call__(self, xs: np.ndarray) -> np.ndarray:
+        xs = np.ascontiguousarray(xs, dtype=np.float64).reshape(-1, len(self.dims))
+        out = np.empty((xs.shape[0], self.cfg.m))
+        if xs.shape[0]:
+            self._fn(xs.ctypes.data, xs.shape[0], out.ctypes.data, C.c_void_p(self.ctx))
+        return out
+
+    def __del__(self):
+        if getattr(self, "ctx", None):
+            N.workloads().wl_cut_free(C.c_void_p(self.ctx))
+            self.ctx = None
+
+
+def build_cut_grid(cfg: Config, dims: Tuple[int, ...], level: int, eps: float) -> SparseGridFunction:
+    cut = CutTarget(cfg, dims)
+    return SparseGridFunction.build(cut.addr, len(dims), cfg.m, level, eps, cfg.mode, ctx=cut.ctx)
+
+
 def build_hdmr(cfg: Config) -> Tuple[VectorizedDdsg, HdmrParts]:
     parts = build_hdmr_parts(cfg)
     return VectorizedDdsg.compile(parts.d, parts.m, parts.f_anchor, parts.slots), parts
