@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
+    ap.add_argument("--no-refine", action="store_true",
+                    help="build the 1-d cuts at their final level instead of one distributed refinement step")
     return ap.parse_args()
 
 
@@ -222,7 +224,33 @@ def run_ours(args, rank, world, local_rank, dist):
     n_total = args.points or cfg.n_points
     n_local = n_total // world + (1 if rank < n_total % world else 0)
     t0 = time.time()
-    if cfg.kind == "hdmr":
+    refine_info = None
+    if cfg.kind == "hdmr" and not args.no_refine:
+        # BASELINE config 5: "one refinement step whose new surpluses are NCCL
+        # all-gathered before re-evaluation" -- build the 1-d cuts one level
+        # short, then refine them on all ranks (each rank evaluates the target
+        # and hierarchizes its share of the new nodes on its GPU; the surplus
+        # rows are all-gathered over NCCL and appended everywhere).
+        import dataclasses
+
+        from paper_2202_06555_b200.ddsg import VectorizedDdsg
+        from paper_2202_06555_b200.refine import refine_step
+
+        coarse = dataclasses.replace(cfg, level_1d=cfg.level_1d - 1)
+        parts = W.build_hdmr_parts(coarse)
+        idx = [i for i, (u, b, g) in enumerate(parts.slots) if len(u) == 1]
+        grids = [parts.slots[i][2] for i in idx]
+        cuts = [W.CutTarget(cfg, parts.slots[i][0]) for i in idx]
+        t_ref = time.time()
+        st = refine_step(grids, [cfg.level_1d - 1] * len(grids), lambda gi, xs: cuts[gi](xs), dist=dist,
+                         device=True, comm_device=f"cuda:{local_rank}")
+        refine_info = {"new_nodes": st.new_nodes, "rounds": st.rounds, "allgather_bytes": st.gathered_bytes,
+                       "hierarchize_s": round(st.hierarchize_s, 3), "allgather_s": round(st.allgather_s, 4),
+                       "total_s": round(time.time() - t_ref, 2),
+                       "collective": "all_gather_into_tensor (NCCL)" if dist is not None else "none (1 rank)"}
+        obj = VectorizedDdsg.compile(parts.d, parts.m, parts.f_anchor, parts.slots)
+        evaluate = obj.evaluate_batch
+    elif cfg.kind == "hdmr":
         obj, parts = W.build_hdmr(cfg)
         evaluate = obj.evaluate_batch
     else:
@@ -340,6 +368,7 @@ def run_ours(args, rank, world, local_rank, dist):
                        "l2": f"inputs {n_local * cfg.d * 8 / 1e9:.1f} GB per GPU, larger than L2 (no flush needed)",
                        "build_s": round(build_s, 1)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "refinement": refine_info,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

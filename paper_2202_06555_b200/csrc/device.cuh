@@ -11,6 +11,7 @@
 
 namespace ddsg_b200 {
 class FastHdmr;
+class PlainGrid;
 }
 
 namespace ddsg_b200 {
@@ -62,13 +63,15 @@ class DeviceProgram {
   bool ready() const { return ready_; }
   const HostProgram& host() const { return hp_; }
   const FastHdmr* fast() const { return fast_; }
+  const PlainGrid* plain() const { return plain_; }
 
  private:
   HostProgram hp_;
   std::vector<void*> allocs_;
   EvalParams p_{};
   bool ready_ = false;
-  FastHdmr* fast_ = nullptr;  // slot-staged kernel program, when the program qualifies
+  FastHdmr* fast_ = nullptr;    // slot-staged kernel program, when the program qualifies
+  PlainGrid* plain_ = nullptr;  // prefix-walk plain-grid kernel program, when it qualifies
   template <typename T>
   const T* put(const std::vector<T>& v);
 };

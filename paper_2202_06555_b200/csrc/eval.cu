@@ -21,6 +21,7 @@
 #include "basis.cuh"
 #include "device.cuh"
 #include "fast_hdmr.cuh"
+#include "plain.cuh"
 
 namespace ddsg_b200 {
 
@@ -67,6 +68,7 @@ KernelTimer& kernel_timer() {
 DeviceProgram::~DeviceProgram() {
   for (void* p : allocs_) cudaFree(p);
   delete fast_;
+  delete plain_;
 }
 
 template <typename T>
@@ -84,6 +86,8 @@ void DeviceProgram::upload(const HostProgram& hp) {
   allocs_.clear();
   delete fast_;
   fast_ = nullptr;
+  delete plain_;
+  plain_ = nullptr;
   ready_ = false;
   hp_ = hp;
   EvalParams p{};
@@ -117,6 +121,11 @@ void DeviceProgram::upload(const HostProgram& hp) {
   if (!fast_->build(hp)) {
     delete fast_;
     fast_ = nullptr;
+  }
+  plain_ = new PlainGrid();
+  if (!plain_->build(hp, p_)) {
+    delete plain_;
+    plain_ = nullptr;
   }
   ready_ = true;
 }
@@ -359,6 +368,7 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
                            Scratch& xt_scratch) {
   if (n <= 0) return 0;
   const EvalParams P = prog.params(exact);
+  if (const PlainGrid* pg = prog.plain()) return pg->launch(exact, dx, n, base, dy, dbad, st);
   if (const FastHdmr* f = prog.fast()) {
     // chunk so the dim-major scratch stays <= ~1 GiB
     const int d = f->dim();

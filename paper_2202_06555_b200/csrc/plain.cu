@@ -1,0 +1,233 @@
+// Plain-grid evaluation kernel (BASELINE configs 1-3): one thread per point
+// and up to kMC output columns, walking the grid's subspaces in canonical
+// order (per stored-order run) with incremental prefix products.
+//
+// The reference's node weight is the dim-ordered product
+// w = ((1 * v_0) * v_1) * ... (sparse_grid.hpp:116-122): its partial products
+// are exactly prefix products, so for consecutive subspaces l, l' whose level
+// vectors first differ at dim q only the suffix q..d-1 is recomputed (3.7
+// factors per subspace on average for config 2, 6.0 for config 3).  The 1-d
+// factors v(x_j, l) and candidate cells are computed once per point into a
+// shared-memory table.  Rounding is bit-identical to the reference (EXACT:
+// separate mul and add per term; a zero prefix stays zero, which is the
+// reference's early exit).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "basis.cuh"
+#include "plain.cuh"
+
+namespace ddsg_b200 {
+
+namespace plain {
+
+struct Params {
+  int d, m, n_sub, runs, lmax, mode;
+  const uint8_t* levels;   // [n_sub][d]
+  const int16_t* q;        // [n_sub] first dim to recompute
+  const int32_t* base;     // [n_sub] first row (full) or slab offset (partial)
+  const uint8_t* full;     // [n_sub]
+  const int32_t* slab;     // partial subspaces: cell -> row or -1
+  const int16_t* row_run;  // [rows]
+  const double* surplus;   // [rows][m]
+};
+
+template <int kDMax, int kMC, int kExact>
+__global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
+                                                         int64_t base, double* __restrict__ y,
+                                                         unsigned long long* bad) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * kThreads + tid;
+  const bool valid = p < n;
+  const int d = P.d, L = P.lmax;
+  double* fv = reinterpret_cast<double*>(smem);                              // [d*L][kThreads]
+  uint16_t* fk = reinterpret_cast<uint16_t*>(fv + static_cast<int64_t>(d) * L * kThreads);  // [d*L][kThreads]
+  bool ok = valid;
+  for (int j = 0; j < d; ++j) {
+    const double xv = valid ? x[p * d + j] : 0.5;
+    ok &= (xv >= 0.0 && xv <= 1.0);
+    for (int l = 1; l <= L; ++l) {
+      const uint32_t kk = cell_at(xv, l);
+      fv[(j * L + l - 1) * kThreads + tid] = basis_at(P.mode, l, kk, xv);
+      fk[(j * L + l - 1) * kThreads + tid] = static_cast<uint16_t>(kk);
+    }
+  }
+  if (valid && !ok) atomicMin(bad, static_cast<unsigned long long>(base + p));
+  if (!valid || !ok) return;  // no block-wide barrier below: each thread owns its table column
+
+  for (int c0 = 0; c0 < P.m; c0 += kMC) {
+    const int nc = min(kMC, P.m - c0);
+    double acc[kMC];
+#pragma unroll
+    for (int c = 0; c < kMC; ++c) acc[c] = 0.0;
+    for (int run = 0; run < P.runs; ++run) {
+      double pw[kDMax];
+      uint32_t pc[kDMax];
+#pragma unroll
+      for (int j = 0; j < kDMax; ++j) {
+        pw[j] = 0.0;
+        pc[j] = 0u;
+      }
+      for (int s = 0; s < P.n_sub; ++s) {
+        const int q = P.q[s];
+        const uint8_t* lv = P.levels + static_cast<int64_t>(s) * d;
+#pragma unroll
+        for (int j = 0; j < kDMax; ++j) {
+          if (j >= q && j < d) {
+            const int l = lv[j];
+            const int t = (j * L + l - 1) * kThreads + tid;
+            const double v = fv[t];
+            const uint32_t kk = fk[t];
+            if (j == 0) {
+              pw[0] = v;  // fl(1 * v_0)
+              pc[0] = kk;
+            } else {
+              pw[j] = __dmul_rn(pw[j - 1], v);
+              pc[j] = (pc[j - 1] << (l - 1)) | kk;
+            }
+          } else if (j >= d && j > 0) {
+            pw[j] = pw[j - 1];
+            pc[j] = pc[j - 1];
+          }
+        }
+        const double w = pw[kDMax - 1];
+        if (w == 0.0) continue;  // support test (sparse_grid.hpp:123)
+        int row = P.base[s];
+        if (P.full[s])
+          row += static_cast<int>(pc[kDMax - 1]);
+        else
+          row = P.slab[row + static_cast<int>(pc[kDMax - 1])];
+        if (row < 0) continue;
+        if (P.runs > 1 && P.row_run[row] != run) continue;
+        const double* sr = P.surplus + static_cast<int64_t>(row) * P.m + c0;
+#pragma unroll
+        for (int c = 0; c < kMC; ++c) {
+          if (c < nc) {
+            const double sv = __ldg(sr + c);
+            acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w, sv)) : __fma_rn(w, sv, acc[c]);
+          }
+        }
+      }
+    }
+    double* yp = y + p * P.m + c0;
+#pragma unroll
+    for (int c = 0; c < kMC; ++c)
+      if (c < nc) yp[c] = acc[c];
+  }
+}
+
+}  // namespace plain
+
+using namespace plain;
+
+PlainGrid::~PlainGrid() {
+  for (void* p : allocs_) cudaFree(p);
+}
+
+template <typename T>
+const T* PlainGrid::put(const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  void* p = nullptr;
+  DDSG_CUDA(cudaMalloc(&p, v.size() * sizeof(T)));
+  allocs_.push_back(p);
+  DDSG_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return static_cast<const T*>(p);
+}
+
+bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
+  usable_ = false;
+  if (!hp.plain || hp.slot_k.size() != 1) return false;
+  const int d = hp.d;
+  if (d > kMaxDim) return false;
+  const int s0 = hp.slot_sub_begin[0], s1 = hp.slot_sub_end[0];
+  const int n_sub = s1 - s0;
+  int lmax = 1;
+  for (int s = s0; s < s1; ++s)
+    for (int j = 0; j < d; ++j) lmax = std::max<int>(lmax, hp.levels[hp.sub_lv_off[s] + j]);
+  if (lmax > 16) return false;
+  const size_t smem = static_cast<size_t>(d) * lmax * kThreads * (sizeof(double) + sizeof(uint16_t));
+  if (smem > 200 * 1024) return false;
+  std::vector<uint8_t> levels(static_cast<size_t>(n_sub) * d);
+  std::vector<int16_t> q(n_sub);
+  std::vector<int32_t> base(n_sub);
+  std::vector<uint8_t> full(n_sub);
+  for (int s = 0; s < n_sub; ++s) {
+    const uint8_t* lv = &hp.levels[hp.sub_lv_off[s0 + s]];
+    std::copy(lv, lv + d, &levels[static_cast<size_t>(s) * d]);
+    int qq = 0;
+    if (s > 0) {
+      const uint8_t* prev = &levels[static_cast<size_t>(s - 1) * d];
+      while (qq < d && prev[qq] == lv[qq]) ++qq;
+    }
+    q[s] = static_cast<int16_t>(qq);
+    int64_t cells = 1;
+    for (int j = 0; j < d; ++j) cells <<= (lv[j] - 1);
+    const int64_t slab_off = hp.sub_slab_off[s0 + s];
+    if (hp.sub_nodes[s0 + s] == cells) {
+      full[s] = 1;
+      base[s] = hp.slab[slab_off];
+    } else {
+      full[s] = 0;
+      base[s] = static_cast<int32_t>(slab_off);
+    }
+  }
+  d_ = d;
+  m_ = hp.m;
+  n_sub_ = n_sub;
+  lmax_ = lmax;
+  mode_ = hp.slot_mode[0];
+  runs_ = hp.slot_runs[0];
+  smem_ = smem;
+  levels_ = put(levels);
+  q_ = put(q);
+  base_ = put(base);
+  full_ = put(full);
+  slab_ = dev.slab;
+  row_run_ = dev.row_run;
+  surplus_ = dev.surplus;
+  usable_ = true;
+  return true;
+}
+
+template <int kDMax, int kMC>
+static void launch_plain(const Params& P, int exact, const double* x, int64_t n, int64_t base, double* y,
+                         unsigned long long* bad, cudaStream_t st, size_t smem) {
+  const unsigned grid = static_cast<unsigned>((n + kThreads - 1) / kThreads);
+  if (exact) {
+    DDSG_CUDA(cudaFuncSetAttribute(plain_kernel<kDMax, kMC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    plain_kernel<kDMax, kMC, 1><<<grid, kThreads, smem, st>>>(P, x, n, base, y, bad);
+  } else {
+    DDSG_CUDA(cudaFuncSetAttribute(plain_kernel<kDMax, kMC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    plain_kernel<kDMax, kMC, 0><<<grid, kThreads, smem, st>>>(P, x, n, base, y, bad);
+  }
+}
+
+int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, double* y,
+                          unsigned long long* bad, cudaStream_t st) const {
+  Params P{d_, m_, n_sub_, runs_, lmax_, mode_, levels_, q_, base_, full_, slab_, row_run_, surplus_};
+  kernel_timer().begin(st);
+  // column chunk: all outputs per thread when m is small
+  const int mc = m_ <= 1 ? 1 : (m_ <= 12 ? 12 : 24);
+  if (d_ <= 4) {
+    if (mc == 1) launch_plain<4, 1>(P, exact, x, n, base, y, bad, st, smem_);
+    else if (mc == 12) launch_plain<4, 12>(P, exact, x, n, base, y, bad, st, smem_);
+    else launch_plain<4, 24>(P, exact, x, n, base, y, bad, st, smem_);
+  } else if (d_ <= 10) {
+    if (mc == 1) launch_plain<10, 1>(P, exact, x, n, base, y, bad, st, smem_);
+    else if (mc == 12) launch_plain<10, 12>(P, exact, x, n, base, y, bad, st, smem_);
+    else launch_plain<10, 24>(P, exact, x, n, base, y, bad, st, smem_);
+  } else {
+    if (mc == 1) launch_plain<20, 1>(P, exact, x, n, base, y, bad, st, smem_);
+    else if (mc == 12) launch_plain<20, 12>(P, exact, x, n, base, y, bad, st, smem_);
+    else launch_plain<20, 24>(P, exact, x, n, base, y, bad, st, smem_);
+  }
+  kernel_timer().end(st);
+  DDSG_CUDA(cudaGetLastError());
+  return 1;
+}
+
+}  // namespace ddsg_b200

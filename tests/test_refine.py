@@ -92,3 +92,17 @@ def test_refine_step_two_gloo_ranks(tmp_path, world):
             assert np.array_equal(o[f"k{i}"], k2)
             assert np.array_equal(bits(o[f"s{i}"]), bits(s2))
     assert outs[0]["gathered"][0] > 0
+
+
+@pytest.mark.gpu
+def test_refine_step_gpu_hierarchize_equals_next_level_build():
+    """Same step with the new nodes hierarchized by the GPU kernels (EXACT,
+    stored order): bit-identical to the reference-exact build at the next level."""
+    grids = _grids(0)
+    cuts, f = _f_eval()
+    refine_step(grids, _level_sums(), f, dist=None, device=True)
+    for g, h in zip(grids, _grids(1)):
+        k1, s1 = g.nodes()
+        k2, s2 = h.nodes()
+        assert np.array_equal(k1, k2)
+        assert np.array_equal(bits(s1), bits(s2))
