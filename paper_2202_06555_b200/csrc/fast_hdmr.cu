@@ -373,12 +373,29 @@ __device__ __forceinline__ void leaf_full2(const unsigned char* table, double x0
   }
 }
 
+// The header fields every slot needs, fetched with four 16-byte loads.
+struct HeaderCore {
+  int32_t k, mode, nlev, d0, d1, tree_t, tree_s, b_kind;
+  double b;
+  uint32_t present, full;
+  int32_t table_off, slab_off, zero_row, fast_full;
+};
+static_assert(sizeof(HeaderCore) == 64, "header core");
+__device__ __forceinline__ HeaderCore load_core(const unsigned char* blk) {
+  HeaderCore h;
+  const uint4* src = reinterpret_cast<const uint4*>(blk);
+  uint4* dst = reinterpret_cast<uint4*>(&h);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dst[i] = src[i];
+  return h;
+}
+
 template <int kExact>
-__device__ __forceinline__ void leaf_dispatch(const SlotHeader& H, const unsigned char* blk, double x0, double x1,
-                                              double (&acc)[kCols]) {
-  const unsigned char* table = blk + H.table_off;
-  if (H.fast_full) {
-    switch (H.mode * 64 + H.k * 16 + H.nlev) {
+__device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHeader& H, const unsigned char* blk,
+                                              double x0, double x1, double (&acc)[kCols]) {
+  const unsigned char* table = blk + Hc.table_off;
+  if (Hc.fast_full) {
+    switch (Hc.mode * 64 + Hc.k * 16 + Hc.nlev) {
 #define DDSG_P1(MD, LV) \
   case MD * 64 + 16 + LV: \
     leaf_full1<kExact, MD, LV>(table, x0, acc); \
@@ -419,31 +436,31 @@ __device__ __forceinline__ void leaf_dispatch(const SlotHeader& H, const unsigne
   }
 }
 
-// Pending level i of the pairwise tree for this thread (levels >= 1).
+// Pending level i (>= 1) of the pairwise tree for this thread.
 struct TreeStore {
-  double2* smem;   // [kSmemLevels][kCols/2][kPoints]
+  double2* smem;   // [kSmemLevels][kCols/2][kPoints] (levels > kTmemLevels)
   uint32_t tbase;  // TMEM address of this warp's lane quarter / column block
   int tid;
   __device__ __forceinline__ void load(int i, double (&v)[kCols]) const {
-    if (i <= kSmemLevels) {
-      const double2* L = smem + (static_cast<int64_t>(i - 1) * (kCols / 2)) * kPoints + tid;
+    if (i <= kTmemLevels) {
+      tmem_load8(tbase + 16u * static_cast<uint32_t>(i - 1), v);
+    } else {
+      const double2* L = smem + (static_cast<int64_t>(i - kTmemLevels - 1) * (kCols / 2)) * kPoints + tid;
 #pragma unroll
       for (int q = 0; q < kCols / 2; ++q) {
         const double2 x = L[q * kPoints];
         v[2 * q] = x.x;
         v[2 * q + 1] = x.y;
       }
-    } else {
-      tmem_load8(tbase + 16u * static_cast<uint32_t>(i - kSmemLevels - 1), v);
     }
   }
   __device__ __forceinline__ void store(int i, const double (&v)[kCols]) const {
-    if (i <= kSmemLevels) {
-      double2* L = smem + (static_cast<int64_t>(i - 1) * (kCols / 2)) * kPoints + tid;
+    if (i <= kTmemLevels) {
+      tmem_store8(tbase + 16u * static_cast<uint32_t>(i - 1), v);
+    } else {
+      double2* L = smem + (static_cast<int64_t>(i - kTmemLevels - 1) * (kCols / 2)) * kPoints + tid;
 #pragma unroll
       for (int q = 0; q < kCols / 2; ++q) L[q * kPoints] = make_double2(v[2 * q], v[2 * q + 1]);
-    } else {
-      tmem_store8(tbase + 16u * static_cast<uint32_t>(i - kSmemLevels - 1), v);
     }
   }
 };
@@ -461,9 +478,9 @@ __global__ void __launch_bounds__(kPoints, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kStages);
   unsigned char* stages = smem + kHeaderBytes;
   double2* deep = reinterpret_cast<double2*>(stages + kStages * stage_bytes);
-  const int smem_levels = levels - 1 < kSmemLevels ? (levels - 1 > 0 ? levels - 1 : 0) : kSmemLevels;
+  const int smem_levels = min(max(levels - 1 - kTmemLevels, 0), kSmemLevels);
   int16_t* sdims = reinterpret_cast<int16_t*>(deep + static_cast<int64_t>(smem_levels) * (kCols / 2) * kPoints);
-  const bool use_tmem = levels - 1 > kSmemLevels;
+  const bool use_tmem = levels > 1;
 
   // CTA order: column blocks in groups of cb_group; within a group, the
   // group's column blocks of one point tile are adjacent.  Concurrent CTAs
@@ -524,34 +541,35 @@ __global__ void __launch_bounds__(kPoints, 1)
     mbar_wait(&bars[st], static_cast<uint32_t>((a / kStages) & 1));
     const unsigned char* blk = stages + st * stage_bytes;
     const SlotHeader& H = *reinterpret_cast<const SlotHeader*>(blk);
+    const HeaderCore Hc = load_core(blk);
     double acc[kCols];
 #pragma unroll
     for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
-    const int k = H.k;
+    const int k = Hc.k;
     const double x0 = xc0, x1 = xc1;
     if (a + 1 < n_active) {  // prefetch the next slot's coordinates
       xc0 = xt[static_cast<int64_t>(sdims[2 * (a + 1)]) * n + pc];
       xc1 = xt[static_cast<int64_t>(sdims[2 * (a + 1) + 1]) * n + pc];
     }
     if (k == 0) {
-      const double* r0 = reinterpret_cast<const double*>(blk + H.table_off);
+      const double* r0 = reinterpret_cast<const double*>(blk + Hc.table_off);
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = r0[c];
     } else {
-      leaf_dispatch<kExact>(H, blk, x0, x1, acc);
-      if (H.b_kind == 0) {
-        const double b = H.b;
+      leaf_dispatch<kExact>(Hc, H, blk, x0, x1, acc);
+      if (Hc.b_kind == 0) {
+        const double b = Hc.b;
 #pragma unroll
         for (int c = 0; c < kCols; ++c) acc[c] = __dmul_rn(acc[c], b);
-      } else if (H.b_kind == 2) {
+      } else if (Hc.b_kind == 2) {
 #pragma unroll
         for (int c = 0; c < kCols; ++c) acc[c] = -acc[c];
       }
     }
     // pairwise tree (perfect-tree embedding): merge with the pending left
     // siblings at levels s.. while the position bit is set, then park.
-    const int t = H.tree_t;
-    int i = H.tree_s;
+    const int t = Hc.tree_t;
+    int i = Hc.tree_s;
     if (i == 0 && i < levels) {
       if (t & 1) {
 #pragma unroll
@@ -787,7 +805,7 @@ bool FastHdmr::build(const HostProgram& hp) {
     const int64_t budget = int64_t{64} << 20;  // staged tables kept L2-resident per CTA wave
     cb_group_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_cb_, budget / std::max<int64_t>(per_cb, 1))));
   }
-  const int64_t deep_bytes = std::min(std::max(0, levels - 1), kSmemLevels) * int64_t{kCols} * kPoints * 8;
+  const int64_t deep_bytes = std::min(std::max(0, levels - 1 - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
   const int64_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
   if (smem > 227 * 1024) {
     why_ = "shared-memory footprint too large";
@@ -851,7 +869,7 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   transpose_check_kernel<<<tgrid, dim3(32, 8), 0, st>>>(x, n, d_, base, xt, bad);
   DDSG_CUDA(cudaGetLastError());
   const int64_t tiles = (n + kPoints - 1) / kPoints;
-  const int64_t deep_bytes = std::min(std::max(0, levels_ - 1), kSmemLevels) * int64_t{kCols} * kPoints * 8;
+  const int64_t deep_bytes = std::min(std::max(0, levels_ - 1 - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
   const size_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * static_cast<size_t>(n_active_) + 15) / 16 * 16;
   const dim3 grid(static_cast<unsigned>(tiles * n_cb_));
   kernel_timer().begin(st);

@@ -13,10 +13,10 @@
 //    shared-memory broadcast path delivers 256 B/clk/SM.
 //  * Leaf (slot) values enter the reference's pairwise tree through a
 //    perfect-binary-tree embedding (leaf a at position t_a spanning 2^s_a):
-//    pending level 0 lives in registers, levels 1..kSmemLevels in shared
-//    memory, deeper (rarely touched) levels in tensor memory: each thread
-//    owns TMEM lane (its lane in the warp's lane quarter) and 16 columns per
-//    level (tcgen05.st/ld 32x32b.x16).
+//    pending level 0 lives in registers, levels 1..8 in tensor memory (each
+//    thread owns its TMEM lane in the warp's lane quarter, 16 columns per
+//    level, tcgen05.st/ld 32x32b.x16 -- off the shared-memory pipe that the
+//    gathers saturate), the rarely touched levels >= 9 in shared memory.
 //  * EXACT mode: DMUL then DADD per term (bit-identical to the reference);
 //    FAST mode: one DFMA per term.
 #pragma once
@@ -41,9 +41,9 @@ constexpr int kL1 = 10;                  // max level of order-1 slots
 constexpr int kL2 = 6;                   // max level (per dim) of order-2 slots
 constexpr int kSub2 = kL2 * (kL2 + 1) / 2;  // canonical subspaces of a full order-2 grid
 constexpr int kMaxSub = kSub2 > kL1 ? kSub2 : kL1;
-constexpr int kSmemLevels = 4;           // tree levels 1..4 in shared memory (level 0 in registers)
-constexpr int kTmemLevels = 8;           // levels 5..12 in tensor memory (128 columns per warp)
-constexpr int kMaxLevels = 1 + kSmemLevels + kTmemLevels;  // 2^14 active slots
+constexpr int kTmemLevels = 8;           // tree levels 1..8 in tensor memory (128 columns per warp)
+constexpr int kSmemLevels = 4;           // levels 9..12 in shared memory (level 0 in registers)
+constexpr int kMaxLevels = 1 + kTmemLevels + kSmemLevels;  // 2^13 active slots
 constexpr int kStages = 4;
 constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
 
