@@ -524,9 +524,7 @@ __global__ void __launch_bounds__(kPoints, 1)
   double xc0 = xt[static_cast<int64_t>(sdims[0]) * n + pc];
   double xc1 = xt[static_cast<int64_t>(sdims[1]) * n + pc];
   double L0[kCols];
-  double root[kCols];
-#pragma unroll
-  for (int c = 0; c < kCols; ++c) root[c] = 0.0;
+  const int c0 = cb * kCols;
 
   for (int a = 0; a < n_active; ++a) {
     const int st = a % kStages;
@@ -591,20 +589,15 @@ __global__ void __launch_bounds__(kPoints, 1)
       }
       if (i < levels) {
         store.store(i, acc);
-      } else {
+      } else if (valid) {  // the root: written out directly (keeps no registers live)
+        double* yp = y + p * m + c0;
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) root[c] = acc[c];
+        for (int c = 0; c < kCols; ++c)
+          if (c0 + c < m) yp[c] = acc[c];
       }
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
-  }
-  if (valid) {
-    const int c0 = cb * kCols;
-    double* yp = y + p * m + c0;
-#pragma unroll
-    for (int c = 0; c < kCols; ++c)
-      if (c0 + c < m) yp[c] = root[c];
   }
   if (use_tmem) {
     tmem_fence_before();
