@@ -442,10 +442,10 @@ struct TreeStore {
   uint32_t tbase;  // TMEM address of this warp's lane quarter / column block
   int tid;
   __device__ __forceinline__ void load(int i, double (&v)[kCols]) const {
-    if (i <= kTmemLevels) {
-      tmem_load8(tbase + 16u * static_cast<uint32_t>(i - 1), v);
+    if (i < kTmemLevels) {
+      tmem_load8(tbase + 16u * static_cast<uint32_t>(i), v);
     } else {
-      const double2* L = smem + (static_cast<int64_t>(i - kTmemLevels - 1) * (kCols / 2)) * kPoints + tid;
+      const double2* L = smem + (static_cast<int64_t>(i - kTmemLevels) * (kCols / 2)) * kPoints + tid;
 #pragma unroll
       for (int q = 0; q < kCols / 2; ++q) {
         const double2 x = L[q * kPoints];
@@ -455,10 +455,10 @@ struct TreeStore {
     }
   }
   __device__ __forceinline__ void store(int i, const double (&v)[kCols]) const {
-    if (i <= kTmemLevels) {
-      tmem_store8(tbase + 16u * static_cast<uint32_t>(i - 1), v);
+    if (i < kTmemLevels) {
+      tmem_store8(tbase + 16u * static_cast<uint32_t>(i), v);
     } else {
-      double2* L = smem + (static_cast<int64_t>(i - kTmemLevels - 1) * (kCols / 2)) * kPoints + tid;
+      double2* L = smem + (static_cast<int64_t>(i - kTmemLevels) * (kCols / 2)) * kPoints + tid;
 #pragma unroll
       for (int q = 0; q < kCols / 2; ++q) L[q * kPoints] = make_double2(v[2 * q], v[2 * q + 1]);
     }
@@ -478,9 +478,9 @@ __global__ void __launch_bounds__(kPoints, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kStages);
   unsigned char* stages = smem + kHeaderBytes;
   double2* deep = reinterpret_cast<double2*>(stages + kStages * stage_bytes);
-  const int smem_levels = min(max(levels - 1 - kTmemLevels, 0), kSmemLevels);
+  const int smem_levels = min(max(levels - kTmemLevels, 0), kSmemLevels);
   int16_t* sdims = reinterpret_cast<int16_t*>(deep + static_cast<int64_t>(smem_levels) * (kCols / 2) * kPoints);
-  const bool use_tmem = levels > 1;
+  const bool use_tmem = levels > 0;
 
   // CTA order: column blocks in groups of cb_group; within a group, the
   // group's column blocks of one point tile are adjacent.  Concurrent CTAs
@@ -523,7 +523,6 @@ __global__ void __launch_bounds__(kPoints, 1)
 
   double xc0 = xt[static_cast<int64_t>(sdims[0]) * n + pc];
   double xc1 = xt[static_cast<int64_t>(sdims[1]) * n + pc];
-  double L0[kCols];
   const int c0 = cb * kCols;
 
   for (int a = 0; a < n_active; ++a) {
@@ -568,18 +567,7 @@ __global__ void __launch_bounds__(kPoints, 1)
     // siblings at levels s.. while the position bit is set, then park.
     const int t = Hc.tree_t;
     int i = Hc.tree_s;
-    if (i == 0 && i < levels) {
-      if (t & 1) {
-#pragma unroll
-        for (int c = 0; c < kCols; ++c) acc[c] = __dadd_rn(L0[c], acc[c]);
-        i = 1;
-      } else {
-#pragma unroll
-        for (int c = 0; c < kCols; ++c) L0[c] = acc[c];
-        i = -1;  // parked
-      }
-    }
-    if (i >= 0) {
+    {
       while (i < levels && ((t >> i) & 1)) {
         double v[kCols];
         store.load(i, v);
@@ -798,7 +786,7 @@ bool FastHdmr::build(const HostProgram& hp) {
     const int64_t budget = int64_t{64} << 20;  // staged tables kept L2-resident per CTA wave
     cb_group_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_cb_, budget / std::max<int64_t>(per_cb, 1))));
   }
-  const int64_t deep_bytes = std::min(std::max(0, levels - 1 - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
+  const int64_t deep_bytes = std::min(std::max(0, levels - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
   const int64_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
   if (smem > 227 * 1024) {
     why_ = "shared-memory footprint too large";
@@ -862,7 +850,7 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   transpose_check_kernel<<<tgrid, dim3(32, 8), 0, st>>>(x, n, d_, base, xt, bad);
   DDSG_CUDA(cudaGetLastError());
   const int64_t tiles = (n + kPoints - 1) / kPoints;
-  const int64_t deep_bytes = std::min(std::max(0, levels_ - 1 - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
+  const int64_t deep_bytes = std::min(std::max(0, levels_ - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
   const size_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * static_cast<size_t>(n_active_) + 15) / 16 * 16;
   const dim3 grid(static_cast<unsigned>(tiles * n_cb_));
   kernel_timer().begin(st);

@@ -43,7 +43,7 @@ constexpr int kSub2 = kL2 * (kL2 + 1) / 2;  // canonical subspaces of a full ord
 constexpr int kMaxSub = kSub2 > kL1 ? kSub2 : kL1;
 constexpr int kTmemLevels = 8;           // tree levels 1..8 in tensor memory (128 columns per warp)
 constexpr int kSmemLevels = 4;           // levels 9..12 in shared memory (level 0 in registers)
-constexpr int kMaxLevels = 1 + kTmemLevels + kSmemLevels;  // 2^13 active slots
+constexpr int kMaxLevels = kTmemLevels + kSmemLevels;  // 2^12 active slots
 constexpr int kStages = 4;
 constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
 
