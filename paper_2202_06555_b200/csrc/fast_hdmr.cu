@@ -471,13 +471,13 @@ __global__ void __launch_bounds__(kPoints, 1)
                      const int32_t* __restrict__ block_len, const int16_t* __restrict__ slot_dims,
                      int n_active, int n_cb, int cb_group, int levels, const double* __restrict__ xt, int64_t n,
                      int m,
-                     double* __restrict__ y, int64_t stage_bytes) {
+                     double* __restrict__ y, int64_t stage_bytes, int n_stages) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [kStages] full, [kStages] empty
-  uint64_t* empty = bars + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kStages);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [kMaxStages] full, [kMaxStages] empty
+  uint64_t* empty = bars + kMaxStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
   unsigned char* stages = smem + kHeaderBytes;
-  double2* deep = reinterpret_cast<double2*>(stages + kStages * stage_bytes);
+  double2* deep = reinterpret_cast<double2*>(stages + n_stages * stage_bytes);
   const int smem_levels = min(max(levels - kTmemLevels, 0), kSmemLevels);
   int16_t* sdims = reinterpret_cast<int16_t*>(deep + static_cast<int64_t>(smem_levels) * (kCols / 2) * kPoints);
   const bool use_tmem = levels > 0;
@@ -502,12 +502,12 @@ __global__ void __launch_bounds__(kPoints, 1)
   const int32_t* lens = block_len + static_cast<int64_t>(cb) * n_active;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < n_stages; ++s) {
       mbar_init(&bars[s], 1);
       mbar_init(&empty[s], kWarps);
     }
     fence_mbar_init();
-    for (int s = 0; s < kStages && s < n_active; ++s) {
+    for (int s = 0; s < n_stages && s < n_active; ++s) {
       mbar_expect_tx(&bars[s], static_cast<uint32_t>(lens[s]));
       bulk_g2s(stages + s * stage_bytes, blocks + offs[s], static_cast<uint32_t>(lens[s]), &bars[s]);
     }
@@ -525,17 +525,20 @@ __global__ void __launch_bounds__(kPoints, 1)
   double xc1 = xt[static_cast<int64_t>(sdims[1]) * n + pc];
   const int c0 = cb * kCols;
 
+  // ring position of slot a (st) and of slot a-1 (pst), with their phase
+  // parities, advanced incrementally (no runtime division per slot)
+  int st = 0, pst = n_stages - 1;
+  uint32_t ph = 0, pph = 1;
   for (int a = 0; a < n_active; ++a) {
-    const int st = a % kStages;
-    if (tid == 0 && a >= 1 && a - 1 + kStages < n_active) {
+    if (tid == 0 && a >= 1 && a - 1 + n_stages < n_active) {
       // refill the stage released by slot a-1 (all warps arrived on its empty barrier)
-      const int b = a - 1, sb = b % kStages, nxt = b + kStages;
-      mbar_wait(&empty[sb], static_cast<uint32_t>((b / kStages) & 1));
+      const int nxt = a - 1 + n_stages;
+      mbar_wait(&empty[pst], pph);
       fence_proxy_async();
-      mbar_expect_tx(&bars[sb], static_cast<uint32_t>(lens[nxt]));
-      bulk_g2s(stages + sb * stage_bytes, blocks + offs[nxt], static_cast<uint32_t>(lens[nxt]), &bars[sb]);
+      mbar_expect_tx(&bars[pst], static_cast<uint32_t>(lens[nxt]));
+      bulk_g2s(stages + pst * stage_bytes, blocks + offs[nxt], static_cast<uint32_t>(lens[nxt]), &bars[pst]);
     }
-    mbar_wait(&bars[st], static_cast<uint32_t>((a / kStages) & 1));
+    mbar_wait(&bars[st], ph);
     const unsigned char* blk = stages + st * stage_bytes;
     const SlotHeader& H = *reinterpret_cast<const SlotHeader*>(blk);
     const HeaderCore Hc = load_core(blk);
@@ -586,6 +589,12 @@ __global__ void __launch_bounds__(kPoints, 1)
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
+    pst = st;
+    pph = ph;
+    if (++st == n_stages) {
+      st = 0;
+      ph ^= 1u;
+    }
   }
   if (use_tmem) {
     tmem_fence_before();
@@ -787,8 +796,10 @@ bool FastHdmr::build(const HostProgram& hp) {
     cb_group_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_cb_, budget / std::max<int64_t>(per_cb, 1))));
   }
   const int64_t deep_bytes = std::min(std::max(0, levels - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
-  const int64_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
-  if (smem > 227 * 1024) {
+  const int64_t fixed = kHeaderBytes + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
+  n_stages_ = static_cast<int>(std::min<int64_t>(kMaxStages, (227 * 1024 - fixed) / block_bytes_));
+  const int64_t smem = fixed + int64_t{n_stages_} * block_bytes_;
+  if (n_stages_ < 2 || smem > 227 * 1024) {
     why_ = "shared-memory footprint too large";
     return false;
   }
@@ -851,17 +862,17 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   DDSG_CUDA(cudaGetLastError());
   const int64_t tiles = (n + kPoints - 1) / kPoints;
   const int64_t deep_bytes = std::min(std::max(0, levels_ - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
-  const size_t smem = kHeaderBytes + kStages * block_bytes_ + deep_bytes + (4 * static_cast<size_t>(n_active_) + 15) / 16 * 16;
+  const size_t smem = kHeaderBytes + n_stages_ * block_bytes_ + deep_bytes + (4 * static_cast<size_t>(n_active_) + 15) / 16 * 16;
   const dim3 grid(static_cast<unsigned>(tiles * n_cb_));
   kernel_timer().begin(st);
   if (exact)
     fast_hdmr_kernel<1><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
                                                      block_len_, slot_dims_, n_active_, n_cb_, cb_group_, levels_, xt, n, m_, y,
-                                                     block_bytes_);
+                                                     block_bytes_, n_stages_);
   else
     fast_hdmr_kernel<0><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
                                                      block_len_, slot_dims_, n_active_, n_cb_, cb_group_, levels_, xt, n, m_, y,
-                                                     block_bytes_);
+                                                     block_bytes_, n_stages_);
   kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());
   return 2;

@@ -44,7 +44,7 @@ constexpr int kMaxSub = kSub2 > kL1 ? kSub2 : kL1;
 constexpr int kTmemLevels = 8;           // tree levels 1..8 in tensor memory (128 columns per warp)
 constexpr int kSmemLevels = 4;           // levels 9..12 in shared memory (level 0 in registers)
 constexpr int kMaxLevels = kTmemLevels + kSmemLevels;  // 2^12 active slots
-constexpr int kStages = 4;
+constexpr int kMaxStages = 4;            // shared-memory ring depth (fewer when slot blocks are large)
 constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
 
 // Per-slot header at the front of every staged block (16-B aligned, 160 B).
@@ -92,7 +92,7 @@ class FastHdmr {
  private:
   bool usable_ = false;
   std::string why_;
-  int d_ = 0, m_ = 0, n_cb_ = 0, cb_group_ = 1, n_active_ = 0, levels_ = 0;
+  int d_ = 0, m_ = 0, n_cb_ = 0, cb_group_ = 1, n_active_ = 0, levels_ = 0, n_stages_ = fast::kMaxStages;
   int64_t block_bytes_ = 0;  // stage size (max block), multiple of 128
   void* blocks_ = nullptr;   // [n_cb][n_active] blocks of block_bytes_ each (offsets below)
   int64_t* block_off_ = nullptr;  // device: [n_cb * n_active] byte offsets

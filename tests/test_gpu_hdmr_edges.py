@@ -1,0 +1,144 @@
+"""Edge cases of the HDMR evaluation path (slot kernel and its fallbacks),
+each checked bit for bit against the CPU oracle on the same grid bits.
+
+Grids are full grids with seeded random surpluses (the evaluation path does
+not care how surpluses were obtained), so every case is cheap to set up."""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from helpers import bits
+from paper_2202_06555_b200.ddsg import (MODIFIED_LINEAR, ZERO_BOUNDARY, SparseGridFunction, VectorizedDdsg,
+                                        uniform_points)
+from paper_2202_06555_b200.workloads import telescoping_b
+
+pytestmark = pytest.mark.gpu
+
+
+def full_keys(k: int, L: int) -> np.ndarray:
+    """All nodes of the regular k-dim grid of level L in canonical order."""
+    out = []
+    for s in range(k, L + k):
+        for lv in itertools.product(range(1, L + 1), repeat=k):
+            if sum(lv) != s:
+                continue
+            for cells in itertools.product(*[range(1 << (l - 1)) for l in lv]):
+                out.append([(1 << (l - 1)) + c for l, c in zip(lv, cells)])
+    return np.array(sorted(out, key=lambda key: (sum(int(v).bit_length() for v in key), key)), dtype=np.uint32)
+
+
+def make(d, m, family, levels, mode=MODIFIED_LINEAR, b=None, seed=0, poison=None):
+    rng = np.random.default_rng(seed)
+    b = telescoping_b(family) if b is None else b
+    slots_o, slots_g = [], []
+    fa = rng.uniform(-1, 1, m)
+    for u, bu in zip(family, b):
+        if not u:
+            slots_o.append((u, bu, None))
+            slots_g.append((u, bu, None))
+            continue
+        keys = full_keys(len(u), levels[len(u)])
+        sur = rng.uniform(-1, 1, (len(keys), m))
+        if poison is not None and u == poison[0]:
+            sur[poison[1] % len(keys), poison[2] % m] = poison[3]
+        slots_o.append((u, bu, (mode, keys, sur)))
+        slots_g.append((u, bu, SparseGridFunction.from_nodes(len(u), m, levels[len(u)], 0.0, mode, keys, sur)))
+    vec = VectorizedDdsg.compile(d, m, fa, slots_g)
+    return vec, fa, slots_o
+
+
+def check(vec, d, m, fa, slots_o, x, nan_ok=False):
+    rc, want, _ = O.port_hdmr_eval(d, m, fa, slots_o, x)
+    assert rc == 0
+    y = vec.evaluate_batch(x)
+    if nan_ok:
+        assert np.array_equal(np.isnan(y), np.isnan(want))
+        mask = ~np.isnan(want)
+        assert np.array_equal(bits(y[mask]), bits(want[mask]))
+    else:
+        assert np.array_equal(bits(y), bits(want))
+    nnz_o, h_o = O.port_hdmr_support(d, m, slots_o, x)
+    nnz, h = vec.support(x)
+    assert np.array_equal(nnz, nnz_o) and np.array_equal(h, h_o)
+
+
+def pts(d, n=700, seed=5):
+    x = uniform_points(seed, n, d)
+    x[:6] = np.array([0.0, 1.0, 0.5, 0.25, 1 - 2.0 ** -53, 2.0 ** -40])[:, None]
+    return x
+
+
+def family_1d_2d(d, pairs):
+    return [()] + [(j,) for j in range(d)] + sorted(pairs)
+
+
+def test_only_anchor_slot():
+    d, m = 3, 5
+    vec, fa, so = make(d, m, [()], {})
+    check(vec, d, m, fa, so, pts(d))
+
+
+def test_empty_batch():
+    vec, fa, so = make(4, 3, family_1d_2d(4, [(0, 1)]), {1: 4, 2: 3})
+    assert vec.evaluate_batch(np.zeros((0, 4))).shape == (0, 3)
+
+
+@pytest.mark.parametrize("mode", [ZERO_BOUNDARY, MODIFIED_LINEAR])
+@pytest.mark.parametrize("m", [1, 8, 9, 23])
+def test_modes_and_column_blocks(mode, m):
+    d = 6
+    fam = family_1d_2d(d, [(0, 1), (1, 2), (2, 5), (3, 4)])
+    vec, fa, so = make(d, m, fam, {1: 6, 2: 4}, mode=mode, seed=m)
+    assert vec.uses_slot_kernel()
+    check(vec, d, m, fa, so, pts(d))
+
+
+def test_b_kinds():
+    # b = 1, -1, 2 (power of two), -3 (general DMUL), 0 (skipped)
+    d, m = 4, 7
+    fam = family_1d_2d(d, [(0, 1), (2, 3)])
+    b = [5, 1, -1, 2, -3, 1, 0]
+    vec, fa, so = make(d, m, fam, {1: 5, 2: 3}, b=b)
+    check(vec, d, m, fa, so, pts(d))
+
+
+def test_non_finite_surplus_takes_general_path():
+    d, m = 4, 3
+    fam = family_1d_2d(d, [(0, 1)])
+    vec, fa, so = make(d, m, fam, {1: 5, 2: 3}, poison=((0, 1), 7, 1, np.inf))
+    check(vec, d, m, fa, so, pts(d), nan_ok=True)
+
+
+@pytest.mark.parametrize("L1,expect_slot_kernel", [(10, True), (11, False)])
+def test_deep_1d_cuts(L1, expect_slot_kernel):
+    d, m = 3, 9
+    fam = family_1d_2d(d, [(0, 2)])
+    vec, fa, so = make(d, m, fam, {1: L1, 2: 4})
+    assert vec.uses_slot_kernel() == expect_slot_kernel
+    check(vec, d, m, fa, so, pts(d, 400))
+
+
+def test_order3_slots_fall_back_exactly():
+    d, m = 4, 5
+    fam = [()] + [(j,) for j in range(d)] + [(0, 1), (0, 2), (1, 2)] + [(0, 1, 2)]
+    vec, fa, so = make(d, m, fam, {1: 4, 2: 3, 3: 3})
+    assert not vec.uses_slot_kernel()
+    check(vec, d, m, fa, so, pts(d, 300))
+
+
+def test_many_slots_deep_tree():
+    # 1 + 60 + 200 slots -> 9 tree levels (TMEM + shared-memory levels)
+    d, m = 60, 3
+    rng = np.random.default_rng(1)
+    pairs = set()
+    while len(pairs) < 200:
+        a, b = sorted(rng.choice(d, 2, replace=False).tolist())
+        pairs.add((a, b))
+    fam = family_1d_2d(d, pairs)
+    vec, fa, so = make(d, m, fam, {1: 3, 2: 2})
+    assert vec.uses_slot_kernel()
+    check(vec, d, m, fa, so, pts(d, 600))
