@@ -27,6 +27,9 @@
 #include "ddsg/runtime.hpp"
 #include "ddsg/sparse_grid.hpp"
 #include "oracles.hpp"
+#ifdef DDSG_REF_WITH_JSON
+#include "ddsg/serialize.hpp"  // needs nlohmann json.hpp
+#endif
 
 using namespace ddsg;
 
@@ -308,6 +311,39 @@ void ref_decomp_anchor(const ref_decomp* h, double* f_anchor) {
   const auto& fa = h->src->anchor().f_anchor;
   std::copy(fa.begin(), fa.end(), f_anchor);
 }
+
+#ifdef DDSG_REF_WITH_JSON
+// serialize.hpp:31-145: to_json / sparse_grid_from_json / ddsg_from_json.
+// Returned strings are owned by the driver until the next call on this thread.
+thread_local std::string g_json;
+const char* ref_grid_to_json(const ref_grid* g) {
+  g_json = to_json(g->g).dump();
+  return g_json.c_str();
+}
+int ref_grid_from_json(const char* text, ref_grid** out) {
+  return guarded([&] {
+    auto h = std::make_unique<ref_grid>();
+    h->g = sparse_grid_from_json(nlohmann::json::parse(text));
+    *out = h.release();
+  });
+}
+const char* ref_decomp_to_json(const ref_decomp* h) {
+  g_json = to_json(*h->src).dump();
+  return g_json.c_str();
+}
+// ddsg_from_json + compile; evaluation through ref_hdmr_eval.
+int ref_hdmr_from_json(const char* text, ref_hdmr** out) {
+  return guarded([&] {
+    auto h = std::make_unique<ref_hdmr>();
+    h->src = std::make_shared<const DdsgFunction>(ddsg_from_json(nlohmann::json::parse(text)));
+    h->vec = VectorizedDdsg::compile(h->src);
+    *out = h.release();
+  });
+}
+int ref_json_enabled() { return 1; }
+#else
+int ref_json_enabled() { return 0; }
+#endif
 
 // oracle::uniform_points (proj/tests/oracles.hpp:45-53), point-major.
 void ref_uniform_points(int dim, int64_t count, uint64_t seed, double* out) {

@@ -99,6 +99,16 @@ def ref():
         L.ref_sg_node_count_bruteforce.restype = _u64
         L.ref_sg_node_count_bruteforce.argtypes = [_i, _i]
         L.ref_default_workers.restype = C.c_uint
+        L.ref_json_enabled.restype = _i
+        if L.ref_json_enabled():
+            L.ref_grid_to_json.restype = C.c_char_p
+            L.ref_grid_to_json.argtypes = [_p]
+            L.ref_grid_from_json.restype = _i
+            L.ref_grid_from_json.argtypes = [C.c_char_p, C.POINTER(_p)]
+            L.ref_decomp_to_json.restype = C.c_char_p
+            L.ref_decomp_to_json.argtypes = [_p]
+            L.ref_hdmr_from_json.restype = _i
+            L.ref_hdmr_from_json.argtypes = [C.c_char_p, C.POINTER(_p)]
         _ref = L
     return _ref
 
@@ -266,7 +276,8 @@ class RefHdmr:
         return q
 
 
-def ref_decompose(d, m, k_max, max_level, fn_addr, ctx=None, eps_rho=0.0, eps_eta=0.0, eps_gamma=0.0, mode=1):
+def ref_decompose(d, m, k_max, max_level, fn_addr, ctx=None, eps_rho=0.0, eps_eta=0.0, eps_gamma=0.0, mode=1,
+                  want_json=False):
     """Runs the reference decompose (center anchor) and returns
     (f_anchor, [(dims, b, keys, surplus) ...] in coeff_b order)."""
     L = ref()
@@ -288,5 +299,6 @@ def ref_decompose(d, m, k_max, max_level, fn_addr, ctx=None, eps_rho=0.0, eps_et
             out.append((dims, b.value, keys, sur))
         else:
             out.append((dims, b.value, None, None))
+    text = L.ref_decomp_to_json(h).decode() if want_json else None
     L.ref_decomp_free(h)
-    return fa, out
+    return (fa, out, text) if want_json else (fa, out)
