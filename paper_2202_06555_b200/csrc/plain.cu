@@ -25,15 +25,17 @@ namespace ddsg_b200 {
 
 namespace plain {
 
+// One 32-byte record per subspace, read with two warp-uniform 16-byte loads:
+//   w[0] = first row (full subspace) or slab offset (partial)
+//   w[1] = q (first dim to recompute) | full << 8
+//   w[2..7] = levels as 4-bit nibbles, dim j in word 2 + j/8, bits 4*(j%8)
 struct Params {
   int d, m, n_sub, runs, lmax, mode;
-  const uint8_t* levels;   // [n_sub][d]
-  const int16_t* q;        // [n_sub] first dim to recompute
-  const int32_t* base;     // [n_sub] first row (full) or slab offset (partial)
-  const uint8_t* full;     // [n_sub]
+  const uint4* rec;        // [n_sub][2]
   const int32_t* slab;     // partial subspaces: cell -> row or -1
   const int16_t* row_run;  // [rows]
-  const double* surplus;   // [rows][m]
+  const double* surplus;   // [rows][ms] (ms = m rounded up to even: 16-byte rows)
+  int ms;
 };
 
 // kTable: 1 = 1-d factors from a per-thread shared-memory table, 0 =
@@ -85,12 +87,15 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         pc[j] = 0u;
       }
       for (int s = 0; s < P.n_sub; ++s) {
-        const int q = P.q[s];
-        const uint8_t* lv = P.levels + static_cast<int64_t>(s) * d;
+        const uint4 r0 = __ldg(P.rec + 2 * s);
+        uint4 r1 = make_uint4(0u, 0u, 0u, 0u);
+        if (kDMax > 16) r1 = __ldg(P.rec + 2 * s + 1);
+        const int q = static_cast<int>(r0.y & 0xffu);
+        const uint32_t lw[6] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
         for (int j = 0; j < kDMax; ++j) {
           if (j >= q && j < d) {
-            const int l = lv[j];
+            const int l = static_cast<int>((lw[j / 8] >> (4 * (j % 8))) & 15u);
             double v;
             uint32_t kk;
             if (kTable) {
@@ -115,19 +120,27 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         }
         const double w = pw[kDMax - 1];
         if (w == 0.0) continue;  // support test (sparse_grid.hpp:123)
-        int row = P.base[s];
-        if (P.full[s])
+        int row = static_cast<int>(r0.x);
+        if ((r0.y >> 8) & 1u)
           row += static_cast<int>(pc[kDMax - 1]);
         else
           row = P.slab[row + static_cast<int>(pc[kDMax - 1])];
         if (row < 0) continue;
         if (P.runs > 1 && P.row_run[row] != run) continue;
-        const double* sr = P.surplus + static_cast<int64_t>(row) * P.m + c0;
+        const double* sr = P.surplus + static_cast<int64_t>(row) * P.ms + c0;
+        if (kMC == 1) {
+          const double sv = __ldg(sr);
+          acc[0] = kExact ? __dadd_rn(acc[0], __dmul_rn(w, sv)) : __fma_rn(w, sv, acc[0]);
+        } else {
+          // 16-byte loads: one L1 sector request per lane per two columns
 #pragma unroll
-        for (int c = 0; c < kMC; ++c) {
-          if (c < nc) {
-            const double sv = __ldg(sr + c);
-            acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w, sv)) : __fma_rn(w, sv, acc[c]);
+          for (int c = 0; c < kMC; c += 2) {
+            if (c < nc) {
+              const double2 sv = __ldg(reinterpret_cast<const double2*>(sr + c));
+              acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w, sv.x)) : __fma_rn(w, sv.x, acc[c]);
+              if (kMC > 1)
+                acc[c + 1] = kExact ? __dadd_rn(acc[c + 1], __dmul_rn(w, sv.y)) : __fma_rn(w, sv.y, acc[c + 1]);
+            }
           }
         }
       }
@@ -170,29 +183,23 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   if (lmax > 16) return false;
   const size_t smem = static_cast<size_t>(d) * lmax * kThreads * (sizeof(double) + sizeof(uint16_t));
   if (smem > 200 * 1024) return false;
-  std::vector<uint8_t> levels(static_cast<size_t>(n_sub) * d);
-  std::vector<int16_t> q(n_sub);
-  std::vector<int32_t> base(n_sub);
-  std::vector<uint8_t> full(n_sub);
+  if (lmax > 15) return false;  // 4-bit level nibbles
+  std::vector<uint32_t> rec(static_cast<size_t>(n_sub) * 8, 0u);
   for (int s = 0; s < n_sub; ++s) {
     const uint8_t* lv = &hp.levels[hp.sub_lv_off[s0 + s]];
-    std::copy(lv, lv + d, &levels[static_cast<size_t>(s) * d]);
     int qq = 0;
     if (s > 0) {
-      const uint8_t* prev = &levels[static_cast<size_t>(s - 1) * d];
+      const uint8_t* prev = &hp.levels[hp.sub_lv_off[s0 + s - 1]];
       while (qq < d && prev[qq] == lv[qq]) ++qq;
     }
-    q[s] = static_cast<int16_t>(qq);
     int64_t cells = 1;
     for (int j = 0; j < d; ++j) cells <<= (lv[j] - 1);
     const int64_t slab_off = hp.sub_slab_off[s0 + s];
-    if (hp.sub_nodes[s0 + s] == cells) {
-      full[s] = 1;
-      base[s] = hp.slab[slab_off];
-    } else {
-      full[s] = 0;
-      base[s] = static_cast<int32_t>(slab_off);
-    }
+    const bool is_full = hp.sub_nodes[s0 + s] == cells;
+    uint32_t* r = &rec[static_cast<size_t>(s) * 8];
+    r[0] = static_cast<uint32_t>(is_full ? hp.slab[slab_off] : slab_off);
+    r[1] = static_cast<uint32_t>(qq) | (is_full ? 0x100u : 0u);
+    for (int j = 0; j < d; ++j) r[2 + j / 8] |= static_cast<uint32_t>(lv[j]) << (4 * (j % 8));
   }
   d_ = d;
   m_ = hp.m;
@@ -201,13 +208,19 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   mode_ = hp.slot_mode[0];
   runs_ = hp.slot_runs[0];
   smem_ = smem;
-  levels_ = put(levels);
-  q_ = put(q);
-  base_ = put(base);
-  full_ = put(full);
+  rec_ = reinterpret_cast<const uint4*>(put(rec));
+  // row-padded copy of the surpluses (even stride -> 16-byte aligned rows)
+  ms_ = hp.m == 1 ? 1 : (hp.m + 1) / 2 * 2;
+  if (ms_ != hp.m) {
+    std::vector<double> pad(static_cast<size_t>(hp.rows) * ms_, 0.0);
+    for (int64_t r = 0; r < hp.rows; ++r)
+      std::copy(hp.surplus.begin() + r * hp.m, hp.surplus.begin() + (r + 1) * hp.m, pad.begin() + r * ms_);
+    surplus_ = put(pad);
+  } else {
+    surplus_ = dev.surplus;
+  }
   slab_ = dev.slab;
   row_run_ = dev.row_run;
-  surplus_ = dev.surplus;
   usable_ = true;
   return true;
 }
@@ -232,7 +245,7 @@ static void launch_plain(const Params& P, int exact, const double* x, int64_t n,
 
 int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, double* y,
                           unsigned long long* bad, cudaStream_t st) const {
-  Params P{d_, m_, n_sub_, runs_, lmax_, mode_, levels_, q_, base_, full_, slab_, row_run_, surplus_};
+  Params P{d_, m_, n_sub_, runs_, lmax_, mode_, rec_, slab_, row_run_, surplus_, ms_};
   kernel_timer().begin(st);
   // column chunk: all outputs per thread when m is small
   const int mc = m_ <= 1 ? 1 : (m_ <= 12 ? 12 : 24);

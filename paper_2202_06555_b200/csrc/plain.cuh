@@ -32,12 +32,9 @@ class PlainGrid {
 
  private:
   bool usable_ = false;
-  int d_ = 0, m_ = 0, n_sub_ = 0, lmax_ = 0, mode_ = 0, runs_ = 1;
+  int d_ = 0, m_ = 0, ms_ = 0, n_sub_ = 0, lmax_ = 0, mode_ = 0, runs_ = 1;
   size_t smem_ = 0;
-  const uint8_t* levels_ = nullptr;
-  const int16_t* q_ = nullptr;
-  const int32_t* base_ = nullptr;
-  const uint8_t* full_ = nullptr;
+  const uint4* rec_ = nullptr;  // [n_sub][2] packed subspace records
   const int32_t* slab_ = nullptr;
   const int16_t* row_run_ = nullptr;
   const double* surplus_ = nullptr;
