@@ -206,6 +206,78 @@ ddsg_status ddsg_grid_support(const ddsg_grid_t* g, const double* x, int64_t n, 
  * the reference's test oracle generates them (proj/tests/oracles.hpp:45-53). */
 void ddsg_uniform_points(uint64_t seed, int64_t n, int dim, double* out);
 
+/* ------------------------------------------------ batched policy callers
+ *
+ * the time iteration's consumers of the policy
+ * interpolant, restructured so that every successor state of a whole batch
+ * of grid points / samples is evaluated in ONE batched policy evaluation on
+ * the device.  The policy is a device object: exactly one of policy_hdmr /
+ * policy_grid is non-NULL (the reference's PolicyEvaluator built by
+ * compiled_evaluator, time_iteration.hpp:86-91).  Its input is the canonical
+ * state x in [0,1]^(2N) (N log-productivities, then N capitals) and its
+ * output the flat policy (k'[N], mu[N] for the non-smooth variant, lambda)
+ * (irbc.hpp:215-236).  Buffers may be host or device memory. */
+
+typedef enum { DDSG_IRBC_SMOOTH = 0, DDSG_IRBC_NONSMOOTH = 1 } ddsg_irbc_variant;
+
+/* IrbcParameters (irbc.hpp:27-53) in flat form.  gamma and tau point to
+ * caller-owned arrays of `countries` doubles. */
+typedef struct {
+  int countries;
+  int variant; /* ddsg_irbc_variant */
+  double beta, alpha, delta, sigma, rho_a, phi_adj, gamma_base;
+  double lna_half_width, k_lo, k_hi;
+  double A;      /* derived */
+  double* gamma; /* [countries] */
+  double* tau;   /* [countries], derived */
+} ddsg_irbc_params;
+
+/* refresh_derived (irbc.hpp:59-92): validates, fills gamma when fill_gamma
+ * != 0 (gamma_j = gamma_base + 0.75 j/(N-1)), then A and tau.  Errors:
+ * INVALID_ARGUMENT with the reference's messages. */
+ddsg_status ddsg_irbc_refresh_derived(ddsg_irbc_params* p, int fill_gamma);
+
+/* steady_state_lambda (irbc.hpp:248-263), host bisection. */
+ddsg_status ddsg_irbc_steady_state_lambda(const ddsg_irbc_params* p, double* lambda);
+
+/* foc_residuals (irbc.hpp:306-361) for n states at once:
+ *   a, k        [n][N]      state (productivity levels, capitals)
+ *   candidate   [n][pdim]   flat candidate policy (pdim = N+1 or 2N+1)
+ *   residuals   [n][pdim]   out
+ *   clamped     [n]         out (may be NULL): successor states clamped into
+ *                           the box, the reference's return value
+ * All 2(N+1) successor states of all n points are evaluated by one batched
+ * policy call.  Errors: INVALID_ARGUMENT (bad parameters/handles),
+ * DOMAIN_ERROR when a successor state is NaN (the reference's
+ * check_point), *bad_index = the lowest failing state. */
+ddsg_status ddsg_irbc_foc_residuals(const ddsg_hdmr_t* policy_hdmr, const ddsg_grid_t* policy_grid,
+                                    const ddsg_irbc_params* p, int64_t n, const double* a, const double* k,
+                                    const double* candidate, double* residuals, int32_t* clamped,
+                                    int64_t* bad_index, void* stream);
+
+/* foc_jacobian (solver.hpp:129-165) for n states at once: forward
+ * differences jac[i][r][c] = (res(z_i + h_c e_c)[r] - r0[i][r]) / h_c with
+ * h_c = fd_epsilon * max(|z_ic|, 1e-2), then (non-smooth variant) the
+ * Fischer-Burmeister rows replaced by their generalized derivative.
+ *   z, r0 [n][pdim], jac [n][pdim][pdim] (row-major, jac[i][r][c]).
+ * Perturbing mu or lambda leaves the successor states unchanged, so only
+ * 1 + N distinct successor sets per point are evaluated (one batched call). */
+ddsg_status ddsg_irbc_foc_jacobian(const ddsg_hdmr_t* policy_hdmr, const ddsg_grid_t* policy_grid,
+                                   const ddsg_irbc_params* p, int64_t n, const double* a, const double* k,
+                                   const double* z, const double* r0, double fd_epsilon, double* jac,
+                                   int64_t* bad_index, void* stream);
+
+/* euler_errors (solver.hpp:377-436) on caller-supplied canonical samples
+ * xs[n][2N] (the reference draws them with std::mt19937_64(seed) +
+ * uniform_real_distribution(0,1), point-major: ddsg_uniform_points):
+ *   errs[n]     per-sample worst-country relative Euler error (out)
+ *   mean, worst sequential mean / max over errs (out; log10 is the caller's)
+ *   clamp_count successor states clamped into the box, summed (out, may be NULL) */
+ddsg_status ddsg_irbc_euler_errors(const ddsg_hdmr_t* policy_hdmr, const ddsg_grid_t* policy_grid,
+                                   const ddsg_irbc_params* p, int64_t n, const double* xs, double* errs,
+                                   double* mean, double* worst, uint64_t* clamp_count, int64_t* bad_index,
+                                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,11 @@
 // VectorizedDdsg::{compile, evaluate, evaluate_batch, quadrature}
 // (ddsg_eval.hpp:40-151), detail::for_each_index (runtime.hpp:104-137),
 // basis_1d / basis_nd (basis.hpp:67-84) and oracle::uniform_points
-// (proj/tests/oracles.hpp:45-53).
+// (proj/tests/oracles.hpp:45-53), and the IRBC policy callers: the
+// reference's own foc_residuals (irbc.hpp:306-361), refresh_derived and
+// steady_state_lambda, plus Eigen-free restatements of foc_jacobian
+// (solver.hpp:129-165) and euler_errors (solver.hpp:377-436) on top of them
+// (solver.hpp needs Eigen, which is absent here).
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -24,6 +28,7 @@
 #include "ddsg/basis.hpp"
 #include "ddsg/ddsg_eval.hpp"
 #include "ddsg/hdmr.hpp"
+#include "ddsg/irbc.hpp"
 #include "ddsg/runtime.hpp"
 #include "ddsg/sparse_grid.hpp"
 #include "oracles.hpp"
@@ -355,5 +360,183 @@ void ref_uniform_points(int dim, int64_t count, uint64_t seed, double* out) {
 uint64_t ref_sg_node_count_bruteforce(int n, int L) { return oracle::sg_node_count_bruteforce(n, L); }
 
 unsigned ref_default_workers() { return default_worker_count(); }
+
+}  // extern "C"
+
+// ------------------------------------------------------------- IRBC callers
+
+namespace {
+
+irbc::IrbcParameters irbc_from_flat(int countries, int variant, const double* scal, const double* gamma) {
+  // scal = {beta, alpha, delta, sigma, rho_a, phi_adj, gamma_base, lna_half_width, k_lo, k_hi}
+  irbc::IrbcParameters p;
+  p.countries = countries;
+  p.variant = variant ? irbc::Variant::nonsmooth : irbc::Variant::smooth;
+  p.beta = scal[0];
+  p.alpha = scal[1];
+  p.delta = scal[2];
+  p.sigma = scal[3];
+  p.rho_a = scal[4];
+  p.phi_adj = scal[5];
+  p.gamma_base = scal[6];
+  p.lna_half_width = scal[7];
+  p.k_lo = scal[8];
+  p.k_hi = scal[9];
+  if (gamma) p.gamma.assign(gamma, gamma + countries);
+  irbc::refresh_derived(p);
+  return p;
+}
+
+// compiled_evaluator (time_iteration.hpp:86-91) over a ref_hdmr, or the
+// plain grid's interpolate.
+irbc::PolicyEvaluator ref_policy(const ref_hdmr* h, const ref_grid* g) {
+  if (h)
+    return [h](std::span<const double> x, std::span<double> out) {
+      thread_local EvalWorkspace ws;
+      h->vec.evaluate(x, out, ws);
+    };
+  return [g](std::span<const double> x, std::span<double> out) { g->g.interpolate(x, out); };
+}
+
+irbc::EconomicState state_of(int N, const double* a, const double* k) {
+  irbc::EconomicState st;
+  st.a.assign(a, a + N);
+  st.k.assign(k, k + N);
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+// refresh_derived (irbc.hpp:59-92): writes gamma[N], tau[N] and A.
+int ref_irbc_refresh(int countries, int variant, const double* scal, const double* gamma_in, double* gamma_out,
+                     double* tau_out, double* A_out) {
+  return guarded([&] {
+    const auto p = irbc_from_flat(countries, variant, scal, gamma_in);
+    std::copy(p.gamma.begin(), p.gamma.end(), gamma_out);
+    std::copy(p.tau.begin(), p.tau.end(), tau_out);
+    *A_out = p.A;
+  });
+}
+
+int ref_irbc_steady_lambda(int countries, int variant, const double* scal, const double* gamma, double* out) {
+  return guarded([&] { *out = irbc::steady_state_lambda(irbc_from_flat(countries, variant, scal, gamma)); });
+}
+
+// foc_residuals (irbc.hpp:306-361) per state; clamped[i] = its return value.
+int ref_irbc_foc_residuals(const ref_hdmr* h, const ref_grid* g, int countries, int variant, const double* scal,
+                           const double* gamma, int64_t n, const double* a, const double* k, const double* cand,
+                           double* res, int32_t* clamped) {
+  return guarded([&] {
+    const auto p = irbc_from_flat(countries, variant, scal, gamma);
+    const auto quad = irbc::make_shock_quadrature(countries);
+    const auto pol = ref_policy(h, g);
+    const int pd = p.policy_dim();
+    irbc::FocWorkspace ws;
+    for (int64_t i = 0; i < n; ++i) {
+      const auto st = state_of(countries, a + i * countries, k + i * countries);
+      const auto cv = irbc::PolicyValue::from_flat(std::span<const double>(cand + i * pd, pd), p);
+      const int c = irbc::foc_residuals(st, cv, pol, p, quad, std::span<double>(res + i * pd, pd), ws);
+      if (clamped) clamped[i] = c;
+    }
+  });
+}
+
+// foc_jacobian (solver.hpp:129-165) restated without Eigen: jac[i][r][c].
+int ref_irbc_foc_jacobian(const ref_hdmr* h, const ref_grid* g, int countries, int variant, const double* scal,
+                          const double* gamma, int64_t n, const double* a, const double* k, const double* z,
+                          const double* r0, double fd_epsilon, double* jac) {
+  return guarded([&] {
+    const auto p = irbc_from_flat(countries, variant, scal, gamma);
+    const auto quad = irbc::make_shock_quadrature(countries);
+    const auto pol = ref_policy(h, g);
+    const int nn = p.policy_dim(), N = countries;
+    irbc::FocWorkspace ws;
+    std::vector<double> zp(nn), res(nn);
+    for (int64_t i = 0; i < n; ++i) {
+      const auto st = state_of(N, a + i * N, k + i * N);
+      const double* zi = z + i * nn;
+      const double* ri = r0 + i * nn;
+      double* J = jac + i * nn * nn;
+      zp.assign(zi, zi + nn);
+      for (int c = 0; c < nn; ++c) {
+        const double hh = fd_epsilon * std::max(std::abs(zi[c]), 1e-2);
+        zp[c] = zi[c] + hh;
+        const auto cand = irbc::PolicyValue::from_flat(std::span<const double>(zp.data(), zp.size()), p);
+        irbc::foc_residuals(st, cand, pol, p, quad, res, ws);
+        for (int rr = 0; rr < nn; ++rr) J[rr * nn + c] = (res[rr] - ri[rr]) / hh;
+        zp[c] = zi[c];
+      }
+      if (p.variant == irbc::Variant::nonsmooth) {
+        for (int j = 0; j < N; ++j) {
+          const int row = N + j;
+          const double mu = zi[N + j];
+          const double s = zi[j] - (1.0 - p.delta) * st.k[j];
+          const double norm = std::sqrt(mu * mu + s * s);
+          double dmu, ds;
+          if (norm == 0.0) {
+            dmu = 1.0 - 1.0 / std::sqrt(2.0);
+            ds = 1.0 - 1.0 / std::sqrt(2.0);
+          } else {
+            dmu = 1.0 - mu / norm;
+            ds = 1.0 - s / norm;
+          }
+          for (int c = 0; c < nn; ++c) J[row * nn + c] = 0.0;
+          J[row * nn + N + j] = dmu;
+          J[row * nn + j] = ds;
+        }
+      }
+    }
+  });
+}
+
+// euler_errors (solver.hpp:377-436) restated without Eigen, on the samples
+// xs[n][2N] (the caller draws them as the reference does).  stats = {mean,
+// worst}; workers as the reference's for_each_index over 64 blocks.
+int ref_irbc_euler_errors(const ref_hdmr* h, const ref_grid* g, int countries, int variant, const double* scal,
+                          const double* gamma, int64_t n, const double* xs, unsigned workers, double* errs,
+                          double* stats, uint64_t* clamp_count) {
+  return guarded([&] {
+    const auto p = irbc_from_flat(countries, variant, scal, gamma);
+    const auto quad = irbc::make_shock_quadrature(countries);
+    const auto policy = ref_policy(h, g);
+    const size_t N = static_cast<size_t>(countries), d = 2 * N, m = static_cast<size_t>(p.policy_dim());
+    std::vector<uint64_t> clamps_per_block(64, 0);
+    const size_t n_blocks = std::min<size_t>(64, static_cast<size_t>(n));
+    detail::for_each_index(n_blocks, workers, [&](size_t b) {
+      irbc::FocWorkspace ws;
+      std::vector<double> pol(m), res(m);
+      uint64_t local = 0;
+      for (size_t i = b; i < static_cast<size_t>(n); i += n_blocks) {
+        const std::span<const double> x(xs + i * d, d);
+        const auto st = irbc::from_canonical(x, p);
+        policy(x, pol);
+        const auto pv = irbc::PolicyValue::from_flat(pol, p);
+        local += static_cast<uint64_t>(irbc::foc_residuals(st, pv, policy, p, quad, res, ws));
+        double worst = 0.0;
+        for (size_t j = 0; j < N; ++j) {
+          const double g1 = pv.k_next[j] / st.k[j] - 1.0;
+          const double denom = pv.lambda * (1.0 + p.phi_adj * g1);
+          const double numerator = denom - res[j];
+          worst = std::max(worst, std::abs(numerator / denom - 1.0));
+        }
+        errs[i] = worst;
+      }
+      clamps_per_block[b] = local;
+    });
+    double mean = 0.0, worst = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      mean += errs[i];
+      worst = std::max(worst, errs[i]);
+    }
+    stats[0] = mean / static_cast<double>(n);
+    stats[1] = worst;
+    if (clamp_count) {
+      *clamp_count = 0;
+      for (uint64_t c : clamps_per_block) *clamp_count += c;
+    }
+  });
+}
 
 }  // extern "C"

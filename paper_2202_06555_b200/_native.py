@@ -63,7 +63,21 @@ SIGNATURES = {
     "ddsg_hdmr_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
     "ddsg_grid_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
     "ddsg_uniform_points": (None, [C.c_uint64, _i64, _i, _p]),
+    "ddsg_irbc_refresh_derived": (_i, [_p, _i]),
+    "ddsg_irbc_steady_state_lambda": (_i, [_p, C.POINTER(_d)]),
+    "ddsg_irbc_foc_residuals": (_i, [_p, _p, _p, _i64, _pd, _pd, _pd, _pd, _pd, C.POINTER(_i64), _p]),
+    "ddsg_irbc_foc_jacobian": (_i, [_p, _p, _p, _i64, _pd, _pd, _pd, _pd, _d, _pd, C.POINTER(_i64), _p]),
+    "ddsg_irbc_euler_errors": (_i, [_p, _p, _p, _i64, _pd, _pd, C.POINTER(_d), C.POINTER(_d), C.POINTER(C.c_uint64),
+                                    C.POINTER(_i64), _p]),
 }
+
+
+class IrbcParamsC(C.Structure):
+    """ddsg_irbc_params (include/ddsg_b200.h)."""
+
+    _fields_ = [("countries", _i), ("variant", _i), ("beta", _d), ("alpha", _d), ("delta", _d), ("sigma", _d),
+                ("rho_a", _d), ("phi_adj", _d), ("gamma_base", _d), ("lna_half_width", _d), ("k_lo", _d),
+                ("k_hi", _d), ("A", _d), ("gamma", C.POINTER(_d)), ("tau", C.POINTER(_d))]
 
 for _name, (_res, _args) in SIGNATURES.items():
     _fn = getattr(lib, _name)

@@ -17,6 +17,7 @@
 #include "../../include/ddsg_b200.h"
 #include "device.cuh"
 #include "grid_host.hpp"
+#include "irbc.cuh"
 #include "program.hpp"
 
 using namespace ddsg_b200;
@@ -482,6 +483,170 @@ void ddsg_uniform_points(uint64_t seed, int64_t n, int dim, double* out) {
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> unif(0.0, 1.0);
   for (int64_t i = 0; i < n * dim; ++i) out[i] = unif(rng);
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------- IRBC callers
+
+namespace {
+
+// IrbcParameters -> irbc::Params, with the validation of refresh_derived.
+irbc::Params irbc_params(const ddsg_irbc_params* p) {
+  if (!p) fail(DDSG_INVALID_ARGUMENT, "irbc: null parameters");
+  if (p->countries < 1) fail(DDSG_INVALID_ARGUMENT, "irbc: countries must be >= 1");
+  if (p->countries > 2048) fail(DDSG_INVALID_ARGUMENT, "irbc: at most 2048 countries on the device path");
+  if (p->variant != DDSG_IRBC_SMOOTH && p->variant != DDSG_IRBC_NONSMOOTH)
+    fail(DDSG_INVALID_ARGUMENT, "irbc: unknown variant");
+  if (!p->gamma || !p->tau) fail(DDSG_INVALID_ARGUMENT, "irbc: null gamma / tau");
+  irbc::Params q;
+  q.countries = p->countries;
+  q.nonsmooth = p->variant == DDSG_IRBC_NONSMOOTH;
+  q.beta = p->beta;
+  q.alpha = p->alpha;
+  q.delta = p->delta;
+  q.sigma = p->sigma;
+  q.rho_a = p->rho_a;
+  q.phi_adj = p->phi_adj;
+  q.lna_half_width = p->lna_half_width;
+  q.k_lo = p->k_lo;
+  q.k_hi = p->k_hi;
+  q.A = p->A;
+  q.gamma.assign(p->gamma, p->gamma + p->countries);
+  q.tau.assign(p->tau, p->tau + p->countries);
+  return q;
+}
+
+// The policy as a batched device evaluator (compiled_evaluator,
+// time_iteration.hpp:86-91): canonical states [2N] -> flat policy [pdim].
+irbc::PolicyFn irbc_policy(const ddsg_hdmr_t* h, const ddsg_grid_t* g, const irbc::Params& p) {
+  if ((h == nullptr) == (g == nullptr))
+    fail(DDSG_INVALID_ARGUMENT, "irbc: exactly one of policy_hdmr / policy_grid must be given");
+  int d = 0, m = 0, exact = 1;
+  const DeviceProgram* prog = nullptr;
+  if (h) {
+    auto* self = const_cast<ddsg_hdmr_t*>(h);
+    d = h->d;
+    m = h->m;
+    exact = h->eval_mode == DDSG_EVAL_EXACT;
+    prog = &self->dev.get(h->prog);
+  } else {
+    auto* self = const_cast<ddsg_grid_t*>(g);
+    d = g->g.dim;
+    m = g->g.m;
+    exact = g->eval_mode == DDSG_EVAL_EXACT;
+    prog = &self->dev.get(self->program());
+  }
+  if (d != p.state_dim() || m != p.pdim())
+    fail(DDSG_INVALID_ARGUMENT, "irbc: policy dimensions do not match the model (dim 2N, out_dim pdim)");
+  return [prog, exact](const double* dx, int64_t n, double* dy, cudaStream_t st) {
+    return evaluate(*prog, exact, dx, n, dy, st);
+  };
+}
+
+void irbc_domain_fail(int64_t bad, int64_t* bad_index) {
+  if (bad_index) *bad_index = bad;
+  fail(DDSG_DOMAIN_ERROR, "task " + std::to_string(bad) + " failed: ddsg: query outside unit cube");
+}
+
+}  // namespace
+
+extern "C" {
+
+ddsg_status ddsg_irbc_refresh_derived(ddsg_irbc_params* p, int fill_gamma) {
+  return guarded([&] {
+    // irbc.hpp:59-92, same checks, messages and arithmetic (host libm)
+    if (!p) fail(DDSG_INVALID_ARGUMENT, "irbc: null parameters");
+    if (p->countries < 1) fail(DDSG_INVALID_ARGUMENT, "irbc: countries must be >= 1");
+    if (!(p->beta > 0.0 && p->beta < 1.0)) fail(DDSG_INVALID_ARGUMENT, "irbc: beta in (0,1)");
+    if (!(p->delta > 0.0 && p->delta < 1.0)) fail(DDSG_INVALID_ARGUMENT, "irbc: delta in (0,1)");
+    if (!(p->alpha > 0.0 && p->alpha < 1.0)) fail(DDSG_INVALID_ARGUMENT, "irbc: alpha in (0,1)");
+    if (!(p->sigma >= 0.0)) fail(DDSG_INVALID_ARGUMENT, "irbc: sigma must be >= 0");
+    if (!(p->rho_a >= 0.0 && p->rho_a < 1.0)) fail(DDSG_INVALID_ARGUMENT, "irbc: rho_a in [0,1)");
+    if (!(p->phi_adj >= 0.0)) fail(DDSG_INVALID_ARGUMENT, "irbc: phi_adj must be >= 0");
+    if (!(p->k_lo > 0.0 && p->k_hi > p->k_lo))
+      fail(DDSG_INVALID_ARGUMENT, "irbc: capital box must satisfy 0 < k_lo < k_hi");
+    if (!(p->lna_half_width > 0.0)) fail(DDSG_INVALID_ARGUMENT, "irbc: lna_half_width must be > 0");
+    if (!p->gamma || !p->tau) fail(DDSG_INVALID_ARGUMENT, "irbc: null gamma / tau");
+    const int N = p->countries;
+    if (fill_gamma)
+      for (int j = 0; j < N; ++j)
+        p->gamma[j] = N == 1 ? p->gamma_base
+                             : p->gamma_base + 0.75 * static_cast<double>(j) / static_cast<double>(N - 1);
+    for (int j = 0; j < N; ++j)
+      if (!(p->gamma[j] > 0.0)) fail(DDSG_INVALID_ARGUMENT, "irbc: gamma_j must be > 0");
+    p->A = (1.0 - p->beta * (1.0 - p->delta)) / (p->alpha * p->beta);
+    for (int j = 0; j < N; ++j) p->tau[j] = std::pow(p->A, 1.0 / p->gamma[j]);
+  });
+}
+
+ddsg_status ddsg_irbc_steady_state_lambda(const ddsg_irbc_params* p, double* lambda) {
+  return guarded([&] {
+    // irbc.hpp:248-263: geometric bisection, 200 halvings
+    if (!p || !lambda || !p->gamma) fail(DDSG_INVALID_ARGUMENT, "irbc: null argument");
+    const double target = static_cast<double>(p->countries) * (p->A - p->delta);
+    if (!(target > 0.0)) fail(DDSG_DOMAIN_ERROR, "irbc: steady-state consumption would be non-positive");
+    double lo = 1e-8, hi = 1e8;
+    auto g = [&](double lam) {
+      double s = 0.0;
+      for (int j = 0; j < p->countries; ++j) s += p->A * std::pow(lam, -p->gamma[j]);
+      return s - target;
+    };
+    for (int it = 0; it < 200; ++it) {
+      const double mid = std::sqrt(lo * hi);
+      (g(mid) > 0.0 ? lo : hi) = mid;
+    }
+    *lambda = std::sqrt(lo * hi);
+  });
+}
+
+ddsg_status ddsg_irbc_foc_residuals(const ddsg_hdmr_t* policy_hdmr, const ddsg_grid_t* policy_grid,
+                                    const ddsg_irbc_params* p, int64_t n, const double* a, const double* k,
+                                    const double* candidate, double* residuals, int32_t* clamped,
+                                    int64_t* bad_index, void* stream) {
+  if (bad_index) *bad_index = -1;
+  return guarded([&] {
+    const irbc::Params q = irbc_params(p);
+    const irbc::PolicyFn pol = irbc_policy(policy_hdmr, policy_grid, q);
+    if (n < 0) fail(DDSG_INVALID_ARGUMENT, "foc_residuals: negative state count");
+    if (n > 0 && (!a || !k || !candidate || !residuals)) fail(DDSG_INVALID_ARGUMENT, "foc_residuals: null buffers");
+    const int64_t bad = irbc::foc_residuals(q, pol, n, a, k, candidate, residuals, clamped,
+                                            static_cast<cudaStream_t>(stream));
+    if (bad >= 0) irbc_domain_fail(bad, bad_index);
+  });
+}
+
+ddsg_status ddsg_irbc_foc_jacobian(const ddsg_hdmr_t* policy_hdmr, const ddsg_grid_t* policy_grid,
+                                   const ddsg_irbc_params* p, int64_t n, const double* a, const double* k,
+                                   const double* z, const double* r0, double fd_epsilon, double* jac,
+                                   int64_t* bad_index, void* stream) {
+  if (bad_index) *bad_index = -1;
+  return guarded([&] {
+    const irbc::Params q = irbc_params(p);
+    const irbc::PolicyFn pol = irbc_policy(policy_hdmr, policy_grid, q);
+    if (n < 0) fail(DDSG_INVALID_ARGUMENT, "foc_jacobian: negative state count");
+    if (n > 0 && (!a || !k || !z || !r0 || !jac)) fail(DDSG_INVALID_ARGUMENT, "foc_jacobian: null buffers");
+    const int64_t bad =
+        irbc::foc_jacobian(q, pol, n, a, k, z, r0, fd_epsilon, jac, static_cast<cudaStream_t>(stream));
+    if (bad >= 0) irbc_domain_fail(bad, bad_index);
+  });
+}
+
+ddsg_status ddsg_irbc_euler_errors(const ddsg_hdmr_t* policy_hdmr, const ddsg_grid_t* policy_grid,
+                                   const ddsg_irbc_params* p, int64_t n, const double* xs, double* errs,
+                                   double* mean, double* worst, uint64_t* clamp_count, int64_t* bad_index,
+                                   void* stream) {
+  if (bad_index) *bad_index = -1;
+  return guarded([&] {
+    const irbc::Params q = irbc_params(p);
+    const irbc::PolicyFn pol = irbc_policy(policy_hdmr, policy_grid, q);
+    // solver.hpp:381
+    if (n < 1) fail(DDSG_INVALID_ARGUMENT, "euler_errors: n_samples must be >= 1");
+    if (!xs || !errs || !mean || !worst) fail(DDSG_INVALID_ARGUMENT, "euler_errors: null buffers");
+    const int64_t bad = irbc::euler_errors(q, pol, n, xs, errs, mean, worst, clamp_count,
+                                           static_cast<cudaStream_t>(stream));
+    if (bad >= 0) irbc_domain_fail(bad, bad_index);
+  });
 }
 
 }  // extern "C"

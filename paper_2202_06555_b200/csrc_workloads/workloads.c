@@ -377,3 +377,129 @@ int wl_cut_eval(const double* ys, int64_t count, double* out, void* ctx) {
   free(xs);
   return rc;
 }
+
+/* --------------------------------------------------- IRBC policy targets */
+
+/* Policy-shaped targets for the batched IRBC callers (SURVEY.md §8(f) rows
+ * 2-3).  Canonical state x in [0,1]^(2N): N log-productivities, then N
+ * capitals (irbc.hpp:188-226); flat policy k'[N], (mu[N]), lambda
+ * (irbc.hpp:230-246):
+ *   lna_j = 2 w x_j - w,  k_j = k_lo + x_{N+j} (k_hi - k_lo)
+ *   inv_j = delta k_j + ca_j lna_j + ck_j (1 - k_j)
+ *           + sum_{pairs r owned by j} cc_r (x_p - 1/2)(x_q - 1/2)
+ *   k'_j  = (1 - delta) k_j + max(0, inv_j)   (irreversible investment)
+ *   mu_j  = 0.1 max(0, -inv_j)                (non-smooth variant)
+ *   lambda = lam0 exp(-0.1 mean_j lna_j + 0.05 mean_j (k_j - 1))
+ * steady = 1 gives the reference tests' steady policy instead
+ * (test_irbc.cpp:14-24): k' = k, mu = 0, lambda = lam0. */
+typedef struct {
+  int N, nonsmooth, steady, n_pairs;
+  double delta, k_lo, k_hi, lw, lam0;
+  double *ca, *ck, *cc;
+  int *pp, *pq, *owner;
+} wl_irbc;
+
+wl_irbc* wl_irbc_new(int N, int nonsmooth, int steady, int n_pairs, uint64_t seed, double delta, double k_lo,
+                     double k_hi, double lw, double lam0) {
+  if (N < 1 || n_pairs < 0 || (n_pairs > 0 && 2 * N < 2)) return NULL;
+  wl_irbc* t = (wl_irbc*)calloc(1, sizeof(wl_irbc));
+  t->N = N;
+  t->nonsmooth = nonsmooth;
+  t->steady = steady;
+  t->delta = delta;
+  t->k_lo = k_lo;
+  t->k_hi = k_hi;
+  t->lw = lw;
+  t->lam0 = lam0;
+  const int d = 2 * N;
+  const long maxp = (long)d * (d - 1) / 2;
+  if (n_pairs > maxp) n_pairs = (int)maxp;
+  t->n_pairs = n_pairs;
+  t->ca = (double*)malloc(sizeof(double) * (size_t)N);
+  t->ck = (double*)malloc(sizeof(double) * (size_t)N);
+  t->cc = (double*)malloc(sizeof(double) * (size_t)(n_pairs + 1));
+  t->pp = (int*)malloc(sizeof(int) * (size_t)(n_pairs + 1));
+  t->pq = (int*)malloc(sizeof(int) * (size_t)(n_pairs + 1));
+  t->owner = (int*)malloc(sizeof(int) * (size_t)(n_pairs + 1));
+  mt64 rng;
+  mt64_seed(&rng, seed);
+  for (int j = 0; j < N; ++j) {
+    t->ca[j] = unif(&rng, 0.01, 0.05);
+    t->ck[j] = unif(&rng, 0.01, 0.05);
+  }
+  int r = 0;
+  while (r < n_pairs) {
+    int p = (int)(mt64_next(&rng) % (uint64_t)d), q = (int)(mt64_next(&rng) % (uint64_t)d);
+    if (p == q) continue;
+    if (p > q) {
+      int tmp = p;
+      p = q;
+      q = tmp;
+    }
+    int dup = 0;
+    for (int s = 0; s < r; ++s) dup |= (t->pp[s] == p && t->pq[s] == q);
+    if (dup) continue;
+    t->pp[r] = p;
+    t->pq[r] = q;
+    ++r;
+  }
+  for (int i = 1; i < r; ++i) /* insertion sort (p, q) */
+    for (int k = i; k > 0 && (t->pp[k - 1] > t->pp[k] || (t->pp[k - 1] == t->pp[k] && t->pq[k - 1] > t->pq[k])); --k) {
+      int a = t->pp[k], b = t->pq[k];
+      t->pp[k] = t->pp[k - 1];
+      t->pq[k] = t->pq[k - 1];
+      t->pp[k - 1] = a;
+      t->pq[k - 1] = b;
+    }
+  for (int s = 0; s < r; ++s) {
+    t->owner[s] = (int)(mt64_next(&rng) % (uint64_t)N);
+    t->cc[s] = unif(&rng, -0.2, 0.2);
+  }
+  return t;
+}
+
+void wl_irbc_free(wl_irbc* t) {
+  if (!t) return;
+  free(t->ca);
+  free(t->ck);
+  free(t->cc);
+  free(t->pp);
+  free(t->pq);
+  free(t->owner);
+  free(t);
+}
+
+int wl_irbc_pairs(const wl_irbc* t, int32_t* pairs) {
+  for (int r = 0; r < t->n_pairs; ++r) {
+    pairs[2 * r] = t->pp[r];
+    pairs[2 * r + 1] = t->pq[r];
+  }
+  return t->n_pairs;
+}
+
+int wl_irbc_policy(const double* xs, int64_t count, double* out, void* ctx) {
+  const wl_irbc* t = (const wl_irbc*)ctx;
+  const int N = t->N, d = 2 * N, m = t->nonsmooth ? 2 * N + 1 : N + 1;
+  double* inv = (double*)malloc(sizeof(double) * (size_t)N);
+  for (int64_t i = 0; i < count; ++i) {
+    const double* x = xs + i * d;
+    double* o = out + i * m;
+    double mlna = 0.0, mk = 0.0;
+    for (int j = 0; j < N; ++j) {
+      const double lna = x[j] * 2.0 * t->lw - t->lw;
+      const double k = t->k_lo + x[N + j] * (t->k_hi - t->k_lo);
+      inv[j] = t->delta * k + t->ca[j] * lna + t->ck[j] * (1.0 - k);
+      mlna += lna;
+      mk += k - 1.0;
+    }
+    for (int r = 0; r < t->n_pairs; ++r) inv[t->owner[r]] += t->cc[r] * (x[t->pp[r]] - 0.5) * (x[t->pq[r]] - 0.5);
+    for (int j = 0; j < N; ++j) {
+      const double k = t->k_lo + x[N + j] * (t->k_hi - t->k_lo);
+      o[j] = t->steady ? k : (1.0 - t->delta) * k + (inv[j] > 0.0 ? inv[j] : 0.0);
+      if (t->nonsmooth) o[N + j] = t->steady ? 0.0 : 0.1 * (inv[j] < 0.0 ? -inv[j] : 0.0);
+    }
+    o[m - 1] = t->steady ? t->lam0 : t->lam0 * exp(-0.1 * mlna / N + 0.05 * mk / N);
+  }
+  free(inv);
+  return 0;
+}

@@ -171,3 +171,82 @@ def points(cfg: Config, n: Optional[int] = None, seed: Optional[int] = None) -> 
     from .ddsg import uniform_points
 
     return uniform_points(cfg.seed if seed is None else seed, cfg.n_points if n is None else n, cfg.d)
+
+
+# ------------------------------------------------------ IRBC policy targets
+
+class IrbcPolicyTarget:
+    """wl_irbc_policy (workloads.c): a policy-shaped target on the canonical
+    state cube of an N-country IRBC model, for the batched callers
+    (SURVEY.md §8(f) rows 2-3).  ``steady=True`` is the reference tests'
+    steady policy (k' = k, mu = 0, lambda = lam0; test_irbc.cpp:14-24)."""
+
+    def __init__(self, countries: int, nonsmooth: bool = False, steady: bool = False, n_pairs: int = 0,
+                 seed: int = 20220213, delta: float = 0.01, k_lo: float = 0.5, k_hi: float = 1.5,
+                 lna_half_width: float = 0.4, lam0: float = 1.0):
+        wl = N.workloads()
+        wl.wl_irbc_new.restype = C.c_void_p
+        wl.wl_irbc_new.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double,
+                                   C.c_double, C.c_double, C.c_double]
+        wl.wl_irbc_free.argtypes = [C.c_void_p]
+        wl.wl_irbc_pairs.restype = C.c_int
+        wl.wl_irbc_pairs.argtypes = [C.c_void_p, C.c_void_p]
+        self.countries = countries
+        self.d = 2 * countries
+        self.m = 2 * countries + 1 if nonsmooth else countries + 1
+        self.ctx = wl.wl_irbc_new(countries, int(nonsmooth), int(steady), n_pairs, seed, delta, k_lo, k_hi,
+                                  lna_half_width, lam0)
+        if not self.ctx:
+            raise ValueError("wl_irbc_new: bad arguments")
+        pairs = np.zeros(2 * max(n_pairs, 1), dtype=np.int32)
+        n = wl.wl_irbc_pairs(self.ctx, pairs.ctypes.data)
+        self.pairs = [(int(pairs[2 * r]), int(pairs[2 * r + 1])) for r in range(n)]
+        self.addr = N.wl_fn("wl_irbc_policy")
+        self._fn = wl.wl_irbc_policy
+        self._fn.restype = C.c_int
+        self._fn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+
+    def __call__(self, xs: np.ndarray) -> np.ndarray:
+        xs = np.ascontiguousarray(xs, dtype=np.float64).reshape(-1, self.d)
+        out = np.empty((xs.shape[0], self.m))
+        if xs.shape[0]:
+            self._fn(xs.ctypes.data, xs.shape[0], out.ctypes.data, C.c_void_p(self.ctx))
+        return out
+
+    def __del__(self):
+        if getattr(self, "ctx", None):
+            N.workloads().wl_irbc_free(C.c_void_p(self.ctx))
+            self.ctx = None
+
+
+def build_policy_grid(target: IrbcPolicyTarget, max_level: int, eps: float = 0.0,
+                      mode: int = MODIFIED_LINEAR) -> SparseGridFunction:
+    """The policy as one plain sparse grid on [0,1]^(2N)."""
+    return SparseGridFunction.build(target.addr, target.d, target.m, max_level, eps, mode, ctx=target.ctx)
+
+
+def build_policy_hdmr(target: IrbcPolicyTarget, level_1d: int, level_2d: int, eps_1d: float = 0.0,
+                      eps_2d: float = 0.0, mode: int = MODIFIED_LINEAR) -> Tuple[VectorizedDdsg, HdmrParts]:
+    """The policy as a cut-HDMR (center anchor): all 1-d cuts plus the
+    target's pair cuts, like configs 4-5."""
+    wl = N.workloads()
+    fam: List[Tuple[int, ...]] = [()] + [(k,) for k in range(target.d)] + sorted(set(target.pairs))
+    b = telescoping_b(fam)
+    anchor = np.full(target.d, 0.5)
+    fa = target(anchor)[0]
+    parts = HdmrParts(target.d, target.m, fa)
+    cut_addr = N.wl_fn("wl_cut_eval")
+    for u, bu in zip(fam, b):
+        if not u:
+            parts.slots.append((u, bu, None))
+            continue
+        dims = np.array(u, dtype=np.int32)
+        cut = wl.wl_cut_new(target.addr, target.ctx, target.d, target.m, len(u), dims.ctypes.data,
+                            anchor.ctypes.data)
+        try:
+            lvl, eps = (level_1d, eps_1d) if len(u) == 1 else (level_2d, eps_2d)
+            g = SparseGridFunction.build(cut_addr, len(u), target.m, lvl, eps, mode, ctx=cut)
+        finally:
+            wl.wl_cut_free(C.c_void_p(cut))
+        parts.slots.append((u, bu, g))
+    return VectorizedDdsg.compile(parts.d, parts.m, parts.f_anchor, parts.slots), parts

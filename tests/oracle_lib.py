@@ -99,6 +99,16 @@ def ref():
         L.ref_sg_node_count_bruteforce.restype = _u64
         L.ref_sg_node_count_bruteforce.argtypes = [_i, _i]
         L.ref_default_workers.restype = C.c_uint
+        L.ref_irbc_refresh.restype = _i
+        L.ref_irbc_refresh.argtypes = [_i, _i, _p, _p, _p, _p, C.POINTER(_d)]
+        L.ref_irbc_steady_lambda.restype = _i
+        L.ref_irbc_steady_lambda.argtypes = [_i, _i, _p, _p, C.POINTER(_d)]
+        L.ref_irbc_foc_residuals.restype = _i
+        L.ref_irbc_foc_residuals.argtypes = [_p, _p, _i, _i, _p, _p, _i64, _p, _p, _p, _p, _p]
+        L.ref_irbc_foc_jacobian.restype = _i
+        L.ref_irbc_foc_jacobian.argtypes = [_p, _p, _i, _i, _p, _p, _i64, _p, _p, _p, _p, _d, _p]
+        L.ref_irbc_euler_errors.restype = _i
+        L.ref_irbc_euler_errors.argtypes = [_p, _p, _i, _i, _p, _p, _i64, _p, C.c_uint, _p, _p, C.POINTER(_u64)]
         L.ref_json_enabled.restype = _i
         if L.ref_json_enabled():
             L.ref_grid_to_json.restype = C.c_char_p
@@ -302,3 +312,75 @@ def ref_decompose(d, m, k_max, max_level, fn_addr, ctx=None, eps_rho=0.0, eps_et
     text = L.ref_decomp_to_json(h).decode() if want_json else None
     L.ref_decomp_free(h)
     return (fa, out, text) if want_json else (fa, out)
+
+
+# ------------------------------------------------------------- IRBC callers
+
+def _irbc_scal(p):
+    return np.array([p.beta, p.alpha, p.delta, p.sigma, p.rho_a, p.phi_adj, p.gamma_base, p.lna_half_width,
+                     p.k_lo, p.k_hi], dtype=np.float64)
+
+
+def _irbc_gamma(p):
+    return np.ascontiguousarray(p.gamma, dtype=np.float64) if p.gamma else None
+
+
+def ref_irbc_refresh(p):
+    """(gamma, tau, A) from the reference's refresh_derived (irbc.hpp:59-92)."""
+    n = p.countries
+    g, t, A = np.empty(n), np.empty(n), _d()
+    sc, gi = _irbc_scal(p), _irbc_gamma(p)
+    rc = ref().ref_irbc_refresh(n, p.variant, _ptr(sc), _ptr(gi), _ptr(g), _ptr(t), C.byref(A))
+    return rc, g, t, A.value
+
+
+def ref_irbc_steady_lambda(p):
+    out = _d()
+    sc, gi = _irbc_scal(p), _irbc_gamma(p)
+    rc = ref().ref_irbc_steady_lambda(p.countries, p.variant, _ptr(sc), _ptr(gi), C.byref(out))
+    assert rc == 0, ref().ref_last_error()
+    return out.value
+
+
+def _policy_handles(policy):
+    if isinstance(policy, RefHdmr):
+        return policy.h, None
+    return None, policy.h
+
+
+def ref_irbc_foc_residuals(policy, p, a, k, cand):
+    a, k, cand = (np.ascontiguousarray(v, dtype=np.float64) for v in (a, k, cand))
+    n, pd = cand.shape
+    res = np.empty((n, pd))
+    cl = np.empty(n, dtype=np.int32)
+    h, g = _policy_handles(policy)
+    sc, gi = _irbc_scal(p), _irbc_gamma(p)
+    rc = ref().ref_irbc_foc_residuals(h, g, p.countries, p.variant, _ptr(sc), _ptr(gi), n,
+                                      _ptr(a), _ptr(k), _ptr(cand), _ptr(res), _ptr(cl))
+    assert rc == 0, ref().ref_last_error()
+    return res, cl
+
+
+def ref_irbc_foc_jacobian(policy, p, a, k, z, r0, fd_epsilon=1e-7):
+    a, k, z, r0 = (np.ascontiguousarray(v, dtype=np.float64) for v in (a, k, z, r0))
+    n, pd = z.shape
+    jac = np.empty((n, pd, pd))
+    h, g = _policy_handles(policy)
+    sc, gi = _irbc_scal(p), _irbc_gamma(p)
+    rc = ref().ref_irbc_foc_jacobian(h, g, p.countries, p.variant, _ptr(sc), _ptr(gi), n,
+                                     _ptr(a), _ptr(k), _ptr(z), _ptr(r0), fd_epsilon, _ptr(jac))
+    assert rc == 0, ref().ref_last_error()
+    return jac
+
+
+def ref_irbc_euler_errors(policy, p, xs, workers=1):
+    """(errs, mean, worst, clamp_count) — solver.hpp:377-436 on samples xs."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    n = xs.shape[0]
+    errs, stats, cl = np.empty(n), np.empty(2), _u64()
+    h, g = _policy_handles(policy)
+    sc, gi = _irbc_scal(p), _irbc_gamma(p)
+    rc = ref().ref_irbc_euler_errors(h, g, p.countries, p.variant, _ptr(sc), _ptr(gi), n,
+                                     _ptr(xs), workers, _ptr(errs), _ptr(stats), C.byref(cl))
+    assert rc == 0, ref().ref_last_error()
+    return errs, stats[0], stats[1], cl.value
