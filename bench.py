@@ -45,6 +45,12 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
     ap.add_argument("--no-refine", action="store_true",
                     help="build the 1-d cuts at their final level instead of one distributed refinement step")
+    ap.add_argument("--workload", choices=["eval", "euler", "jacobian"], default="eval",
+                    help="eval: the HDMR evaluation (default, BASELINE metric); euler / jacobian: the batched "
+                         "IRBC policy callers of SURVEY.md §8(f) rows 2-3 on a config-5-shaped policy")
+    ap.add_argument("--countries", type=int, default=150, help="IRBC countries N for --workload euler/jacobian")
+    ap.add_argument("--samples", type=int, default=10000, help="Euler-error samples per step (time_iteration.hpp:32)")
+    ap.add_argument("--states", type=int, default=64, help="states per Jacobian step")
     return ap.parse_args()
 
 
@@ -420,13 +426,216 @@ def run_reference(args, rank, world):
     }), flush=True)
 
 
+# ------------------------------------------- IRBC callers
+
+def build_irbc_policy(args):
+    """A config-5-shaped policy on an N-country IRBC state space: 2N 1-d cuts
+    (L=8) + 2N seeded pair cuts (L=5), eps 1e-8, modified-linear, center anchor."""
+    from paper_2202_06555_b200 import irbc as I
+    from paper_2202_06555_b200 import workloads as W
+
+    p = I.make_parameters(args.countries, I.SMOOTH)
+    tgt = W.IrbcPolicyTarget(args.countries, n_pairs=2 * args.countries, lam0=I.steady_state_lambda(p))
+    vec, parts = W.build_policy_hdmr(tgt, 8, 5, 1e-8, 1e-8)
+    return p, tgt, vec, parts
+
+
+def caller_inputs(args, p, tgt, n):
+    import numpy as np
+
+    from paper_2202_06555_b200 import irbc as I
+    from paper_2202_06555_b200.ddsg import uniform_points
+
+    xs = uniform_points(20220213, n, p.state_dim())
+    a, k = I.from_canonical(xs, p)
+    z = tgt(xs)
+    return xs, a, k, z
+
+
+def run_callers(args, rank, world, local_rank, dist):
+    import numpy as np
+    import torch
+
+    from paper_2202_06555_b200 import irbc as I
+    from paper_2202_06555_b200.ddsg import EXACT, FAST, last_eval_stats, measure_fp64_peak
+
+    torch.cuda.set_device(local_rank)
+    t0 = time.time()
+    p, tgt, vec, parts = build_irbc_policy(args)
+    vec.set_eval_mode(EXACT if args.mode == "exact" else FAST)
+    build_s = time.time() - t0
+    N, pd, Q = p.countries, p.policy_dim(), 2 * (p.countries + 1)
+    euler = args.workload == "euler"
+    n_total = args.samples if euler else args.states
+    if n_total < world:
+        raise SystemExit("fewer units than ranks")
+    n_local = n_total // world + (1 if rank < n_total % world else 0)
+    lo = rank * (n_total // world) + min(rank, n_total % world)
+    xs, a, k, z = caller_inputs(args, p, tgt, n_total)
+    xs, a, k, z = (v[lo:lo + n_local] for v in (xs, a, k, z))
+    dev = lambda v: torch.from_numpy(np.ascontiguousarray(v)).cuda()
+    xs_d, a_d, k_d, z_d = dev(xs), dev(a), dev(k), dev(z)
+    if euler:
+        step = lambda: I.euler_errors_at(vec, p, xs_d)
+        pts_per_unit = 1 + Q
+    else:
+        r0_d, _ = I.foc_residuals(vec, p, a_d, k_d, z_d)
+        step = lambda: I.foc_jacobian(vec, p, a_d, k_d, z_d, r0_d)
+        pts_per_unit = (N + 1) * Q
+    nnz, _ = vec.support(xs_d[: min(n_local, 2048)])
+    nnz_pp = float(np.asarray(nnz).mean())
+    dfma, _ = measure_fp64_peak()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches, main_ms = 0, 0.0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+        l, _, mk = last_eval_stats()
+        launches += l
+        main_ms += mk
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1), main_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t[0]) / args.steps
+    kernel_ms = float(t[1]) / args.steps
+    value = n_total / (ms_per_step / 1e3)
+    flops = 2.0 * pd * nnz_pp * pts_per_unit * n_local
+    achieved = flops / (kernel_ms / 1e3) / 1e12
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": dfma, "unit": "TFLOP/s", "frac": achieved / dfma,
+                "traffic": None, "kernel": "fast_hdmr_kernel (the batched policy evaluation)",
+                "kernel_ms": kernel_ms, "kernel_share": kernel_ms / ms_per_step,
+                "policy_points_per_step": pts_per_unit * n_local, "nnz_per_point": nnz_pp}
+    # e2e: host numpy inputs / outputs through the same call
+    if euler:
+        e_host = lambda: I.euler_errors_at(vec, p, xs)
+    else:
+        r0_h = r0_d.cpu().numpy()
+        e_host = lambda: I.foc_jacobian(vec, p, a, k, z, r0_h)
+    e_host()
+    barrier()
+    t1 = time.perf_counter()
+    for _ in range(args.steps):
+        oh = e_host()
+    e2e_s = (time.perf_counter() - t1) / args.steps
+    dt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    e2e_s = float(dt[0])
+    h2d = n_total * (p.state_dim() * 8 if euler else (2 * N + 2 * pd) * 8)
+    d2h = n_total * (8 if euler else pd * pd * 8)
+    e2e = {"value": n_total / e2e_s, "unit": "samples/s" if euler else "jacobians/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "s_per_step": e2e_s, "timing": "wall clock around the synchronous C-ABI call"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = caller_cpu_baseline(args, p, parts, *caller_inputs(args, p, tgt, max(n_total, 4096)), euler)
+        except Exception as e:
+            cpu = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        unit = "samples/s" if euler else "jacobians/s"
+        metric = ("Euler-error samples/sec (solver.hpp:377-436, 1 + 2(N+1) policy evals each)" if euler else
+                  "FOC Jacobians/sec (solver.hpp:129-165, forward differences, pdim x 2(N+1) policy evals each)")
+        print(json.dumps({
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"irbc_{args.workload}_N{N}", "countries": N, "d": 2 * N, "m": pd,
+                       "units_per_step": n_total, "policy": "config-5-shaped HDMR (2N 1-d cuts L=8, 2N pair cuts L=5)",
+                       "active_slots": vec.info()["n_active"], "nodes": vec.info()["n_nodes"],
+                       "eval_mode": args.mode, "build_s": round(build_s, 1),
+                       "l2": "successor points regenerated each step (several GB), larger than L2"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        }), flush=True)
+
+
+def caller_cpu_baseline(args, p, parts, xs, a, k, z, euler, target_s=None):
+    """The reference's foc_residuals under the oracle driver's restatements of
+    euler_errors / foc_jacobian (oracle/_ref), all host threads, bounded sample."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+
+    target_s = args.cpu_seconds if target_s is None else target_s
+    workers = cpu_cores()
+    libs = reference_variants()
+    if not libs:
+        return None
+    O._ref = None
+    O.REF_PATH = libs[-1]
+    grids = []
+    for u, b, g in parts.slots:
+        if g is None:
+            grids.append(None)
+        else:
+            kk, sur = g.nodes()
+            grids.append(O.ref_from_nodes(len(u), parts.m, g.boundary_mode, g.max_level, g.eps_gamma, kk, sur))
+    ref = O.RefHdmr(parts.d, parts.m, parts.f_anchor, [(u, b) for u, b, _ in parts.slots], grids)
+    n = max(1, workers)
+    pd = p.policy_dim()
+    while True:
+        t0 = time.perf_counter()
+        if euler:
+            O.ref_irbc_euler_errors(ref, p, xs[:n], workers=workers)
+        else:
+            O.ref_irbc_foc_residuals(ref, p, a[:n], k[:n], z[:n], workers=workers)
+        dt = time.perf_counter() - t0
+        if dt >= target_s or n >= xs.shape[0]:
+            break
+        n = min(xs.shape[0], max(n * 2, int(n * target_s / max(dt, 1e-3) * 1.1)))
+    if euler:
+        return {"value": n / dt, "unit": "samples/s", "cores": workers, "kind": "reference",
+                "sample": f"euler_errors restatement over the reference's foc_residuals, first {n} samples, "
+                          f"workers={workers} ({O.REF_PATH.name}, {dt:.1f} s)"}
+    # a forward-difference Jacobian is exactly pdim foc_residuals calls (solver.hpp:135-142)
+    return {"value": n / dt / pd, "unit": "jacobians/s", "cores": workers, "kind": "reference",
+            "sample": f"reference foc_residuals on {n} states over {workers} threads ({dt:.1f} s, "
+                      f"{O.REF_PATH.name}); jacobians/s = residuals/s / pdim ({pd} residual calls per Jacobian)"}
+
+
+def run_callers_reference(args, rank, world):
+    if rank != 0:
+        return
+    p, tgt, vec, parts = build_irbc_policy(args)
+    euler = args.workload == "euler"
+    xs, a, k, z = caller_inputs(args, p, tgt, args.samples if euler else args.states)
+    cpu = caller_cpu_baseline(args, p, parts, xs, a, k, z, euler, target_s=20.0)
+    if cpu is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libddsg_ref.so was not built"}))
+        return
+    print(json.dumps({"impl": "reference", "metric": args.workload, "value": cpu["value"], "unit": cpu["unit"],
+                      "n_gpus": world, "steps": 1, "warmup": 0, "higher_is_better": True, "dtype": "f64",
+                      "data": "synthetic", "config": {"workload": f"irbc_{args.workload}_N{p.countries}"},
+                      "cpu_baseline": cpu,
+                      "e2e": {"value": cpu["value"], "unit": cpu["unit"], "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        if args.workload != "eval":
+            run_callers_reference(args, rank, world)
+        else:
+            run_reference(args, rank, world)
         return
     dist = None
     if world > 1:
@@ -437,7 +646,10 @@ def main():
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         dist = tdist
     try:
-        run_ours(args, rank, world, local_rank, dist)
+        if args.workload != "eval":
+            run_callers(args, rank, world, local_rank, dist)
+        else:
+            run_ours(args, rank, world, local_rank, dist)
     finally:
         if dist is not None:
             dist.destroy_process_group()

@@ -425,21 +425,23 @@ int ref_irbc_steady_lambda(int countries, int variant, const double* scal, const
 }
 
 // foc_residuals (irbc.hpp:306-361) per state; clamped[i] = its return value.
+// States are spread over `workers` threads with detail::for_each_index, as
+// the time iteration's per-point solves are (time_iteration.hpp).
 int ref_irbc_foc_residuals(const ref_hdmr* h, const ref_grid* g, int countries, int variant, const double* scal,
                            const double* gamma, int64_t n, const double* a, const double* k, const double* cand,
-                           double* res, int32_t* clamped) {
+                           unsigned workers, double* res, int32_t* clamped) {
   return guarded([&] {
     const auto p = irbc_from_flat(countries, variant, scal, gamma);
     const auto quad = irbc::make_shock_quadrature(countries);
     const auto pol = ref_policy(h, g);
     const int pd = p.policy_dim();
-    irbc::FocWorkspace ws;
-    for (int64_t i = 0; i < n; ++i) {
+    detail::for_each_index(static_cast<size_t>(n), workers, [&](size_t i) {
+      thread_local irbc::FocWorkspace ws;
       const auto st = state_of(countries, a + i * countries, k + i * countries);
       const auto cv = irbc::PolicyValue::from_flat(std::span<const double>(cand + i * pd, pd), p);
       const int c = irbc::foc_residuals(st, cv, pol, p, quad, std::span<double>(res + i * pd, pd), ws);
       if (clamped) clamped[i] = c;
-    }
+    });
   });
 }
 

@@ -465,7 +465,7 @@ struct TreeStore {
   }
 };
 
-template <int kExact>
+template <int kExact, int kCarry>
 __global__ void __launch_bounds__(kPoints, 1)
     fast_hdmr_kernel(const unsigned char* __restrict__ blocks, const int64_t* __restrict__ block_off,
                      const int32_t* __restrict__ block_len, const int16_t* __restrict__ slot_dims,
@@ -479,7 +479,9 @@ __global__ void __launch_bounds__(kPoints, 1)
   unsigned char* stages = smem + kHeaderBytes;
   double2* deep = reinterpret_cast<double2*>(stages + n_stages * stage_bytes);
   const int smem_levels = min(max(levels - kTmemLevels, 0), kSmemLevels);
-  int16_t* sdims = reinterpret_cast<int16_t*>(deep + static_cast<int64_t>(smem_levels) * (kCols / 2) * kPoints);
+  // partial sums of multi-run slots between their blocks ([kCols/2][kPoints], only when present)
+  double2* carry = deep + static_cast<int64_t>(smem_levels) * (kCols / 2) * kPoints;
+  int16_t* sdims = reinterpret_cast<int16_t*>(carry + (kCarry ? (kCols / 2) * kPoints : 0));
   const bool use_tmem = levels > 0;
 
   // CTA order: column blocks in groups of cb_group; within a group, the
@@ -527,11 +529,13 @@ __global__ void __launch_bounds__(kPoints, 1)
 
   // ring position of slot a (st) and of slot a-1 (pst), with their phase
   // parities, advanced incrementally (no runtime division per slot)
+  // ring position of block a (st) and of block a-1 (pst), with their phase
+  // parities, advanced incrementally (no runtime division per block)
   int st = 0, pst = n_stages - 1;
   uint32_t ph = 0, pph = 1;
   for (int a = 0; a < n_active; ++a) {
     if (tid == 0 && a >= 1 && a - 1 + n_stages < n_active) {
-      // refill the stage released by slot a-1 (all warps arrived on its empty barrier)
+      // refill the stage released by block a-1 (all warps arrived on its empty barrier)
       const int nxt = a - 1 + n_stages;
       mbar_wait(&empty[pst], pph);
       fence_proxy_async();
@@ -543,25 +547,41 @@ __global__ void __launch_bounds__(kPoints, 1)
     const SlotHeader& H = *reinterpret_cast<const SlotHeader*>(blk);
     const HeaderCore Hc = load_core(blk);
     double acc[kCols];
+    if (kCarry && (Hc.b_kind & kBCont)) {  // a later stored-order run of the same slot: resume its sum
+      const double2* cs = carry + tid;
 #pragma unroll
-    for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+      for (int q = 0; q < kCols / 2; ++q) {
+        const double2 v = cs[q * kPoints];
+        acc[2 * q] = v.x;
+        acc[2 * q + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+    }
     const int k = Hc.k;
     const double x0 = xc0, x1 = xc1;
-    if (a + 1 < n_active) {  // prefetch the next slot's coordinates
+    if (a + 1 < n_active) {  // prefetch the next block's coordinates
       xc0 = xt[static_cast<int64_t>(sdims[2 * (a + 1)]) * n + pc];
       xc1 = xt[static_cast<int64_t>(sdims[2 * (a + 1) + 1]) * n + pc];
     }
+    bool leaf_done = true;
     if (k == 0) {
       const double* r0 = reinterpret_cast<const double*>(blk + Hc.table_off);
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = r0[c];
     } else {
       leaf_dispatch<kExact>(Hc, H, blk, x0, x1, acc);
-      if (Hc.b_kind == 0) {
+      if (kCarry && (Hc.b_kind & kBMore)) {  // more runs of this slot follow: park the partial sum
+        double2* cs = carry + tid;
+#pragma unroll
+        for (int q = 0; q < kCols / 2; ++q) cs[q * kPoints] = make_double2(acc[2 * q], acc[2 * q + 1]);
+        leaf_done = false;
+      } else if ((Hc.b_kind & 3) == 0) {
         const double b = Hc.b;
 #pragma unroll
         for (int c = 0; c < kCols; ++c) acc[c] = __dmul_rn(acc[c], b);
-      } else if (Hc.b_kind == 2) {
+      } else if ((Hc.b_kind & 3) == 2) {
 #pragma unroll
         for (int c = 0; c < kCols; ++c) acc[c] = -acc[c];
       }
@@ -570,7 +590,7 @@ __global__ void __launch_bounds__(kPoints, 1)
     // siblings at levels s.. while the position bit is set, then park.
     const int t = Hc.tree_t;
     int i = Hc.tree_s;
-    {
+    if (!kCarry || leaf_done) {
       while (i < levels && ((t >> i) & 1)) {
         double v[kCols];
         store.load(i, v);
@@ -688,106 +708,128 @@ bool FastHdmr::build(const HostProgram& hp) {
     Rec::go(0, na, 0, levels, tree_t, tree_s);
   }
 
-  // per-slot headers (column-block independent part)
+  // Staged blocks (column-block independent part): one per active slot, or
+  // one per stored-order run of a slot whose grid is stored in several
+  // canonically sorted runs.  The blocks of a multi-run slot
+  // hold disjoint row sets; the kernel accumulates them in run order
+  // (b_kind flags kBCont / kBMore), exactly the reference's stored order.
   struct SlotPlan {
     SlotHeader h;
-    int64_t row_begin = 0, rows = 0;
+    std::vector<int64_t> rows;  // program rows staged in this block, in order
     std::vector<int16_t> slab;
     int64_t bytes = 0;
+    int slot = 0;
   };
-  std::vector<SlotPlan> plans(na);
+  std::vector<SlotPlan> plans;
   std::vector<int16_t> dims16;
   int64_t max_bytes = 0;
   for (int a = 0; a < na; ++a) {
-    SlotPlan& P = plans[a];
-    std::memset(&P.h, 0, sizeof(SlotHeader));
-    SlotHeader& H = P.h;
     const int k = hp.slot_k[a];
     if (k > 2) {
       why_ = "slot order > 2";
       return false;
     }
-    if (hp.slot_runs[a] != 1) {
-      why_ = "grid stored in non-canonical order (multi-run evaluation is on the generic kernel)";
-      return false;
-    }
-    H.k = k;
-    H.mode = hp.slot_mode[a];
-    H.tree_t = tree_t[a];
-    H.tree_s = tree_s[a];
-    H.table_off = sizeof(SlotHeader);
-    dims16.push_back(0);
-    dims16.push_back(0);
-    if (k == 0) {
-      H.b_kind = 1;  // b * f_anchor is folded into the staged row
-      P.rows = 1;
-    } else {
-      const double b = hp.slot_b[a];
-      H.b = b;
-      H.b_kind = b == 1.0 ? 1 : (b == -1.0 ? 2 : 0);
-      H.d0 = hp.slot_dims[hp.slot_dims_off[a]];
-      H.d1 = k == 2 ? hp.slot_dims[hp.slot_dims_off[a] + 1] : 0;
-      if (H.d0 > 32767 || H.d1 > 32767) {
-        why_ = "point dimension above 32767";
-        return false;
-      }
-      dims16[2 * a] = static_cast<int16_t>(H.d0);
-      dims16[2 * a + 1] = static_cast<int16_t>(H.d1);
-      P.row_begin = hp.slot_row_begin[a];
-      P.rows = hp.slot_row_end[a] - hp.slot_row_begin[a];
-      if (P.rows > 32767) {
-        why_ = "slot has more than 32767 nodes";
-        return false;
-      }
-      int nlev = 0;
-      for (int s = hp.slot_sub_begin[a]; s < hp.slot_sub_end[a]; ++s) {
-        const uint8_t* lv = &hp.levels[hp.sub_lv_off[s]];
-        const int l1 = lv[0], l2 = k == 2 ? lv[1] : 0;
-        nlev = std::max(nlev, std::max(l1, l2));
-        if ((k == 1 && l1 > kL1) || (k == 2 && (l1 > kL2 || l2 > kL2))) {
-          why_ = "slot level above the kernel's static maximum";
+    const int runs = k == 0 ? 1 : hp.slot_runs[a];
+    const int64_t row_begin = k == 0 ? 0 : hp.slot_row_begin[a];
+    const int64_t row_count = k == 0 ? 0 : hp.slot_row_end[a] - row_begin;
+    std::vector<int32_t> local(static_cast<size_t>(row_count), -1);
+    for (int r = 0; r < runs; ++r) {
+      plans.emplace_back();
+      SlotPlan& P = plans.back();
+      P.slot = a;
+      std::memset(&P.h, 0, sizeof(SlotHeader));
+      SlotHeader& H = P.h;
+      H.k = k;
+      H.mode = hp.slot_mode[a];
+      H.tree_t = tree_t[a];
+      H.tree_s = tree_s[a];
+      H.table_off = sizeof(SlotHeader);
+      const int flags = (r > 0 ? kBCont : 0) | (r + 1 < runs ? kBMore : 0);
+      dims16.push_back(0);
+      dims16.push_back(0);
+      const size_t di = dims16.size() - 2;
+      if (k == 0) {
+        H.b_kind = 1;  // b * f_anchor is folded into the staged row
+        P.rows.push_back(-1);
+      } else {
+        const double b = hp.slot_b[a];
+        H.b = b;
+        H.b_kind = (b == 1.0 ? 1 : (b == -1.0 ? 2 : 0)) | flags;
+        H.d0 = hp.slot_dims[hp.slot_dims_off[a]];
+        H.d1 = k == 2 ? hp.slot_dims[hp.slot_dims_off[a] + 1] : 0;
+        if (H.d0 > 32767 || H.d1 > 32767) {
+          why_ = "point dimension above 32767";
           return false;
         }
-        const int idx = canon_index(k, l1, l2);
-        const int64_t cells = int64_t{1} << (l1 - 1 + (k == 2 ? l2 - 1 : 0));
-        H.present |= 1u << idx;
-        const int32_t* slab = &hp.slab[hp.sub_slab_off[s]];
-        if (hp.sub_nodes[s] == cells) {
-          H.full |= 1u << idx;
-          H.sub_base[idx] = static_cast<int16_t>(slab[0] - P.row_begin);
-        } else {
-          if (P.slab.size() + cells > 32767) {
-            why_ = "slab too large";
+        dims16[di] = static_cast<int16_t>(H.d0);
+        dims16[di + 1] = static_cast<int16_t>(H.d1);
+        std::fill(local.begin(), local.end(), -1);
+        for (int64_t q = 0; q < row_count; ++q)
+          if (runs == 1 || hp.row_run[row_begin + q] == r) {
+            local[q] = static_cast<int32_t>(P.rows.size());
+            P.rows.push_back(row_begin + q);
+          }
+        if (P.rows.size() > 32766) {
+          why_ = "slot has more than 32766 nodes";
+          return false;
+        }
+        int nlev = 0;
+        for (int sb = hp.slot_sub_begin[a]; sb < hp.slot_sub_end[a]; ++sb) {
+          const uint8_t* lv = &hp.levels[hp.sub_lv_off[sb]];
+          const int l1 = lv[0], l2 = k == 2 ? lv[1] : 0;
+          // the order-2 leaf walks every (l1, l2) with l1 + l2 <= nlev + 1
+          const int reach = k == 2 ? l1 + l2 - 1 : l1;
+          if ((k == 1 && l1 > kL1) || (k == 2 && reach > kL2)) {
+            why_ = "slot level above the kernel's static maximum";
             return false;
           }
-          H.sub_base[idx] = static_cast<int16_t>(P.slab.size());
-          for (int64_t c = 0; c < cells; ++c)
-            P.slab.push_back(slab[c] < 0 ? int16_t{-1} : static_cast<int16_t>(slab[c] - P.row_begin));
-        }
-      }
-      H.nlev = nlev;
-      {
-        // fast_full: the grid is the full grid of its max level (every canonical
-        // subspace present and complete) and all its surpluses are finite
-        const int nsub = k == 1 ? nlev : nlev * (nlev + 1) / 2;
-        const uint32_t all = nsub >= 32 ? 0xffffffffu : ((1u << nsub) - 1u);
-        bool finite = true;
-        for (int64_t r = 0; r < P.rows && finite; ++r)
-          for (int c = 0; c < m_; ++c)
-            if (!std::isfinite(hp.surplus[(P.row_begin + r) * m_ + c])) {
-              finite = false;
-              break;
+          const int idx = canon_index(k, l1, l2);
+          const int64_t cells = int64_t{1} << (l1 - 1 + (k == 2 ? l2 - 1 : 0));
+          const int32_t* slab = &hp.slab[hp.sub_slab_off[sb]];
+          int64_t n_in = 0;
+          for (int64_t c = 0; c < cells; ++c) n_in += slab[c] >= 0 && local[slab[c] - row_begin] >= 0;
+          if (n_in == 0) continue;  // no node of this run in the subspace
+          nlev = std::max(nlev, reach);
+          H.present |= 1u << idx;
+          if (n_in == cells) {  // complete: its rows are consecutive in canonical order
+            H.full |= 1u << idx;
+            H.sub_base[idx] = static_cast<int16_t>(local[slab[0] - row_begin]);
+          } else {
+            if (P.slab.size() + cells > 32767) {
+              why_ = "slab too large";
+              return false;
             }
-        H.fast_full = (H.present == all && H.full == all && finite) ? 1 : 0;
+            H.sub_base[idx] = static_cast<int16_t>(P.slab.size());
+            for (int64_t c = 0; c < cells; ++c)
+              P.slab.push_back(slab[c] < 0 ? int16_t{-1} : static_cast<int16_t>(local[slab[c] - row_begin]));
+          }
+        }
+        H.nlev = std::max(nlev, 1);
+        {
+          // fast_full: the block is the full grid of its max level (every
+          // canonical subspace present and complete) with finite surpluses
+          const int nsub = k == 1 ? nlev : nlev * (nlev + 1) / 2;
+          const uint32_t all = nsub >= 32 ? 0xffffffffu : ((1u << nsub) - 1u);
+          bool finite = true;
+          for (size_t q = 0; q < P.rows.size() && finite; ++q)
+            for (int c = 0; c < m_; ++c)
+              if (!std::isfinite(hp.surplus[P.rows[q] * m_ + c])) {
+                finite = false;
+                break;
+              }
+          H.fast_full = (nlev > 0 && H.present == all && H.full == all && finite) ? 1 : 0;
+        }
+        H.zero_row = static_cast<int32_t>(P.rows.size());  // all-zero row appended to the table
+        P.rows.push_back(-1);
       }
-      H.zero_row = static_cast<int32_t>(P.rows);  // all-zero row appended to the table
-      P.rows += 1;
+      const int64_t table_bytes = static_cast<int64_t>(P.rows.size()) * kStride * 8;
+      H.slab_off = static_cast<int32_t>(sizeof(SlotHeader) + table_bytes);
+      P.bytes = (sizeof(SlotHeader) + table_bytes + P.slab.size() * 2 + 15) / 16 * 16;
+      max_bytes = std::max(max_bytes, P.bytes);
     }
-    const int64_t table_bytes = P.rows * kStride * 8;
-    H.slab_off = static_cast<int32_t>(sizeof(SlotHeader) + table_bytes);
-    P.bytes = (sizeof(SlotHeader) + table_bytes + P.slab.size() * 2 + 15) / 16 * 16;
-    max_bytes = std::max(max_bytes, P.bytes);
   }
+  const int nb = static_cast<int>(plans.size());
+  n_blocks_ = nb;
   block_bytes_ = (max_bytes + 127) / 128 * 128;
   {
     int64_t per_cb = 0;
@@ -796,7 +838,8 @@ bool FastHdmr::build(const HostProgram& hp) {
     cb_group_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_cb_, budget / std::max<int64_t>(per_cb, 1))));
   }
   const int64_t deep_bytes = std::min(std::max(0, levels - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
-  const int64_t fixed = kHeaderBytes + deep_bytes + (4 * int64_t{na} + 15) / 16 * 16;
+  has_carry_ = nb > na ? 1 : 0;
+  const int64_t fixed = kHeaderBytes + deep_bytes + has_carry_ * int64_t{kCols} * kPoints * 8 + (4 * int64_t{nb} + 15) / 16 * 16;
   n_stages_ = static_cast<int>(std::min<int64_t>(kMaxStages, (227 * 1024 - fixed) / block_bytes_));
   const int64_t smem = fixed + int64_t{n_stages_} * block_bytes_;
   if (n_stages_ < 2 || smem > 227 * 1024) {
@@ -805,32 +848,32 @@ bool FastHdmr::build(const HostProgram& hp) {
   }
 
   // column-blocked staged blocks
-  std::vector<int64_t> off(static_cast<size_t>(n_cb_) * na);
-  std::vector<int32_t> len(static_cast<size_t>(n_cb_) * na);
+  std::vector<int64_t> off(static_cast<size_t>(n_cb_) * nb);
+  std::vector<int32_t> len(static_cast<size_t>(n_cb_) * nb);
   int64_t total = 0;
   for (int cb = 0; cb < n_cb_; ++cb)
-    for (int a = 0; a < na; ++a) {
-      off[static_cast<size_t>(cb) * na + a] = total;
-      len[static_cast<size_t>(cb) * na + a] = static_cast<int32_t>(plans[a].bytes);
+    for (int a = 0; a < nb; ++a) {
+      off[static_cast<size_t>(cb) * nb + a] = total;
+      len[static_cast<size_t>(cb) * nb + a] = static_cast<int32_t>(plans[a].bytes);
       total += plans[a].bytes;
     }
   std::vector<unsigned char> host(total, 0);
   for (int cb = 0; cb < n_cb_; ++cb)
-    for (int a = 0; a < na; ++a) {
+    for (int a = 0; a < nb; ++a) {
       const SlotPlan& P = plans[a];
-      unsigned char* blk = host.data() + off[static_cast<size_t>(cb) * na + a];
+      unsigned char* blk = host.data() + off[static_cast<size_t>(cb) * nb + a];
       std::memcpy(blk, &P.h, sizeof(SlotHeader));
       double* table = reinterpret_cast<double*>(blk + sizeof(SlotHeader));
-      for (int64_t r = 0; r < P.rows; ++r)
+      const bool empty_slot = hp.slot_k[P.slot] == 0;
+      for (size_t r = 0; r < P.rows.size(); ++r)
         for (int c = 0; c < kCols; ++c) {
           const int col = cb * kCols + c;
           double v = 0.0;
-          const bool zero_row = hp.slot_k[a] != 0 && r == P.rows - 1;
-          if (col < m_ && !zero_row) {
-            if (hp.slot_k[a] == 0)
-              v = hp.slot_b[a] * hp.f_anchor[col];  // row = b * f_anchor (ddsg_eval.hpp:94-96)
-            else
-              v = hp.surplus[(P.row_begin + r) * m_ + col];
+          if (col < m_) {
+            if (empty_slot)
+              v = hp.slot_b[P.slot] * hp.f_anchor[col];  // row = b * f_anchor (ddsg_eval.hpp:94-96)
+            else if (P.rows[r] >= 0)
+              v = hp.surplus[P.rows[r] * m_ + col];  // (the zero row stays 0)
           }
           table[r * kStride + c] = v;
         }
@@ -845,9 +888,13 @@ bool FastHdmr::build(const HostProgram& hp) {
   DDSG_CUDA(cudaMemcpy(slot_dims_, dims16.data(), dims16.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
   DDSG_CUDA(cudaMalloc(&block_len_, len.size() * sizeof(int32_t)));
   DDSG_CUDA(cudaMemcpy(block_len_, len.data(), len.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  DDSG_CUDA(cudaFuncSetAttribute(fast_hdmr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  DDSG_CUDA(cudaFuncSetAttribute(fast_hdmr_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-  DDSG_CUDA(cudaFuncSetAttribute(fast_hdmr_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  DDSG_CUDA(cudaFuncSetAttribute(fast_hdmr_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  DDSG_CUDA(cudaFuncSetAttribute(fast_hdmr_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  DDSG_CUDA(cudaFuncSetAttribute(fast_hdmr_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   usable_ = true;
   why_.clear();
@@ -862,17 +909,14 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   DDSG_CUDA(cudaGetLastError());
   const int64_t tiles = (n + kPoints - 1) / kPoints;
   const int64_t deep_bytes = std::min(std::max(0, levels_ - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
-  const size_t smem = kHeaderBytes + n_stages_ * block_bytes_ + deep_bytes + (4 * static_cast<size_t>(n_active_) + 15) / 16 * 16;
+  const size_t smem = kHeaderBytes + n_stages_ * block_bytes_ + deep_bytes + has_carry_ * size_t{kCols} * kPoints * 8 +
+                      (4 * static_cast<size_t>(n_blocks_) + 15) / 16 * 16;
   const dim3 grid(static_cast<unsigned>(tiles * n_cb_));
   kernel_timer().begin(st);
-  if (exact)
-    fast_hdmr_kernel<1><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
-                                                     block_len_, slot_dims_, n_active_, n_cb_, cb_group_, levels_, xt, n, m_, y,
-                                                     block_bytes_, n_stages_);
-  else
-    fast_hdmr_kernel<0><<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_,
-                                                     block_len_, slot_dims_, n_active_, n_cb_, cb_group_, levels_, xt, n, m_, y,
-                                                     block_bytes_, n_stages_);
+  auto kern = exact ? (has_carry_ ? fast_hdmr_kernel<1, 1> : fast_hdmr_kernel<1, 0>)
+                    : (has_carry_ ? fast_hdmr_kernel<0, 1> : fast_hdmr_kernel<0, 0>);
+  kern<<<grid, kPoints, smem, st>>>(static_cast<const unsigned char*>(blocks_), block_off_, block_len_, slot_dims_,
+                                    n_blocks_, n_cb_, cb_group_, levels_, xt, n, m_, y, block_bytes_, n_stages_);
   kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());
   return 2;

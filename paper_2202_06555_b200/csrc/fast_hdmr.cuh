@@ -46,6 +46,8 @@ constexpr int kSmemLevels = 4;           // levels 9..12 in shared memory (level
 constexpr int kMaxLevels = kTmemLevels + kSmemLevels;  // 2^12 active slots
 constexpr int kMaxStages = 4;            // shared-memory ring depth (fewer when slot blocks are large)
 constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
+constexpr int kBCont = 4;   // b_kind flag: continue the previous block's accumulation (later run)
+constexpr int kBMore = 8;   // b_kind flag: another run of the same slot follows
 
 // Per-slot header at the front of every staged block (16-B aligned, 160 B).
 struct SlotHeader {
@@ -55,7 +57,7 @@ struct SlotHeader {
   int32_t d0, d1;     // point dims of the slot
   int32_t tree_t;     // leaf position in the perfect-tree embedding
   int32_t tree_s;     // leaf span exponent
-  int32_t b_kind;     // 0: multiply by b, 1: b == 1, 2: b == -1
+  int32_t b_kind;     // bits 0-1: 0 multiply by b, 1 b == 1, 2 b == -1; | kBCont | kBMore
   double b;
   uint32_t present;   // bit i: canonical subspace i has nodes
   uint32_t full;      // bit i: canonical subspace i has all its cells
@@ -92,7 +94,8 @@ class FastHdmr {
  private:
   bool usable_ = false;
   std::string why_;
-  int d_ = 0, m_ = 0, n_cb_ = 0, cb_group_ = 1, n_active_ = 0, levels_ = 0, n_stages_ = fast::kMaxStages;
+  int d_ = 0, m_ = 0, n_cb_ = 0, cb_group_ = 1, n_active_ = 0, n_blocks_ = 0, has_carry_ = 0, levels_ = 0,
+      n_stages_ = fast::kMaxStages;
   int64_t block_bytes_ = 0;  // stage size (max block), multiple of 128
   void* blocks_ = nullptr;   // [n_cb][n_active] blocks of block_bytes_ each (offsets below)
   int64_t* block_off_ = nullptr;  // device: [n_cb * n_active] byte offsets

@@ -104,7 +104,7 @@ def ref():
         L.ref_irbc_steady_lambda.restype = _i
         L.ref_irbc_steady_lambda.argtypes = [_i, _i, _p, _p, C.POINTER(_d)]
         L.ref_irbc_foc_residuals.restype = _i
-        L.ref_irbc_foc_residuals.argtypes = [_p, _p, _i, _i, _p, _p, _i64, _p, _p, _p, _p, _p]
+        L.ref_irbc_foc_residuals.argtypes = [_p, _p, _i, _i, _p, _p, _i64, _p, _p, _p, C.c_uint, _p, _p]
         L.ref_irbc_foc_jacobian.restype = _i
         L.ref_irbc_foc_jacobian.argtypes = [_p, _p, _i, _i, _p, _p, _i64, _p, _p, _p, _p, _d, _p]
         L.ref_irbc_euler_errors.restype = _i
@@ -348,7 +348,7 @@ def _policy_handles(policy):
     return None, policy.h
 
 
-def ref_irbc_foc_residuals(policy, p, a, k, cand):
+def ref_irbc_foc_residuals(policy, p, a, k, cand, workers=1):
     a, k, cand = (np.ascontiguousarray(v, dtype=np.float64) for v in (a, k, cand))
     n, pd = cand.shape
     res = np.empty((n, pd))
@@ -356,7 +356,7 @@ def ref_irbc_foc_residuals(policy, p, a, k, cand):
     h, g = _policy_handles(policy)
     sc, gi = _irbc_scal(p), _irbc_gamma(p)
     rc = ref().ref_irbc_foc_residuals(h, g, p.countries, p.variant, _ptr(sc), _ptr(gi), n,
-                                      _ptr(a), _ptr(k), _ptr(cand), _ptr(res), _ptr(cl))
+                                      _ptr(a), _ptr(k), _ptr(cand), workers, _ptr(res), _ptr(cl))
     assert rc == 0, ref().ref_last_error()
     return res, cl
 

@@ -259,9 +259,10 @@ def test_hdmr_configs_run_on_slot_kernel(cid, config4, config5):
     assert vec.uses_slot_kernel()
 
 
-def test_hdmr_stored_order_grids_fall_back_exactly():
-    """An HDMR whose component grids are stored out of canonical order is
-    evaluated on the generic kernel in stored order, still bit-exact."""
+def test_hdmr_stored_order_grids_exact():
+    """An HDMR whose component grids are stored out of canonical order runs on
+    the slot kernel run by run (one staged block per stored-order run), in
+    stored order, still bit-exact."""
     z = load(golden_files("hdmr")[0])
     slots = hdmr_slots_from_golden(z, canonical=False)
     rng = np.random.default_rng(3)
@@ -274,4 +275,5 @@ def test_hdmr_stored_order_grids_fall_back_exactly():
             shuffled.append((u, b, (g[0], g[1][p], g[2][p])))
     vec = make_vectorized(int(z["d"]), int(z["m"]), z["f_anchor"], shuffled, int(z["max_level"]), float(z["eps"]))
     rc, want, _ = O.port_hdmr_eval(int(z["d"]), int(z["m"]), z["f_anchor"], shuffled, z["x"])
+    assert vec.uses_slot_kernel()
     assert np.array_equal(bits(vec.evaluate_batch(z["x"])), bits(want))

@@ -155,6 +155,25 @@ CASES = ["smooth2", "nonsmooth3", "grid4"]
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", CASES)
+def test_policy_evaluation_is_bitwise_reference(case, request):
+    """The policies are adaptive builds stored in several runs; the batched
+    evaluation underneath the callers is the reference's, bit for bit."""
+    need_ref()
+    p, t, pol, parts, rpol = request.getfixturevalue(case)
+    x, _, _ = random_states(p, 500, 21)
+    if parts is None:
+        got = pol.interpolate(x)
+        rc, want = rpol.eval(x, p.policy_dim())
+    else:
+        assert pol.uses_slot_kernel()
+        got = pol.evaluate_batch(x)
+        rc, want = rpol.eval(x)
+    assert rc == 0
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
 def test_foc_residuals_match_reference(case, request):
     need_ref()
     p, t, pol, parts, rpol = request.getfixturevalue(case)
