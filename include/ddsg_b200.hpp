@@ -13,6 +13,8 @@
 //   task_error           runtime.hpp:71-92
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <exception>
 #include <functional>
@@ -396,6 +398,8 @@ class VectorizedDdsg {  // ddsg_eval.hpp:28-165
     return q;
   }
 
+  const ddsg_hdmr_t* handle() const { return h_.get(); }
+
  private:
   std::shared_ptr<const DdsgFunction> source_;
   std::shared_ptr<ddsg_hdmr_t> h_;
@@ -403,3 +407,141 @@ class VectorizedDdsg {  // ddsg_eval.hpp:28-165
 };
 
 }  // namespace ddsg_b200
+
+// ---------------------------------------------------------------------------
+// Batched IRBC policy callers: irbc.hpp /
+// solver.hpp names, with the per-point loops replaced by batches whose
+// successor states are evaluated in one device call.
+namespace ddsg_b200::irbc {
+
+enum class Variant { smooth, nonsmooth };  // irbc.hpp:25
+
+struct IrbcParameters {  // irbc.hpp:27-53, same defaults
+  int countries = 2;
+  double beta = 0.99;
+  double alpha = 0.36;
+  double delta = 0.01;
+  double sigma = 0.01;
+  double rho_a = 0.95;
+  double phi_adj = 0.50;
+  double gamma_base = 0.25;
+  std::vector<double> gamma;
+  Variant variant = Variant::smooth;
+  double lna_half_width = 0.4;
+  double k_lo = 0.5;
+  double k_hi = 1.5;
+  double A = 0.0;
+  std::vector<double> tau;
+
+  int state_dim() const { return 2 * countries; }
+  int policy_dim() const { return variant == Variant::smooth ? countries + 1 : 2 * countries + 1; }
+};
+
+namespace detail {
+// Flat view of the parameters; gamma/tau buffers live in the caller's object.
+inline ddsg_irbc_params flat(IrbcParameters& p) {
+  p.gamma.resize(static_cast<std::size_t>(p.countries > 0 ? p.countries : 0));
+  p.tau.resize(p.gamma.size());
+  ddsg_irbc_params c{};
+  c.countries = p.countries;
+  c.variant = p.variant == Variant::smooth ? DDSG_IRBC_SMOOTH : DDSG_IRBC_NONSMOOTH;
+  c.beta = p.beta;
+  c.alpha = p.alpha;
+  c.delta = p.delta;
+  c.sigma = p.sigma;
+  c.rho_a = p.rho_a;
+  c.phi_adj = p.phi_adj;
+  c.gamma_base = p.gamma_base;
+  c.lna_half_width = p.lna_half_width;
+  c.k_lo = p.k_lo;
+  c.k_hi = p.k_hi;
+  c.A = p.A;
+  c.gamma = p.gamma.data();
+  c.tau = p.tau.data();
+  return c;
+}
+}  // namespace detail
+
+// irbc.hpp:59-92
+inline void refresh_derived(IrbcParameters& p) {
+  if (!p.gamma.empty() && p.gamma.size() != static_cast<std::size_t>(p.countries))
+    throw std::invalid_argument("irbc: gamma length must equal countries");
+  const bool fill = p.gamma.empty();
+  ddsg_irbc_params c = detail::flat(p);
+  ::ddsg_b200::detail::check(ddsg_irbc_refresh_derived(&c, fill ? 1 : 0));
+  p.A = c.A;
+}
+
+inline IrbcParameters make_parameters(int countries, Variant variant, double gamma_base = 0.25) {
+  IrbcParameters p;  // irbc.hpp:94-101
+  p.countries = countries;
+  p.variant = variant;
+  p.gamma_base = gamma_base;
+  refresh_derived(p);
+  return p;
+}
+
+inline double steady_state_lambda(IrbcParameters p) {  // irbc.hpp:248-263
+  ddsg_irbc_params c = detail::flat(p);
+  double lam = 0.0;
+  ::ddsg_b200::detail::check(ddsg_irbc_steady_state_lambda(&c, &lam));
+  return lam;
+}
+
+// foc_residuals (irbc.hpp:306-361) for n states: a, k [n][N], candidate /
+// residuals [n][pdim]; returns the clamped-successor count per state.
+// Host or device pointers.
+inline std::vector<int32_t> foc_residuals_batch(const VectorizedDdsg& policy_next, IrbcParameters p, int64_t n,
+                                                const double* a, const double* k, const double* candidate,
+                                                double* residuals, void* stream = nullptr) {
+  ddsg_irbc_params c = detail::flat(p);
+  std::vector<int32_t> clamped(static_cast<std::size_t>(n));
+  int64_t bad = -1;
+  const ddsg_status s = ddsg_irbc_foc_residuals(policy_next.handle(), nullptr, &c, n, a, k, candidate, residuals,
+                                                clamped.data(), &bad, stream);
+  if (s != DDSG_OK) ::ddsg_b200::detail::raise(s, true, bad);
+  return clamped;
+}
+
+// foc_jacobian (solver.hpp:129-165) for n states: jac [n][pdim][pdim].
+inline void foc_jacobian_batch(const VectorizedDdsg& policy_next, IrbcParameters p, int64_t n, const double* a,
+                               const double* k, const double* z, const double* r0, double* jac,
+                               double fd_epsilon = 1e-7, void* stream = nullptr) {
+  ddsg_irbc_params c = detail::flat(p);
+  int64_t bad = -1;
+  const ddsg_status s =
+      ddsg_irbc_foc_jacobian(policy_next.handle(), nullptr, &c, n, a, k, z, r0, fd_epsilon, jac, &bad, stream);
+  if (s != DDSG_OK) ::ddsg_b200::detail::raise(s, true, bad);
+}
+
+struct EulerErrors {  // solver.hpp:369-373
+  double avg_log10 = 0.0;
+  double max_log10 = 0.0;
+  std::vector<double> samples;
+};
+
+// euler_errors (solver.hpp:377-436): the same sample stream
+// (std::mt19937_64(seed), uniform (0,1), point-major); `workers` kept for
+// signature parity (the result never depends on it).
+inline EulerErrors euler_errors(const VectorizedDdsg& policy, IrbcParameters p, int n_samples, uint64_t seed,
+                                unsigned workers = 1, uint64_t* clamp_count = nullptr) {
+  (void)workers;
+  if (n_samples < 1) throw std::invalid_argument("euler_errors: n_samples must be >= 1");
+  std::vector<double> xs(static_cast<std::size_t>(n_samples) * static_cast<std::size_t>(p.state_dim()));
+  ddsg_uniform_points(seed, n_samples, p.state_dim(), xs.data());
+  ddsg_irbc_params c = detail::flat(p);
+  EulerErrors out;
+  out.samples.resize(static_cast<std::size_t>(n_samples));
+  double mean = 0.0, worst = 0.0;
+  uint64_t cl = 0;
+  int64_t bad = -1;
+  const ddsg_status s = ddsg_irbc_euler_errors(policy.handle(), nullptr, &c, n_samples, xs.data(),
+                                               out.samples.data(), &mean, &worst, &cl, &bad, nullptr);
+  if (s != DDSG_OK) ::ddsg_b200::detail::raise(s);
+  out.avg_log10 = std::log10(std::max(mean, 1e-16));
+  out.max_log10 = std::log10(std::max(worst, 1e-16));
+  if (clamp_count) *clamp_count += cl;
+  return out;
+}
+
+}  // namespace ddsg_b200::irbc

@@ -381,10 +381,74 @@ static void gpu_cases() {
   }
 }
 
+// Batched IRBC callers through the shim (test_irbc.cpp:28-52, 189-206;
+// test_solver.cpp:170-196).
+static void irbc_cpu_cases() {
+  using namespace ddsg_b200::irbc;
+  auto p = make_parameters(4, Variant::smooth);
+  CHECK(std::abs(p.A - (1.0 - 0.99 * 0.99) / (0.36 * 0.99)) <= 1e-15);
+  CHECK(p.gamma.size() == 4 && p.gamma[1] == 0.5 && p.gamma[3] == 1.0);
+  CHECK(std::abs(1.0 - p.beta * (p.alpha * p.A + 1.0 - p.delta)) < 1e-12);
+  for (int j = 0; j < 4; ++j) CHECK(std::abs(p.tau[j] - std::pow(p.A, 1.0 / p.gamma[j])) <= 1e-15);
+  const double lam = steady_state_lambda(p);
+  double sum = 0.0;
+  for (double g : p.gamma) sum += p.A * std::pow(lam, -g);
+  CHECK(std::abs(sum - 4.0 * (p.A - p.delta)) <= 1e-10);
+  IrbcParameters bad = p;
+  bad.beta = 1.5;
+  CHECK(throws<std::invalid_argument>([&] { refresh_derived(bad); }));
+}
+
+static void irbc_gpu_cases() {
+  using namespace ddsg_b200::irbc;
+  // steady policy k' = k, lambda = lambda_ss as a 1-d-cut HDMR (exact for linear cuts)
+  auto p = make_parameters(2, Variant::smooth);
+  p.gamma.assign(2, 0.25);
+  p.sigma = 0.0;
+  refresh_derived(p);
+  const double lam = steady_state_lambda(p);
+  const double klo = p.k_lo, khi = p.k_hi;
+  GridEvaluator steady = [=](std::span<const double> x, std::span<double> out) {
+    out[0] = klo + x[2] * (khi - klo);
+    out[1] = klo + x[3] * (khi - klo);
+    out[2] = lam;
+  };
+  auto src = full_decomposition(steady, 4, 3, 1, 2, BoundaryMode::modified_linear);
+  const auto pol = VectorizedDdsg::compile(src);
+  const double a[2] = {1.0, 1.0}, k[2] = {1.0, 1.0}, cand[3] = {1.0, 1.0, lam};
+  double res[3];
+  const auto cl = foc_residuals_batch(pol, p, 1, a, k, cand, res);
+  CHECK(cl.size() == 1 && cl[0] == 0);
+  for (double r : res) CHECK(std::abs(r) < 1e-10);
+  // Euler errors on a degenerate box are exact and deterministic
+  auto q = p;
+  q.k_lo = 1.0 - 5e-11;
+  q.k_hi = 1.0 + 5e-11;
+  q.lna_half_width = 5e-11;
+  refresh_derived(q);
+  const double lq = steady_state_lambda(q);
+  GridEvaluator steady_q = [=](std::span<const double> x, std::span<double> out) {
+    out[0] = q.k_lo + x[2] * (q.k_hi - q.k_lo);
+    out[1] = q.k_lo + x[3] * (q.k_hi - q.k_lo);
+    out[2] = lq;
+  };
+  const auto pq = VectorizedDdsg::compile(full_decomposition(steady_q, 4, 3, 1, 2, BoundaryMode::modified_linear));
+  const auto e1 = euler_errors(pq, q, 500, 99);
+  const auto e2 = euler_errors(pq, q, 500, 99, 4);
+  CHECK(e1.avg_log10 < -8.0 && e1.max_log10 < -8.0);
+  CHECK(e1.samples == e2.samples && e1.avg_log10 == e2.avg_log10);
+}
+
 int main(int argc, char** argv) {
   const std::string which = argc > 1 ? argv[1] : "cpu";
-  if (which == "cpu" || which == "all") cpu_cases();
-  if (which == "gpu" || which == "all") gpu_cases();
+  if (which == "cpu" || which == "all") {
+    cpu_cases();
+    irbc_cpu_cases();
+  }
+  if (which == "gpu" || which == "all") {
+    gpu_cases();
+    irbc_gpu_cases();
+  }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;
 }

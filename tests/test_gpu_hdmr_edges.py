@@ -142,3 +142,31 @@ def test_many_slots_deep_tree():
     vec, fa, so = make(d, m, fam, {1: 3, 2: 2})
     assert vec.uses_slot_kernel()
     check(vec, d, m, fa, so, pts(d, 600))
+
+
+@pytest.mark.parametrize("mode", [MODIFIED_LINEAR, ZERO_BOUNDARY])
+def test_order2_subspace_beyond_max_single_level(mode):
+    """A pair grid holding (2,2) but no level-3 subspace: its max single level
+    is 2 while its level sum reaches 4, so the slot kernel must walk every
+    (l1, l2) with l1 + l2 <= 4 (nlev = max level sum - 1)."""
+    rng = np.random.default_rng(11)
+    keys = [k for k in full_keys(2, 3) if all(int(v).bit_length() <= 2 for v in k)]
+    keys = np.array(keys, dtype=np.uint32)
+    assert any(int(a).bit_length() == 2 and int(b).bit_length() == 2 for a, b in keys)
+    d, m = 3, 5
+    family = [(), (0,), (1,), (2,), (0, 2)]
+    b = telescoping_b(family)
+    fa = rng.uniform(-1, 1, m)
+    slots_o, slots_g = [], []
+    for u, bu in zip(family, b):
+        if not u:
+            slots_o.append((u, bu, None))
+            slots_g.append((u, bu, None))
+            continue
+        kk = keys if len(u) == 2 else full_keys(1, 4)
+        sur = rng.uniform(-1, 1, (len(kk), m))
+        slots_o.append((u, bu, (mode, kk, sur)))
+        slots_g.append((u, bu, SparseGridFunction.from_nodes(len(u), m, 4, 0.0, mode, kk, sur)))
+    vec = VectorizedDdsg.compile(d, m, fa, slots_g)
+    assert vec.uses_slot_kernel()
+    check(vec, d, m, fa, slots_o, pts(d))
