@@ -92,31 +92,43 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         if (kDMax > 16) r1 = __ldg(P.rec + 2 * s + 1);
         const int q = static_cast<int>(r0.y & 0xffu);
         const uint32_t lw[6] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-        for (int j = 0; j < kDMax; ++j) {
-          if (j >= q && j < d) {
-            const int l = static_cast<int>((lw[j / 8] >> (4 * (j % 8))) & 15u);
-            double v;
-            uint32_t kk;
-            if (kTable) {
-              const int t = (j * L + l - 1) * kThreads + tid;
-              v = fv[t];
-              kk = fk[t];
-            } else {
-              kk = cell_at(xr[j], l);
-              v = basis_at(P.mode, l, kk, xr[j]);
-            }
-            if (j == 0) {
-              pw[0] = v;  // fl(1 * v_0)
-              pc[0] = kk;
-            } else {
-              pw[j] = __dmul_rn(pw[j - 1], v);
-              pc[j] = (pc[j - 1] << (l - 1)) | kk;
-            }
-          } else if (j >= d && j > 0) {
-            pw[j] = pw[j - 1];
-            pc[j] = pc[j - 1];
-          }
+        // recompute the suffix q..kDMax-1 only: jump into the unrolled dim
+        // chain at q (warp-uniform) and fall through
+        switch (q) {
+#define DDSG_DIM(J)                                                                 \
+  case J:                                                                           \
+    if (J < kDMax) {                                                                \
+      if (J < d) {                                                                  \
+        const int l = static_cast<int>((lw[(J) / 8] >> (4 * ((J) % 8))) & 15u);     \
+        double v;                                                                   \
+        uint32_t kk;                                                                \
+        if (kTable) {                                                               \
+          const int t = ((J) * L + l - 1) * kThreads + tid;                         \
+          v = fv[t];                                                                \
+          kk = fk[t];                                                               \
+        } else {                                                                    \
+          kk = cell_at(xr[(J) < kDMax ? (J) : 0], l);                               \
+          v = basis_at(P.mode, l, kk, xr[(J) < kDMax ? (J) : 0]);                   \
+        }                                                                           \
+        if ((J) == 0) {                                                             \
+          pw[0] = v; /* fl(1 * v_0) */                                              \
+          pc[0] = kk;                                                               \
+        } else {                                                                    \
+          pw[(J) < kDMax ? (J) : 0] = __dmul_rn(pw[(J) > 0 && (J) <= kDMax ? (J) - 1 : 0], v); \
+          pc[(J) < kDMax ? (J) : 0] = (pc[(J) > 0 && (J) <= kDMax ? (J) - 1 : 0] << (l - 1)) | kk; \
+        }                                                                           \
+      } else if ((J) > 0) {                                                         \
+        pw[(J) < kDMax ? (J) : 0] = pw[(J) > 0 && (J) <= kDMax ? (J) - 1 : 0];      \
+        pc[(J) < kDMax ? (J) : 0] = pc[(J) > 0 && (J) <= kDMax ? (J) - 1 : 0];      \
+      }                                                                             \
+    }                                                                               \
+    [[fallthrough]];
+          DDSG_DIM(0) DDSG_DIM(1) DDSG_DIM(2) DDSG_DIM(3) DDSG_DIM(4) DDSG_DIM(5) DDSG_DIM(6) DDSG_DIM(7)
+          DDSG_DIM(8) DDSG_DIM(9) DDSG_DIM(10) DDSG_DIM(11) DDSG_DIM(12) DDSG_DIM(13) DDSG_DIM(14)
+          DDSG_DIM(15) DDSG_DIM(16) DDSG_DIM(17) DDSG_DIM(18) DDSG_DIM(19)
+#undef DDSG_DIM
+          default:
+            break;
         }
         const double w = pw[kDMax - 1];
         if (w == 0.0) continue;  // support test (sparse_grid.hpp:123)
