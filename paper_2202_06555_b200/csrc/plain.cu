@@ -6,14 +6,18 @@
 // w = ((1 * v_0) * v_1) * ... (sparse_grid.hpp:116-122): its partial products
 // are exactly prefix products, so for consecutive subspaces l, l' whose level
 // vectors first differ at dim q only the suffix q..d-1 is recomputed (3.7
-// factors per subspace on average for config 2, 6.0 for config 3).  The 1-d
-// factors v(x_j, l) are recomputed from the coordinates held in registers
-// (measured 2x faster than a per-thread shared-memory factor table, whose
-// footprint capped occupancy at 12 warps/SM on this latency-bound gather;
-// the table variant is kept behind kTable).  Surplus rows are gathered
-// through L1 (97% hit rate on config 2).  Rounding is bit-identical to the
-// reference (EXACT: separate mul and add per term; a zero prefix stays zero,
-// which is the reference's early exit).
+// factors per subspace on average for config 2, 6.0 for config 3), entered
+// by a warp-uniform jump at q.  The 1-d factors are recomputed in registers:
+// the candidate cell from a 31-bit fixed-point copy of x (one shift), the
+// value as v = fl(A - |fl(x 2^l - B)|) (basis.cuh's exact restatement, the
+// boundary mode a template parameter).  The next term's cell, weight and row
+// are computed while the current term's surplus row is in flight (address
+// software pipelining); surplus rows are gathered through L1 (95-98 % hits
+// on config 2) with 16-byte loads.  Terms the reference skips (w == 0, an
+// absent node, a node of another stored-order run) read an all-zero row
+// instead: the accumulator is never -0, so adding w * 0 leaves its bits
+// unchanged, and non-finite surpluses are never multiplied by 0.  Rounding is
+// bit-identical to the reference (EXACT: separate mul and add per term).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,48 +34,60 @@ namespace plain {
 //   w[1] = q (first dim to recompute) | full << 8
 //   w[2..7] = levels as 4-bit nibbles, dim j in word 2 + j/8, bits 4*(j%8)
 struct Params {
-  int d, m, n_sub, runs, lmax, mode;
+  int d, m, n_sub, runs;
   const uint4* rec;        // [n_sub][2]
   const int32_t* slab;     // partial subspaces: cell -> row or -1
   const int16_t* row_run;  // [rows]
-  const double* surplus;   // [rows][ms] (ms = m rounded up to even: 16-byte rows)
+  const double* surplus;   // [rows + 1][ms] (ms = m rounded up to even: 16-byte rows); row `zero_row` = 0
   int ms;
+  int zero_row;
 };
 
-// kTable: 1 = 1-d factors from a per-thread shared-memory table, 0 =
-// recomputed from the coordinates held in registers (no shared memory, so
-// more warps per SM hide the gather latency).
-template <int kDMax, int kMC, int kExact, int kTable>
+// Exact 1-d factor of the candidate cell at (runtime) level l:
+// xi = floor(x 2^31), so floor(x 2^(l-1)) = xi >> (32 - l); clamped at x = 1.
+template <int kMode>
+__device__ __forceinline__ void factor(double x, uint32_t xi, int l, uint32_t& kk, double& v) {
+  const uint32_t ncell = 1u << (l - 1);
+  kk = min(xi >> (32 - l), ncell - 1u);
+  if (kMode == 1 && l == 1) {
+    v = 1.0;
+    return;
+  }
+  const double t = __dmul_rn(x, __hiloint2double((1023 + l) << 20, 0));  // x 2^l, exact
+  uint32_t B = 2u * kk + 1u;
+  double A = 1.0;
+  if (kMode == 1) {
+    const bool left = kk == 0u, right = kk == ncell - 1u;
+    B = left ? 0u : (right ? 2u * ncell : B);
+    A = (left || right) ? 2.0 : 1.0;
+  }
+  v = __dadd_rn(A, -fabs(__dadd_rn(t, -static_cast<double>(B))));  // >= 0 at the candidate cell
+}
+
+template <int kDMax, int kMC, int kExact, int kMode>
 __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
                                                          int64_t base, double* __restrict__ y,
                                                          unsigned long long* bad) {
-  extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x;
   const int64_t p = static_cast<int64_t>(blockIdx.x) * kThreads + tid;
   const bool valid = p < n;
-  const int d = P.d, L = P.lmax;
-  double* fv = reinterpret_cast<double*>(smem);                              // [d*L][kThreads]
-  uint16_t* fk = reinterpret_cast<uint16_t*>(fv + static_cast<int64_t>(d) * L * kThreads);  // [d*L][kThreads]
+  const int d = P.d;
   double xr[kDMax];
+  uint32_t xi[kDMax];
   bool ok = valid;
 #pragma unroll
   for (int j = 0; j < kDMax; ++j) {
     xr[j] = 0.5;
+    xi[j] = 0u;
     if (j < d) {
       const double xv = valid ? x[p * d + j] : 0.5;
-      xr[j] = xv;
       ok &= (xv >= 0.0 && xv <= 1.0);
-      if (kTable) {
-        for (int l = 1; l <= L; ++l) {
-          const uint32_t kk = cell_at(xv, l);
-          fv[(j * L + l - 1) * kThreads + tid] = basis_at(P.mode, l, kk, xv);
-          fk[(j * L + l - 1) * kThreads + tid] = static_cast<uint16_t>(kk);
-        }
-      }
+      xr[j] = xv;
+      xi[j] = ok ? static_cast<uint32_t>(__dmul_rn(xv, 2147483648.0)) : 0u;
     }
   }
   if (valid && !ok) atomicMin(bad, static_cast<unsigned long long>(base + p));
-  if (!valid || !ok) return;  // no block-wide barrier below: each thread owns its table column
+  if (!valid || !ok) return;
 
   for (int c0 = 0; c0 < P.m; c0 += kMC) {
     const int nc = min(kMC, P.m - c0);
@@ -86,42 +102,36 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         pw[j] = 0.0;
         pc[j] = 0u;
       }
-      for (int s = 0; s < P.n_sub; ++s) {
+      // weight and surplus row of subspace s (the zero row for skipped terms)
+      auto term = [&](int s, double& w, int& row) {
         const uint4 r0 = __ldg(P.rec + 2 * s);
         uint4 r1 = make_uint4(0u, 0u, 0u, 0u);
         if (kDMax > 16) r1 = __ldg(P.rec + 2 * s + 1);
-        const int q = static_cast<int>(r0.y & 0xffu);
         const uint32_t lw[6] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-        // recompute the suffix q..kDMax-1 only: jump into the unrolled dim
-        // chain at q (warp-uniform) and fall through
-        switch (q) {
-#define DDSG_DIM(J)                                                                 \
-  case J:                                                                           \
-    if (J < kDMax) {                                                                \
-      if (J < d) {                                                                  \
-        const int l = static_cast<int>((lw[(J) / 8] >> (4 * ((J) % 8))) & 15u);     \
-        double v;                                                                   \
-        uint32_t kk;                                                                \
-        if (kTable) {                                                               \
-          const int t = ((J) * L + l - 1) * kThreads + tid;                         \
-          v = fv[t];                                                                \
-          kk = fk[t];                                                               \
-        } else {                                                                    \
-          kk = cell_at(xr[(J) < kDMax ? (J) : 0], l);                               \
-          v = basis_at(P.mode, l, kk, xr[(J) < kDMax ? (J) : 0]);                   \
-        }                                                                           \
-        if ((J) == 0) {                                                             \
-          pw[0] = v; /* fl(1 * v_0) */                                              \
-          pc[0] = kk;                                                               \
-        } else {                                                                    \
-          pw[(J) < kDMax ? (J) : 0] = __dmul_rn(pw[(J) > 0 && (J) <= kDMax ? (J) - 1 : 0], v); \
-          pc[(J) < kDMax ? (J) : 0] = (pc[(J) > 0 && (J) <= kDMax ? (J) - 1 : 0] << (l - 1)) | kk; \
-        }                                                                           \
-      } else if ((J) > 0) {                                                         \
-        pw[(J) < kDMax ? (J) : 0] = pw[(J) > 0 && (J) <= kDMax ? (J) - 1 : 0];      \
-        pc[(J) < kDMax ? (J) : 0] = pc[(J) > 0 && (J) <= kDMax ? (J) - 1 : 0];      \
-      }                                                                             \
-    }                                                                               \
+        // recompute the suffix q..d-1: jump in at q (warp-uniform), fall through
+        switch (static_cast<int>(r0.y & 0xffu)) {
+#define DDSG_DIM(J)                                                                            \
+  case J:                                                                                      \
+    if ((J) < kDMax) {                                                                         \
+      constexpr int jj = (J) < kDMax ? (J) : 0;                                                \
+      constexpr int jp = (J) > 0 && (J) <= kDMax ? (J) - 1 : 0;                                \
+      if (jj < d) {                                                                            \
+        const int l = static_cast<int>((lw[jj / 8] >> (4 * (jj % 8))) & 15u);                 \
+        uint32_t kk;                                                                           \
+        double v;                                                                              \
+        factor<kMode>(xr[jj], xi[jj], l, kk, v);                                               \
+        if ((J) == 0) {                                                                        \
+          pw[0] = v; /* fl(1 * v_0) */                                                         \
+          pc[0] = kk;                                                                          \
+        } else {                                                                               \
+          pw[jj] = __dmul_rn(pw[jp], v);                                                       \
+          pc[jj] = (pc[jp] << (l - 1)) | kk;                                                   \
+        }                                                                                      \
+      } else if ((J) > 0) {                                                                    \
+        pw[jj] = pw[jp];                                                                       \
+        pc[jj] = pc[jp];                                                                       \
+      }                                                                                        \
+    }                                                                                          \
     [[fallthrough]];
           DDSG_DIM(0) DDSG_DIM(1) DDSG_DIM(2) DDSG_DIM(3) DDSG_DIM(4) DDSG_DIM(5) DDSG_DIM(6) DDSG_DIM(7)
           DDSG_DIM(8) DDSG_DIM(9) DDSG_DIM(10) DDSG_DIM(11) DDSG_DIM(12) DDSG_DIM(13) DDSG_DIM(14)
@@ -130,31 +140,43 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
           default:
             break;
         }
-        const double w = pw[kDMax - 1];
-        if (w == 0.0) continue;  // support test (sparse_grid.hpp:123)
-        int row = static_cast<int>(r0.x);
-        if ((r0.y >> 8) & 1u)
-          row += static_cast<int>(pc[kDMax - 1]);
-        else
-          row = P.slab[row + static_cast<int>(pc[kDMax - 1])];
-        if (row < 0) continue;
-        if (P.runs > 1 && P.row_run[row] != run) continue;
-        const double* sr = P.surplus + static_cast<int64_t>(row) * P.ms + c0;
+        w = pw[kDMax - 1];
+        const int cell = static_cast<int>(pc[kDMax - 1]);
+        int r = static_cast<int>(r0.x) + cell;
+        if (!((r0.y >> 8) & 1u)) r = __ldg(P.slab + r);
+        bool use = w != 0.0 && r >= 0;  // sparse_grid.hpp:123 (w == 0 skipped), absent node
+        if (use && P.runs > 1) use = __ldg(P.row_run + r) == run;
+        row = use ? r : P.zero_row;
+      };
+      double w_cur;
+      int row_cur;
+      term(0, w_cur, row_cur);
+      for (int s = 0; s < P.n_sub; ++s) {
+        // issue this term's row loads, compute the next term while they fly
+        double sv[kMC];
+        const double* sr = P.surplus + static_cast<int64_t>(row_cur) * P.ms + c0;
         if (kMC == 1) {
-          const double sv = __ldg(sr);
-          acc[0] = kExact ? __dadd_rn(acc[0], __dmul_rn(w, sv)) : __fma_rn(w, sv, acc[0]);
+          sv[0] = __ldg(sr);
         } else {
-          // 16-byte loads: one L1 sector request per lane per two columns
 #pragma unroll
           for (int c = 0; c < kMC; c += 2) {
+            sv[c] = 0.0;
+            if (kMC > 1) sv[c + 1] = 0.0;
             if (c < nc) {
-              const double2 sv = __ldg(reinterpret_cast<const double2*>(sr + c));
-              acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w, sv.x)) : __fma_rn(w, sv.x, acc[c]);
-              if (kMC > 1)
-                acc[c + 1] = kExact ? __dadd_rn(acc[c + 1], __dmul_rn(w, sv.y)) : __fma_rn(w, sv.y, acc[c + 1]);
+              const double2 v2 = __ldg(reinterpret_cast<const double2*>(sr + c));
+              sv[c] = v2.x;
+              if (kMC > 1) sv[c + 1] = v2.y;
             }
           }
         }
+        double w_nxt = 0.0;
+        int row_nxt = P.zero_row;
+        if (s + 1 < P.n_sub) term(s + 1, w_nxt, row_nxt);
+#pragma unroll
+        for (int c = 0; c < kMC; ++c)
+          if (c < nc) acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[c]);
+        w_cur = w_nxt;
+        row_cur = row_nxt;
       }
     }
     double* yp = y + p * P.m + c0;
@@ -189,12 +211,10 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   if (d > kMaxDim) return false;
   const int s0 = hp.slot_sub_begin[0], s1 = hp.slot_sub_end[0];
   const int n_sub = s1 - s0;
+  if (n_sub == 0) return false;
   int lmax = 1;
   for (int s = s0; s < s1; ++s)
     for (int j = 0; j < d; ++j) lmax = std::max<int>(lmax, hp.levels[hp.sub_lv_off[s] + j]);
-  if (lmax > 16) return false;
-  const size_t smem = static_cast<size_t>(d) * lmax * kThreads * (sizeof(double) + sizeof(uint16_t));
-  if (smem > 200 * 1024) return false;
   if (lmax > 15) return false;  // 4-bit level nibbles
   std::vector<uint32_t> rec(static_cast<size_t>(n_sub) * 8, 0u);
   for (int s = 0; s < n_sub; ++s) {
@@ -216,63 +236,60 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   d_ = d;
   m_ = hp.m;
   n_sub_ = n_sub;
-  lmax_ = lmax;
   mode_ = hp.slot_mode[0];
   runs_ = hp.slot_runs[0];
-  smem_ = smem;
   rec_ = reinterpret_cast<const uint4*>(put(rec));
   // row-padded copy of the surpluses (even stride -> 16-byte aligned rows)
+  // plus one all-zero row for skipped terms
   ms_ = hp.m == 1 ? 1 : (hp.m + 1) / 2 * 2;
-  if (ms_ != hp.m) {
-    std::vector<double> pad(static_cast<size_t>(hp.rows) * ms_, 0.0);
-    for (int64_t r = 0; r < hp.rows; ++r)
-      std::copy(hp.surplus.begin() + r * hp.m, hp.surplus.begin() + (r + 1) * hp.m, pad.begin() + r * ms_);
-    surplus_ = put(pad);
-  } else {
-    surplus_ = dev.surplus;
-  }
+  zero_row_ = static_cast<int>(hp.rows);
+  std::vector<double> pad(static_cast<size_t>(hp.rows + 1) * ms_, 0.0);
+  for (int64_t r = 0; r < hp.rows; ++r)
+    std::copy(hp.surplus.begin() + r * hp.m, hp.surplus.begin() + (r + 1) * hp.m, pad.begin() + r * ms_);
+  surplus_ = put(pad);
   slab_ = dev.slab;
   row_run_ = dev.row_run;
   usable_ = true;
   return true;
 }
 
-template <int kDMax, int kMC>
+template <int kDMax, int kMC, int kMode>
 static void launch_plain(const Params& P, int exact, const double* x, int64_t n, int64_t base, double* y,
-                         unsigned long long* bad, cudaStream_t st, size_t smem) {
+                         unsigned long long* bad, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>((n + kThreads - 1) / kThreads);
-  // factor table only pays off when the recompute is long (many dims changed per subspace)
-  constexpr int kTab = 0;
-  smem = kTab ? smem : 0;
-  if (exact) {
-    DDSG_CUDA(cudaFuncSetAttribute(plain_kernel<kDMax, kMC, 1, kTab>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    plain_kernel<kDMax, kMC, 1, kTab><<<grid, kThreads, smem, st>>>(P, x, n, base, y, bad);
-  } else {
-    DDSG_CUDA(cudaFuncSetAttribute(plain_kernel<kDMax, kMC, 0, kTab>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    plain_kernel<kDMax, kMC, 0, kTab><<<grid, kThreads, smem, st>>>(P, x, n, base, y, bad);
-  }
+  if (exact)
+    plain_kernel<kDMax, kMC, 1, kMode><<<grid, kThreads, 0, st>>>(P, x, n, base, y, bad);
+  else
+    plain_kernel<kDMax, kMC, 0, kMode><<<grid, kThreads, 0, st>>>(P, x, n, base, y, bad);
+}
+
+template <int kDMax, int kMC>
+static void launch_mode(int mode, const Params& P, int exact, const double* x, int64_t n, int64_t base, double* y,
+                        unsigned long long* bad, cudaStream_t st) {
+  if (mode == 1)
+    launch_plain<kDMax, kMC, 1>(P, exact, x, n, base, y, bad, st);
+  else
+    launch_plain<kDMax, kMC, 0>(P, exact, x, n, base, y, bad, st);
 }
 
 int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, double* y,
                           unsigned long long* bad, cudaStream_t st) const {
-  Params P{d_, m_, n_sub_, runs_, lmax_, mode_, rec_, slab_, row_run_, surplus_, ms_};
+  Params P{d_, m_, n_sub_, runs_, rec_, slab_, row_run_, surplus_, ms_, zero_row_};
   kernel_timer().begin(st);
   // column chunk: all outputs per thread when m is small
-  const int mc = m_ <= 1 ? 1 : (m_ <= 12 ? 12 : 24);
   if (d_ <= 4) {
-    if (mc == 1) launch_plain<4, 1>(P, exact, x, n, base, y, bad, st, smem_);
-    else if (mc == 12) launch_plain<4, 12>(P, exact, x, n, base, y, bad, st, smem_);
-    else launch_plain<4, 24>(P, exact, x, n, base, y, bad, st, smem_);
+    if (m_ <= 1) launch_mode<4, 1>(mode_, P, exact, x, n, base, y, bad, st);
+    else if (m_ <= 12) launch_mode<4, 12>(mode_, P, exact, x, n, base, y, bad, st);
+    else launch_mode<4, 24>(mode_, P, exact, x, n, base, y, bad, st);
   } else if (d_ <= 10) {
-    if (mc == 1) launch_plain<10, 1>(P, exact, x, n, base, y, bad, st, smem_);
-    else if (mc == 12) launch_plain<10, 12>(P, exact, x, n, base, y, bad, st, smem_);
-    else launch_plain<10, 24>(P, exact, x, n, base, y, bad, st, smem_);
+    if (m_ <= 1) launch_mode<10, 1>(mode_, P, exact, x, n, base, y, bad, st);
+    else launch_mode<10, 12>(mode_, P, exact, x, n, base, y, bad, st);
   } else {
-    if (mc == 1) launch_plain<20, 1>(P, exact, x, n, base, y, bad, st, smem_);
-    else if (mc == 12) launch_plain<20, 12>(P, exact, x, n, base, y, bad, st, smem_);
-    else launch_plain<20, 24>(P, exact, x, n, base, y, bad, st, smem_);
+    // one chunk of 24 columns (config 3: m = 21) measured fastest despite
+    // 234 registers: every further chunk repeats the whole subspace walk
+    // (kMC 8 / 12 / 24: 0.19 / 0.25 / 0.44 TFLOP/s)
+    if (m_ <= 1) launch_mode<20, 1>(mode_, P, exact, x, n, base, y, bad, st);
+    else launch_mode<20, 24>(mode_, P, exact, x, n, base, y, bad, st);
   }
   kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());

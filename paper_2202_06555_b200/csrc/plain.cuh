@@ -23,8 +23,8 @@ class PlainGrid {
   ~PlainGrid();
 
   // Builds the subspace walk tables when the program is a plain grid with
-  // d <= 20 and levels <= 16; `dev` supplies the already uploaded slab,
-  // run and surplus arrays.
+  // d <= 20 and levels <= 15; `dev` supplies the already uploaded slab and
+  // run arrays (the surpluses are re-laid out with a zero row).
   bool build(const HostProgram& hp, const EvalParams& dev);
   bool usable() const { return usable_; }
   int64_t launch(int exact, const double* x, int64_t n, int64_t base, double* y, unsigned long long* bad,
@@ -32,8 +32,7 @@ class PlainGrid {
 
  private:
   bool usable_ = false;
-  int d_ = 0, m_ = 0, ms_ = 0, n_sub_ = 0, lmax_ = 0, mode_ = 0, runs_ = 1;
-  size_t smem_ = 0;
+  int d_ = 0, m_ = 0, ms_ = 0, n_sub_ = 0, mode_ = 0, runs_ = 1, zero_row_ = 0;
   const uint4* rec_ = nullptr;  // [n_sub][2] packed subspace records
   const int32_t* slab_ = nullptr;
   const int16_t* row_run_ = nullptr;
