@@ -64,7 +64,7 @@ __device__ __forceinline__ void factor(double x, uint32_t xi, int l, uint32_t& k
   v = __dadd_rn(A, -fabs(__dadd_rn(t, -static_cast<double>(B))));  // >= 0 at the candidate cell
 }
 
-template <int kDMax, int kMC, int kExact, int kMode>
+template <int kDMax, int kMC, int kExact, int kMode, int kMultiRun>
 __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
                                                          int64_t base, double* __restrict__ y,
                                                          unsigned long long* bad) {
@@ -72,13 +72,15 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
   const int64_t p = static_cast<int64_t>(blockIdx.x) * kThreads + tid;
   const bool valid = p < n;
   const int d = P.d;
+  // dims d..kDMax-1 are padding: x = 1/2 at level 1 gives the factor 1 and
+  // cell 0 in both modes, so the prefix product and cell index pass through
   double xr[kDMax];
   uint32_t xi[kDMax];
   bool ok = valid;
 #pragma unroll
   for (int j = 0; j < kDMax; ++j) {
     xr[j] = 0.5;
-    xi[j] = 0u;
+    xi[j] = 0x40000000u;
     if (j < d) {
       const double xv = valid ? x[p * d + j] : 0.5;
       ok &= (xv >= 0.0 && xv <= 1.0);
@@ -90,11 +92,10 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
   if (!valid || !ok) return;
 
   for (int c0 = 0; c0 < P.m; c0 += kMC) {
-    const int nc = min(kMC, P.m - c0);
     double acc[kMC];
 #pragma unroll
     for (int c = 0; c < kMC; ++c) acc[c] = 0.0;
-    for (int run = 0; run < P.runs; ++run) {
+    for (int run = 0; run < (kMultiRun ? P.runs : 1); ++run) {
       double pw[kDMax];
       uint32_t pc[kDMax];
 #pragma unroll
@@ -102,34 +103,27 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         pw[j] = 0.0;
         pc[j] = 0u;
       }
-      // weight and surplus row of subspace s (the zero row for skipped terms)
-      auto term = [&](int s, double& w, int& row) {
-        const uint4 r0 = __ldg(P.rec + 2 * s);
-        uint4 r1 = make_uint4(0u, 0u, 0u, 0u);
-        if (kDMax > 16) r1 = __ldg(P.rec + 2 * s + 1);
+      // weight and surplus row of the subspace with record (r0, r1); the
+      // zero row for skipped terms
+      auto term = [&](const uint4& r0, const uint4& r1, double& w, int& row) {
         const uint32_t lw[6] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-        // recompute the suffix q..d-1: jump in at q (warp-uniform), fall through
+        // recompute the suffix q..kDMax-1: jump in at q (warp-uniform), fall through
         switch (static_cast<int>(r0.y & 0xffu)) {
 #define DDSG_DIM(J)                                                                            \
   case J:                                                                                      \
     if ((J) < kDMax) {                                                                         \
       constexpr int jj = (J) < kDMax ? (J) : 0;                                                \
       constexpr int jp = (J) > 0 && (J) <= kDMax ? (J) - 1 : 0;                                \
-      if (jj < d) {                                                                            \
-        const int l = static_cast<int>((lw[jj / 8] >> (4 * (jj % 8))) & 15u);                 \
-        uint32_t kk;                                                                           \
-        double v;                                                                              \
-        factor<kMode>(xr[jj], xi[jj], l, kk, v);                                               \
-        if ((J) == 0) {                                                                        \
-          pw[0] = v; /* fl(1 * v_0) */                                                         \
-          pc[0] = kk;                                                                          \
-        } else {                                                                               \
-          pw[jj] = __dmul_rn(pw[jp], v);                                                       \
-          pc[jj] = (pc[jp] << (l - 1)) | kk;                                                   \
-        }                                                                                      \
-      } else if ((J) > 0) {                                                                    \
-        pw[jj] = pw[jp];                                                                       \
-        pc[jj] = pc[jp];                                                                       \
+      const int l = static_cast<int>((lw[jj / 8] >> (4 * (jj % 8))) & 15u);                   \
+      uint32_t kk;                                                                             \
+      double v;                                                                                \
+      factor<kMode>(xr[jj], xi[jj], l, kk, v);                                                 \
+      if ((J) == 0) {                                                                          \
+        pw[0] = v; /* fl(1 * v_0) */                                                           \
+        pc[0] = kk;                                                                            \
+      } else {                                                                                 \
+        pw[jj] = __dmul_rn(pw[jp], v);                                                         \
+        pc[jj] = (pc[jp] << (l - 1)) | kk;                                                     \
       }                                                                                        \
     }                                                                                          \
     [[fallthrough]];
@@ -141,16 +135,22 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
             break;
         }
         w = pw[kDMax - 1];
-        const int cell = static_cast<int>(pc[kDMax - 1]);
-        int r = static_cast<int>(r0.x) + cell;
+        int r = static_cast<int>(r0.x) + static_cast<int>(pc[kDMax - 1]);
         if (!((r0.y >> 8) & 1u)) r = __ldg(P.slab + r);
         bool use = w != 0.0 && r >= 0;  // sparse_grid.hpp:123 (w == 0 skipped), absent node
-        if (use && P.runs > 1) use = __ldg(P.row_run + r) == run;
+        if (kMultiRun) use = use && __ldg(P.row_run + r) == run;
         row = use ? r : P.zero_row;
       };
+      const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+      // subspace records are prefetched one iteration ahead of their use
+      uint4 ra = __ldg(P.rec), rb = kDMax > 16 ? __ldg(P.rec + 1) : zero4;
       double w_cur;
       int row_cur;
-      term(0, w_cur, row_cur);
+      term(ra, rb, w_cur, row_cur);
+      if (P.n_sub > 1) {
+        ra = __ldg(P.rec + 2);
+        rb = kDMax > 16 ? __ldg(P.rec + 3) : zero4;
+      }
       for (int s = 0; s < P.n_sub; ++s) {
         // issue this term's row loads, compute the next term while they fly
         double sv[kMC];
@@ -159,26 +159,28 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
           sv[0] = __ldg(sr);
         } else {
 #pragma unroll
-          for (int c = 0; c < kMC; c += 2) {
-            sv[c] = 0.0;
-            if (kMC > 1) sv[c + 1] = 0.0;
-            if (c < nc) {
-              const double2 v2 = __ldg(reinterpret_cast<const double2*>(sr + c));
-              sv[c] = v2.x;
-              if (kMC > 1) sv[c + 1] = v2.y;
-            }
+          for (int c = 0; c < kMC; c += 2) {  // rows are padded to whole chunks
+            const double2 v2 = __ldg(reinterpret_cast<const double2*>(sr + c));
+            sv[c] = v2.x;
+            sv[c + 1] = v2.y;
           }
+        }
+        const uint4 ua = ra, ub = rb;
+        if (s + 2 < P.n_sub) {
+          ra = __ldg(P.rec + 2 * (s + 2));
+          if (kDMax > 16) rb = __ldg(P.rec + 2 * (s + 2) + 1);
         }
         double w_nxt = 0.0;
         int row_nxt = P.zero_row;
-        if (s + 1 < P.n_sub) term(s + 1, w_nxt, row_nxt);
+        if (s + 1 < P.n_sub) term(ua, ub, w_nxt, row_nxt);
 #pragma unroll
         for (int c = 0; c < kMC; ++c)
-          if (c < nc) acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[c]);
+          acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[c]);
         w_cur = w_nxt;
         row_cur = row_nxt;
       }
     }
+    const int nc = min(kMC, P.m - c0);
     double* yp = y + p * P.m + c0;
 #pragma unroll
     for (int c = 0; c < kMC; ++c)
@@ -202,6 +204,16 @@ const T* PlainGrid::put(const std::vector<T>& v) {
   allocs_.push_back(p);
   DDSG_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
   return static_cast<const T*>(p);
+}
+
+// Output columns per thread (one chunk when possible: every further chunk
+// repeats the whole subspace walk; config 3 measured 0.19 / 0.25 / 0.44
+// TFLOP/s for chunks of 8 / 12 / 24).
+static int chunk_width(int d, int m) {
+  if (m <= 1) return 1;
+  if (d <= 4) return m <= 12 ? 12 : 24;
+  if (d <= 10) return 12;
+  return 24;
 }
 
 bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
@@ -231,7 +243,8 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
     uint32_t* r = &rec[static_cast<size_t>(s) * 8];
     r[0] = static_cast<uint32_t>(is_full ? hp.slab[slab_off] : slab_off);
     r[1] = static_cast<uint32_t>(qq) | (is_full ? 0x100u : 0u);
-    for (int j = 0; j < d; ++j) r[2 + j / 8] |= static_cast<uint32_t>(lv[j]) << (4 * (j % 8));
+    for (int j = 0; j < kMaxDim; ++j)  // padding dims: level 1
+      r[2 + j / 8] |= static_cast<uint32_t>(j < d ? lv[j] : 1) << (4 * (j % 8));
   }
   d_ = d;
   m_ = hp.m;
@@ -239,9 +252,11 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   mode_ = hp.slot_mode[0];
   runs_ = hp.slot_runs[0];
   rec_ = reinterpret_cast<const uint4*>(put(rec));
-  // row-padded copy of the surpluses (even stride -> 16-byte aligned rows)
-  // plus one all-zero row for skipped terms
-  ms_ = hp.m == 1 ? 1 : (hp.m + 1) / 2 * 2;
+  // row-padded copy of the surpluses (rows padded to whole column chunks, so
+  // every chunk is read with unguarded 16-byte loads) plus one all-zero row
+  // for skipped terms
+  mc_ = chunk_width(d, hp.m);
+  ms_ = (hp.m + mc_ - 1) / mc_ * mc_;
   zero_row_ = static_cast<int>(hp.rows);
   std::vector<double> pad(static_cast<size_t>(hp.rows + 1) * ms_, 0.0);
   for (int64_t r = 0; r < hp.rows; ++r)
@@ -253,43 +268,40 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   return true;
 }
 
-template <int kDMax, int kMC, int kMode>
+template <int kDMax, int kMC, int kMode, int kMulti>
 static void launch_plain(const Params& P, int exact, const double* x, int64_t n, int64_t base, double* y,
                          unsigned long long* bad, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>((n + kThreads - 1) / kThreads);
   if (exact)
-    plain_kernel<kDMax, kMC, 1, kMode><<<grid, kThreads, 0, st>>>(P, x, n, base, y, bad);
+    plain_kernel<kDMax, kMC, 1, kMode, kMulti><<<grid, kThreads, 0, st>>>(P, x, n, base, y, bad);
   else
-    plain_kernel<kDMax, kMC, 0, kMode><<<grid, kThreads, 0, st>>>(P, x, n, base, y, bad);
+    plain_kernel<kDMax, kMC, 0, kMode, kMulti><<<grid, kThreads, 0, st>>>(P, x, n, base, y, bad);
 }
 
 template <int kDMax, int kMC>
 static void launch_mode(int mode, const Params& P, int exact, const double* x, int64_t n, int64_t base, double* y,
                         unsigned long long* bad, cudaStream_t st) {
+  const bool multi = P.runs > 1;
   if (mode == 1)
-    launch_plain<kDMax, kMC, 1>(P, exact, x, n, base, y, bad, st);
+    multi ? launch_plain<kDMax, kMC, 1, 1>(P, exact, x, n, base, y, bad, st)
+          : launch_plain<kDMax, kMC, 1, 0>(P, exact, x, n, base, y, bad, st);
   else
-    launch_plain<kDMax, kMC, 0>(P, exact, x, n, base, y, bad, st);
+    multi ? launch_plain<kDMax, kMC, 0, 1>(P, exact, x, n, base, y, bad, st)
+          : launch_plain<kDMax, kMC, 0, 0>(P, exact, x, n, base, y, bad, st);
 }
 
 int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, double* y,
                           unsigned long long* bad, cudaStream_t st) const {
   Params P{d_, m_, n_sub_, runs_, rec_, slab_, row_run_, surplus_, ms_, zero_row_};
   kernel_timer().begin(st);
-  // column chunk: all outputs per thread when m is small
-  if (d_ <= 4) {
-    if (m_ <= 1) launch_mode<4, 1>(mode_, P, exact, x, n, base, y, bad, st);
-    else if (m_ <= 12) launch_mode<4, 12>(mode_, P, exact, x, n, base, y, bad, st);
-    else launch_mode<4, 24>(mode_, P, exact, x, n, base, y, bad, st);
-  } else if (d_ <= 10) {
-    if (m_ <= 1) launch_mode<10, 1>(mode_, P, exact, x, n, base, y, bad, st);
-    else launch_mode<10, 12>(mode_, P, exact, x, n, base, y, bad, st);
-  } else {
-    // one chunk of 24 columns (config 3: m = 21) measured fastest despite
-    // 234 registers: every further chunk repeats the whole subspace walk
-    // (kMC 8 / 12 / 24: 0.19 / 0.25 / 0.44 TFLOP/s)
-    if (m_ <= 1) launch_mode<20, 1>(mode_, P, exact, x, n, base, y, bad, st);
-    else launch_mode<20, 24>(mode_, P, exact, x, n, base, y, bad, st);
+  switch (d_ <= 4 ? 400 + mc_ : (d_ <= 10 ? 1000 + mc_ : 2000 + mc_)) {
+    case 401: launch_mode<4, 1>(mode_, P, exact, x, n, base, y, bad, st); break;
+    case 412: launch_mode<4, 12>(mode_, P, exact, x, n, base, y, bad, st); break;
+    case 424: launch_mode<4, 24>(mode_, P, exact, x, n, base, y, bad, st); break;
+    case 1001: launch_mode<10, 1>(mode_, P, exact, x, n, base, y, bad, st); break;
+    case 1012: launch_mode<10, 12>(mode_, P, exact, x, n, base, y, bad, st); break;
+    case 2001: launch_mode<20, 1>(mode_, P, exact, x, n, base, y, bad, st); break;
+    default: launch_mode<20, 24>(mode_, P, exact, x, n, base, y, bad, st); break;
   }
   kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());
