@@ -158,12 +158,13 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         if (kMC == 1) {
           sv[0] = __ldg(sr);
         } else {
+          // rows are padded to whole chunks and 32-byte aligned: one 256-bit
+          // load (LDG.E.256) per 4 columns, a whole L1 sector per request
 #pragma unroll
-          for (int c = 0; c < kMC; c += 2) {  // rows are padded to whole chunks
-            const double2 v2 = __ldg(reinterpret_cast<const double2*>(sr + c));
-            sv[c] = v2.x;
-            sv[c + 1] = v2.y;
-          }
+          for (int c = 0; c < kMC; c += 4)
+            asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                : "=d"(sv[c]), "=d"(sv[c + 1]), "=d"(sv[c + 2]), "=d"(sv[c + 3])
+                : "l"(sr + c));
         }
         const uint4 ua = ra, ub = rb;
         if (s + 2 < P.n_sub) {
