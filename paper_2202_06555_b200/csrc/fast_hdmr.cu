@@ -818,6 +818,29 @@ bool FastHdmr::build(const HostProgram& hp) {
                 break;
               }
           H.fast_full = (nlev > 0 && H.present == all && H.full == all && finite) ? 1 : 0;
+          // An adaptive (partial) block with finite surpluses is padded to the
+          // full grid of its level with zero rows: the general path already
+          // adds w * 0 for every absent canonical node (term_row's zero row),
+          // so the padded block adds the same terms in the same order, but
+          // through the static-row path (no slab lookups, loads one term ahead).
+          const int64_t full_rows = k == 1 ? base1(nlev + 1) : base2(1, nlev + 1);
+          if (!H.fast_full && finite && nlev > 0 && (full_rows + 1) * kStride * 8 <= kMaxPaddedBytes) {
+            std::vector<int64_t> padded(static_cast<size_t>(full_rows), -1);
+            for (int sb = hp.slot_sub_begin[a]; sb < hp.slot_sub_end[a]; ++sb) {
+              const uint8_t* lv = &hp.levels[hp.sub_lv_off[sb]];
+              const int l1 = lv[0], l2 = k == 2 ? lv[1] : 0;
+              const int64_t base = k == 1 ? base1(l1) : base2(l1, l2);
+              const int64_t cells = int64_t{1} << (l1 - 1 + (k == 2 ? l2 - 1 : 0));
+              const int32_t* slab = &hp.slab[hp.sub_slab_off[sb]];
+              for (int64_t c = 0; c < cells; ++c)
+                if (slab[c] >= 0 && local[slab[c] - row_begin] >= 0) padded[base + c] = slab[c];
+            }
+            P.rows.assign(padded.begin(), padded.end());
+            P.slab.clear();
+            H.present = all;
+            H.full = all;
+            H.fast_full = 1;
+          }
         }
         H.zero_row = static_cast<int32_t>(P.rows.size());  // all-zero row appended to the table
         P.rows.push_back(-1);

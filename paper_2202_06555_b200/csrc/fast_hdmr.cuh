@@ -46,6 +46,7 @@ constexpr int kSmemLevels = 4;           // levels 9..12 in shared memory (level
 constexpr int kMaxLevels = kTmemLevels + kSmemLevels;  // 2^12 active slots
 constexpr int kMaxStages = 4;            // shared-memory ring depth (fewer when slot blocks are large)
 constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
+constexpr int kMaxPaddedBytes = 96 * 1024;  // largest row table an adaptive block is padded to
 constexpr int kBCont = 4;   // b_kind flag: continue the previous block's accumulation (later run)
 constexpr int kBMore = 8;   // b_kind flag: another run of the same slot follows
 
