@@ -33,9 +33,12 @@ namespace plain {
 //   w[0] = first row (full subspace) or slab offset (partial)
 //   w[1] = q (first dim to recompute) | full << 8
 //   w[2..7] = levels as 4-bit nibbles, dim j in word 2 + j/8, bits 4*(j%8)
+constexpr int kMaxRuns = 15;
+
 struct Params {
-  int d, m, n_sub, runs;
-  const uint4* rec;        // [n_sub][2]
+  int d, m, runs;
+  int run_off[kMaxRuns + 1];  // run r walks records [run_off[r], run_off[r+1])
+  const uint4* rec;        // [records][2]: per run, the subspaces holding nodes of that run
   const int32_t* slab;     // partial subspaces: cell -> row or -1
   const int16_t* row_run;  // [rows]
   const double* surplus;   // [rows + 1][ms] (ms = m rounded up to even: 16-byte rows); row `zero_row` = 0
@@ -142,16 +145,19 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         row = use ? r : P.zero_row;
       };
       const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+      const uint4* rec = P.rec + 2 * P.run_off[run];
+      const int n_sub = P.run_off[run + 1] - P.run_off[run];
+      if (n_sub == 0) continue;
       // subspace records are prefetched one iteration ahead of their use
-      uint4 ra = __ldg(P.rec), rb = kDMax > 16 ? __ldg(P.rec + 1) : zero4;
+      uint4 ra = __ldg(rec), rb = kDMax > 16 ? __ldg(rec + 1) : zero4;
       double w_cur;
       int row_cur;
       term(ra, rb, w_cur, row_cur);
-      if (P.n_sub > 1) {
-        ra = __ldg(P.rec + 2);
-        rb = kDMax > 16 ? __ldg(P.rec + 3) : zero4;
+      if (n_sub > 1) {
+        ra = __ldg(rec + 2);
+        rb = kDMax > 16 ? __ldg(rec + 3) : zero4;
       }
-      for (int s = 0; s < P.n_sub; ++s) {
+      for (int s = 0; s < n_sub; ++s) {
         // issue this term's row loads, compute the next term while they fly
         double sv[kMC];
         const double* sr = P.surplus + static_cast<int64_t>(row_cur) * P.ms + c0;
@@ -167,13 +173,13 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
                 : "l"(sr + c));
         }
         const uint4 ua = ra, ub = rb;
-        if (s + 2 < P.n_sub) {
-          ra = __ldg(P.rec + 2 * (s + 2));
-          if (kDMax > 16) rb = __ldg(P.rec + 2 * (s + 2) + 1);
+        if (s + 2 < n_sub) {
+          ra = __ldg(rec + 2 * (s + 2));
+          if (kDMax > 16) rb = __ldg(rec + 2 * (s + 2) + 1);
         }
         double w_nxt = 0.0;
         int row_nxt = P.zero_row;
-        if (s + 1 < P.n_sub) term(ua, ub, w_nxt, row_nxt);
+        if (s + 1 < n_sub) term(ua, ub, w_nxt, row_nxt);
 #pragma unroll
         for (int c = 0; c < kMC; ++c)
           acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[c]);
@@ -229,29 +235,46 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   for (int s = s0; s < s1; ++s)
     for (int j = 0; j < d; ++j) lmax = std::max<int>(lmax, hp.levels[hp.sub_lv_off[s] + j]);
   if (lmax > 15) return false;  // 4-bit level nibbles
-  std::vector<uint32_t> rec(static_cast<size_t>(n_sub) * 8, 0u);
-  for (int s = 0; s < n_sub; ++s) {
-    const uint8_t* lv = &hp.levels[hp.sub_lv_off[s0 + s]];
-    int qq = 0;
-    if (s > 0) {
-      const uint8_t* prev = &hp.levels[hp.sub_lv_off[s0 + s - 1]];
-      while (qq < d && prev[qq] == lv[qq]) ++qq;
+  // Per stored-order run, the subspaces that hold at least one node of the
+  // run, in canonical order (a run's walk skips the others: config 3's two
+  // runs touch 1,771 and 9,995 of its 10,626 subspaces).
+  const int runs = hp.slot_runs[0];
+  if (runs > kMaxRuns) return false;
+  std::vector<uint32_t> rec;
+  run_off_.assign(1, 0);
+  for (int run = 0; run < runs; ++run) {
+    const uint8_t* prev = nullptr;
+    for (int s = s0; s < s1; ++s) {
+      const uint8_t* lv = &hp.levels[hp.sub_lv_off[s]];
+      int64_t cells = 1;
+      for (int j = 0; j < d; ++j) cells <<= (lv[j] - 1);
+      const int64_t slab_off = hp.sub_slab_off[s];
+      if (runs > 1) {
+        bool has = false;
+        for (int64_t c = 0; c < cells && !has; ++c) {
+          const int32_t row = hp.slab[slab_off + c];
+          has = row >= 0 && hp.row_run[row] == run;
+        }
+        if (!has) continue;
+      }
+      int qq = 0;
+      if (prev)
+        while (qq < d && prev[qq] == lv[qq]) ++qq;
+      prev = lv;
+      const bool is_full = hp.sub_nodes[s] == cells;
+      uint32_t r[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      r[0] = static_cast<uint32_t>(is_full ? hp.slab[slab_off] : slab_off);
+      r[1] = static_cast<uint32_t>(qq) | (is_full ? 0x100u : 0u);
+      for (int j = 0; j < kMaxDim; ++j)  // padding dims: level 1
+        r[2 + j / 8] |= static_cast<uint32_t>(j < d ? lv[j] : 1) << (4 * (j % 8));
+      rec.insert(rec.end(), r, r + 8);
     }
-    int64_t cells = 1;
-    for (int j = 0; j < d; ++j) cells <<= (lv[j] - 1);
-    const int64_t slab_off = hp.sub_slab_off[s0 + s];
-    const bool is_full = hp.sub_nodes[s0 + s] == cells;
-    uint32_t* r = &rec[static_cast<size_t>(s) * 8];
-    r[0] = static_cast<uint32_t>(is_full ? hp.slab[slab_off] : slab_off);
-    r[1] = static_cast<uint32_t>(qq) | (is_full ? 0x100u : 0u);
-    for (int j = 0; j < kMaxDim; ++j)  // padding dims: level 1
-      r[2 + j / 8] |= static_cast<uint32_t>(j < d ? lv[j] : 1) << (4 * (j % 8));
+    run_off_.push_back(static_cast<int>(rec.size() / 8));
   }
   d_ = d;
   m_ = hp.m;
-  n_sub_ = n_sub;
   mode_ = hp.slot_mode[0];
-  runs_ = hp.slot_runs[0];
+  runs_ = runs;
   rec_ = reinterpret_cast<const uint4*>(put(rec));
   // row-padded copy of the surpluses (rows padded to whole column chunks, so
   // every chunk is read with unguarded 16-byte loads) plus one all-zero row
@@ -293,7 +316,17 @@ static void launch_mode(int mode, const Params& P, int exact, const double* x, i
 
 int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, double* y,
                           unsigned long long* bad, cudaStream_t st) const {
-  Params P{d_, m_, n_sub_, runs_, rec_, slab_, row_run_, surplus_, ms_, zero_row_};
+  Params P{};
+  P.d = d_;
+  P.m = m_;
+  P.runs = runs_;
+  for (int r = 0; r <= runs_; ++r) P.run_off[r] = run_off_[r];
+  P.rec = rec_;
+  P.slab = slab_;
+  P.row_run = row_run_;
+  P.surplus = surplus_;
+  P.ms = ms_;
+  P.zero_row = zero_row_;
   kernel_timer().begin(st);
   switch (d_ <= 4 ? 400 + mc_ : (d_ <= 10 ? 1000 + mc_ : 2000 + mc_)) {
     case 401: launch_mode<4, 1>(mode_, P, exact, x, n, base, y, bad, st); break;

@@ -32,7 +32,8 @@ class PlainGrid {
 
  private:
   bool usable_ = false;
-  int d_ = 0, m_ = 0, ms_ = 0, mc_ = 1, n_sub_ = 0, mode_ = 0, runs_ = 1, zero_row_ = 0;
+  int d_ = 0, m_ = 0, ms_ = 0, mc_ = 1, mode_ = 0, runs_ = 1, zero_row_ = 0;
+  std::vector<int> run_off_;
   const uint4* rec_ = nullptr;  // [n_sub][2] packed subspace records
   const int32_t* slab_ = nullptr;
   const int16_t* row_run_ = nullptr;
