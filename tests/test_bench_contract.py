@@ -1,0 +1,71 @@
+"""bench.py's JSON contract, checked on the CPU through the reference arm
+(which runs the reference's own evaluator from oracle/_ref, no GPU), and the
+graft entry points' surface."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+import oracle_lib as O
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def run_bench(*args, env=None, timeout=600):
+    e = dict(os.environ)
+    e.update(env or {})
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True,
+                       timeout=timeout, cwd=str(ROOT), env=e)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_json_line():
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built")
+    d = run_bench("--impl", "reference", "--config", "4", "--steps", "1", "--warmup", "0")
+    assert d["impl"] == "reference"
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["value"] > 0 and d["unit"] == "evals/s" and d["higher_is_better"] is True
+    assert d["config"]["workload"] == "config4_hdmr_d100"
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_reference_arm_non_zero_rank_is_silent():
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "4"],
+                       capture_output=True, text=True, timeout=300, cwd=str(ROOT),
+                       env={**os.environ, "RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_graft_entry_surface():
+    sys.path.insert(0, str(ROOT))
+    import __graft_entry__ as g
+
+    assert callable(g.build) and callable(g.smoke)
+
+
+@pytest.mark.gpu
+def test_bench_default_line_on_gpu():
+    d = run_bench("--steps", "3", "--warmup", "3", "--points", "65536", "--no-cpu-baseline", "--no-refine",
+                  timeout=900)
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
+    assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    rf = d["roofline"]
+    assert rf["bound"] in ("fp64", "hbm", "tensor") and 0 < rf["frac"] < 1 and rf["peak"] > 0
