@@ -251,7 +251,8 @@ def run_ours(args, rank, world, local_rank, dist):
         st = refine_step(grids, [cfg.level_1d - 1] * len(grids), lambda gi, xs: cuts[gi](xs), dist=dist,
                          device=True, comm_device=f"cuda:{local_rank}")
         refine_info = {"new_nodes": st.new_nodes, "rounds": st.rounds, "allgather_bytes": st.gathered_bytes,
-                       "hierarchize_s": round(st.hierarchize_s, 3), "allgather_s": round(st.allgather_s, 4),
+                       "hierarchize_s": round(st.hierarchize_s, 3), "target_eval_s": round(st.target_s, 3),
+                       "allgather_s": round(st.allgather_s, 4),
                        "total_s": round(time.time() - t_ref, 2),
                        "collective": "all_gather_into_tensor (NCCL)" if dist is not None else "none (1 rank)"}
         obj = VectorizedDdsg.compile(parts.d, parts.m, parts.f_anchor, parts.slots)

@@ -29,7 +29,8 @@ class RefineStats:
     new_nodes: int = 0
     rounds: int = 0
     gathered_bytes: int = 0
-    hierarchize_s: float = 0.0
+    hierarchize_s: float = 0.0  # GPU (or host) hierarchization of this rank's share
+    target_s: float = 0.0       # the caller's target evaluations (host model code)
     allgather_s: float = 0.0
     per_round: List[int] = field(default_factory=list)
 
@@ -101,19 +102,21 @@ def refine_step(grids: Sequence[SparseGridFunction], level_sums: Sequence[int],
         q = (total + world - 1) // world
         lo, hi = rank * q, min(total, (rank + 1) * q)
         local = np.zeros((q, m), dtype=np.float64)
-        t0 = time.perf_counter()
         off = 0
         for gi, keys in items:
             a, b = max(lo, off), min(hi, off + len(keys))
             if a < b:
                 sub = keys[a - off:b - off]
                 xs = coords_of(sub)
+                t0 = time.perf_counter()
                 fv = np.asarray(f_eval(gi, xs), dtype=np.float64).reshape(len(sub), m)
+                stats.target_s += time.perf_counter() - t0
                 if not np.all(np.isfinite(fv)):
                     raise FloatingPointError(f"refine_step: non-finite target value on grid {gi}")
+                t0 = time.perf_counter()
                 local[a - lo:b - lo] = grids[gi].hierarchize(sub, fv, device=device)
+                stats.hierarchize_s += time.perf_counter() - t0
             off += len(keys)
-        stats.hierarchize_s += time.perf_counter() - t0
         t0 = time.perf_counter()
         if dist is not None:
             allrows = _all_gather_rows(local, q, m, dist, comm_device)[:total]
