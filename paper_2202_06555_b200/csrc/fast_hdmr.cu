@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -317,6 +318,66 @@ __device__ __forceinline__ void leaf_full1(const unsigned char* table, double x,
   }
 }
 
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// Full order-1 slot in the rotated layout (fast_full == 2): rows of 16
+// doubles holding the 8 columns twice (bank pairs 0-7 and 8-15).  Lane l
+// reads copy (l >> 3) & 1 and, at step j, column (l & 7) ^ j into slot j, so
+// the 16 lanes of a half-warp hit 16 distinct bank pairs whatever their rows:
+// the deep levels' 32-128 candidate rows cost 2 wavefronts per warp load
+// instead of 3.9-5.5 (profiles/r1_lds_rotate.json).  The slot starts from a
+// zero accumulator (rotation-free) and un-rotates it once at the end
+// (3 conditional swap stages).  q0 = shared address of row 0 | lane bits.
+template <int kExact, int kMode, int L>
+__device__ __forceinline__ void leaf_full1_rot(uint32_t q0, double x, double (&acc)[kCols]) {
+  double w[L];
+  uint32_t row[L];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    uint32_t kk;
+    switch (l) {
+#define DDSG_F(LV)                               \
+  case LV:                                       \
+    factor_full<LV, kMode>(x, kk, w[l - 1]);     \
+    break;
+      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4) DDSG_F(5) DDSG_F(6) DDSG_F(7) DDSG_F(8) DDSG_F(9) DDSG_F(10)
+#undef DDSG_F
+      default:
+        kk = 0;
+        w[l - 1] = 0.0;
+    }
+    row[l - 1] = q0 + ((static_cast<uint32_t>(base1(l)) + kk) << 7);
+  }
+  double buf[2][kCols];  // static ping-pong: term i+1 loads while term i accumulates
+#pragma unroll
+  for (int j = 0; j < kCols; ++j) buf[0][j] = lds_f64(row[0] ^ static_cast<uint32_t>(j << 3));
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    if (i + 1 < L) {
+#pragma unroll
+      for (int j = 0; j < kCols; ++j) buf[(i + 1) & 1][j] = lds_f64(row[i + 1] ^ static_cast<uint32_t>(j << 3));
+    }
+    fma_row<kExact>(acc, w[i], buf[i & 1]);
+  }
+  // slot j holds column c0 ^ j: swap back (c0 = this lane's rotation)
+  const uint32_t c0 = (q0 >> 3) & 7u;
+#pragma unroll
+  for (int b = 1; b < kCols; b <<= 1) {
+    const bool flip = (c0 & static_cast<uint32_t>(b)) != 0u;
+#pragma unroll
+    for (int c = 0; c < kCols; ++c)
+      if (!(c & b)) {
+        const double lo = acc[c], hi = acc[c | b];
+        acc[c] = flip ? hi : lo;
+        acc[c | b] = flip ? lo : hi;
+      }
+  }
+}
+
 // Full order-2 slot with max level L per dim (level sum <= L + 1), canonical
 // order; w = fl(v0 * v1) (exact 1 * v when a factor is the modified level-1 constant).
 template <int kExact, int kMode, int L>
@@ -392,8 +453,24 @@ __device__ __forceinline__ HeaderCore load_core(const unsigned char* blk) {
 
 template <int kExact>
 __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHeader& H, const unsigned char* blk,
-                                              double x0, double x1, double (&acc)[kCols]) {
+                                              double x0, double x1, double (&acc)[kCols], uint32_t lanebits) {
   const unsigned char* table = blk + Hc.table_off;
+  if (Hc.fast_full == 2) {
+    const uint32_t q0 = smem_u32(table) | lanebits;
+    switch (Hc.mode * 16 + Hc.nlev) {
+#define DDSG_R1(MD, LV) \
+  case MD * 16 + LV: \
+    leaf_full1_rot<kExact, MD, LV>(q0, x0, acc); \
+    return;
+      DDSG_R1(0, 1) DDSG_R1(0, 2) DDSG_R1(0, 3) DDSG_R1(0, 4) DDSG_R1(0, 5) DDSG_R1(0, 6) DDSG_R1(0, 7)
+      DDSG_R1(0, 8) DDSG_R1(0, 9) DDSG_R1(0, 10)
+      DDSG_R1(1, 1) DDSG_R1(1, 2) DDSG_R1(1, 3) DDSG_R1(1, 4) DDSG_R1(1, 5) DDSG_R1(1, 6) DDSG_R1(1, 7)
+      DDSG_R1(1, 8) DDSG_R1(1, 9) DDSG_R1(1, 10)
+#undef DDSG_R1
+      default:
+        return;
+    }
+  }
   if (Hc.fast_full) {
     switch (Hc.mode * 64 + Hc.k * 16 + Hc.nlev) {
 #define DDSG_P1(MD, LV) \
@@ -497,6 +574,8 @@ __global__ void __launch_bounds__(kPoints, 1)
   const int cb = grp * cb_group + static_cast<int>(rem - tile * gsize);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  // rotated-layout blocks: this lane's table copy (bit 6) and column rotation (bits 3-5)
+  const uint32_t lanebits = static_cast<uint32_t>((((tid >> 3) & 1) << 6) | ((tid & 7) << 3));
   const int64_t p = static_cast<int64_t>(tile) * kPoints + tid;
   const bool valid = p < n;
   const int64_t pc = valid ? p : n - 1;
@@ -571,7 +650,7 @@ __global__ void __launch_bounds__(kPoints, 1)
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = r0[c];
     } else {
-      leaf_dispatch<kExact>(Hc, H, blk, x0, x1, acc);
+      leaf_dispatch<kExact>(Hc, H, blk, x0, x1, acc, lanebits);
       if (kCarry && (Hc.b_kind & kBMore)) {  // more runs of this slot follow: park the partial sum
         double2* cs = carry + tid;
 #pragma unroll
@@ -719,7 +798,12 @@ bool FastHdmr::build(const HostProgram& hp) {
     std::vector<int16_t> slab;
     int64_t bytes = 0;
     int slot = 0;
+    int stride = kStride;  // doubles per staged row (kRotStride for the rotated layout)
   };
+  const bool rot_enabled = [] {
+    const char* e = std::getenv("DDSG_SLOT_ROT");
+    return !(e && std::atoi(e) == 0);
+  }();
   std::vector<SlotPlan> plans;
   std::vector<int16_t> dims16;
   int64_t max_bytes = 0;
@@ -743,7 +827,7 @@ bool FastHdmr::build(const HostProgram& hp) {
       H.mode = hp.slot_mode[a];
       H.tree_t = tree_t[a];
       H.tree_s = tree_s[a];
-      H.table_off = sizeof(SlotHeader);
+      H.table_off = kTableOff;
       const int flags = (r > 0 ? kBCont : 0) | (r + 1 < runs ? kBMore : 0);
       dims16.push_back(0);
       dims16.push_back(0);
@@ -841,13 +925,19 @@ bool FastHdmr::build(const HostProgram& hp) {
             H.full = all;
             H.fast_full = 1;
           }
+          // full single-run 1-d blocks use the rotated layout (conflict-free
+          // deep levels, see leaf_full1_rot); DDSG_SLOT_ROT=0 disables it
+          if (H.fast_full == 1 && k == 1 && runs == 1 && rot_enabled &&
+              static_cast<int64_t>(P.rows.size() + 1) * kRotStride * 8 <= kMaxRotBytes)
+            H.fast_full = 2;
         }
         H.zero_row = static_cast<int32_t>(P.rows.size());  // all-zero row appended to the table
         P.rows.push_back(-1);
       }
-      const int64_t table_bytes = static_cast<int64_t>(P.rows.size()) * kStride * 8;
-      H.slab_off = static_cast<int32_t>(sizeof(SlotHeader) + table_bytes);
-      P.bytes = (sizeof(SlotHeader) + table_bytes + P.slab.size() * 2 + 15) / 16 * 16;
+      P.stride = H.fast_full == 2 ? kRotStride : kStride;
+      const int64_t table_bytes = static_cast<int64_t>(P.rows.size()) * P.stride * 8;
+      H.slab_off = static_cast<int32_t>(kTableOff + table_bytes);
+      P.bytes = (kTableOff + table_bytes + P.slab.size() * 2 + 15) / 16 * 16;
       max_bytes = std::max(max_bytes, P.bytes);
     }
   }
@@ -886,7 +976,7 @@ bool FastHdmr::build(const HostProgram& hp) {
       const SlotPlan& P = plans[a];
       unsigned char* blk = host.data() + off[static_cast<size_t>(cb) * nb + a];
       std::memcpy(blk, &P.h, sizeof(SlotHeader));
-      double* table = reinterpret_cast<double*>(blk + sizeof(SlotHeader));
+      double* table = reinterpret_cast<double*>(blk + kTableOff);
       const bool empty_slot = hp.slot_k[P.slot] == 0;
       for (size_t r = 0; r < P.rows.size(); ++r)
         for (int c = 0; c < kCols; ++c) {
@@ -898,7 +988,8 @@ bool FastHdmr::build(const HostProgram& hp) {
             else if (P.rows[r] >= 0)
               v = hp.surplus[P.rows[r] * m_ + col];  // (the zero row stays 0)
           }
-          table[r * kStride + c] = v;
+          table[r * P.stride + c] = v;
+          if (P.stride == kRotStride) table[r * P.stride + kCols + c] = v;  // second copy
         }
       if (!P.slab.empty())
         std::memcpy(blk + P.h.slab_off, P.slab.data(), P.slab.size() * 2);

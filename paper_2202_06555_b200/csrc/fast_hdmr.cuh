@@ -46,7 +46,10 @@ constexpr int kSmemLevels = 4;           // levels 9..12 in shared memory (level
 constexpr int kMaxLevels = kTmemLevels + kSmemLevels;  // 2^12 active slots
 constexpr int kMaxStages = 4;            // shared-memory ring depth (fewer when slot blocks are large)
 constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
-constexpr int kMaxPaddedBytes = 96 * 1024;  // largest row table an adaptive block is padded to
+constexpr int kTableOff = 256;         // byte offset of the row table in a staged block (128-B aligned rows)
+constexpr int kRotStride = 2 * kCols;  // doubles per row of the rotated layout (two copies of the 8 columns)
+constexpr int kMaxPaddedBytes = 96 * 1024;
+constexpr int kMaxRotBytes = 40 * 1024;     // largest rotated table (1-d levels <= 8: 32 KB)  // largest row table an adaptive block is padded to
 constexpr int kBCont = 4;   // b_kind flag: continue the previous block's accumulation (later run)
 constexpr int kBMore = 8;   // b_kind flag: another run of the same slot follows
 
@@ -65,7 +68,7 @@ struct SlotHeader {
   int32_t table_off;  // byte offset of the row table within the block
   int32_t slab_off;   // byte offset of the int16 slab within the block
   int32_t zero_row;   // index of the all-zero row (target of skipped terms)
-  int32_t fast_full;  // 1: full grid of level nlev with finite surpluses (static row layout)
+  int32_t fast_full;  // 1: full grid of level nlev with finite surpluses (static row layout); 2: same, rotated rows
   int16_t sub_base[kMaxSub];  // first row (full) or slab index (partial) per subspace
   int16_t pad_[(160 - 64 - 2 * kMaxSub) / 2];
 };
