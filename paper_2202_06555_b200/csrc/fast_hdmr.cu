@@ -262,12 +262,6 @@ bool FastHdmr::build(const HostProgram& hp) {
   }
   const int nb = static_cast<int>(plans.size());
   n_blocks_ = nb;
-  for (SlotPlan& P : plans) {
-    SlotHeader& H = P.h;
-    H.code = static_cast<uint32_t>(H.k) | (static_cast<uint32_t>(H.mode) << 2) | (static_cast<uint32_t>(H.nlev) << 4) |
-             (static_cast<uint32_t>(H.b_kind) << 8) | (static_cast<uint32_t>(H.fast_full) << 12) |
-             (static_cast<uint32_t>(H.tree_s) << 16);
-  }
   block_bytes_ = (max_bytes + 127) / 128 * 128;
   {
     int64_t per_cb = 0;

@@ -54,27 +54,23 @@ constexpr int kBCont = 4;   // b_kind flag: continue the previous block's accumu
 constexpr int kBMore = 8;   // b_kind flag: another run of the same slot follows
 
 // Per-slot header at the front of every staged block (16-B aligned, 160 B).
-// The first 16 bytes are all the slot loop needs (one LDS.128): `code`
-// packs k | mode << 2 | nlev << 4 | b_kind << 8 | fast_full << 12 |
-// tree_s << 16 (filled last by the builder from the fields below).
 struct SlotHeader {
-  uint32_t code;
-  int32_t tree_t;     // leaf position in the perfect-tree embedding
-  double b;
   int32_t k;          // slot order 0..2
   int32_t mode;       // boundary mode
-  int32_t nlev;       // order 1: max level; order 2: max level sum - 1
+  int32_t nlev;       // order 1: max level; order 2: max level per dim
   int32_t d0, d1;     // point dims of the slot
+  int32_t tree_t;     // leaf position in the perfect-tree embedding
   int32_t tree_s;     // leaf span exponent
   int32_t b_kind;     // bits 0-1: 0 multiply by b, 1 b == 1, 2 b == -1; | kBCont | kBMore
-  int32_t fast_full;  // 1: full grid of level nlev with finite surpluses (static row layout); 2: same, rotated rows
+  double b;
   uint32_t present;   // bit i: canonical subspace i has nodes
   uint32_t full;      // bit i: canonical subspace i has all its cells
   int32_t table_off;  // byte offset of the row table within the block
   int32_t slab_off;   // byte offset of the int16 slab within the block
   int32_t zero_row;   // index of the all-zero row (target of skipped terms)
+  int32_t fast_full;  // 1: full grid of level nlev with finite surpluses (static row layout); 2: same, rotated rows
   int16_t sub_base[kMaxSub];  // first row (full) or slab index (partial) per subspace
-  int16_t pad_[(160 - 68 - 2 * kMaxSub) / 2];
+  int16_t pad_[(160 - 64 - 2 * kMaxSub) / 2];
 };
 static_assert(sizeof(SlotHeader) == 160, "header layout");
 

@@ -429,33 +429,30 @@ __device__ __forceinline__ void leaf_full2(const unsigned char* table, double x0
   }
 }
 
-// The header fields every slot needs, fetched with one 16-byte load.
+// The header fields every slot needs, fetched with four 16-byte loads.
 struct HeaderCore {
-  uint32_t code;
-  int32_t tree_t;
+  int32_t k, mode, nlev, d0, d1, tree_t, tree_s, b_kind;
   double b;
-  __device__ __forceinline__ int k() const { return static_cast<int>(code & 3u); }
-  __device__ __forceinline__ int mode() const { return static_cast<int>((code >> 2) & 1u); }
-  __device__ __forceinline__ int nlev() const { return static_cast<int>((code >> 4) & 15u); }
-  __device__ __forceinline__ int b_kind() const { return static_cast<int>((code >> 8) & 15u); }
-  __device__ __forceinline__ int fast_full() const { return static_cast<int>((code >> 12) & 3u); }
-  __device__ __forceinline__ int tree_s() const { return static_cast<int>(code >> 16); }
+  uint32_t present, full;
+  int32_t table_off, slab_off, zero_row, fast_full;
 };
-static_assert(sizeof(HeaderCore) == 16, "header core");
+static_assert(sizeof(HeaderCore) == 64, "header core");
 __device__ __forceinline__ HeaderCore load_core(const unsigned char* blk) {
   HeaderCore h;
-  *reinterpret_cast<uint4*>(&h) = *reinterpret_cast<const uint4*>(blk);
+  const uint4* src = reinterpret_cast<const uint4*>(blk);
+  uint4* dst = reinterpret_cast<uint4*>(&h);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dst[i] = src[i];
   return h;
 }
 
 template <int kExact>
 __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHeader& H, const unsigned char* blk,
                                               double x0, double x1, double (&acc)[kCols], uint32_t lanebits) {
-  const unsigned char* table = blk + kTableOff;
-  const int ff = Hc.fast_full();
-  if (ff == 2) {
+  const unsigned char* table = blk + Hc.table_off;
+  if (Hc.fast_full == 2) {
     const uint32_t q0 = smem_u32(table) | lanebits;
-    switch (Hc.mode() * 16 + Hc.nlev()) {
+    switch (Hc.mode * 16 + Hc.nlev) {
 #define DDSG_R1(MD, LV) \
   case MD * 16 + LV: \
     leaf_full1_rot<kExact, MD, LV>(q0, x0, acc); \
@@ -469,8 +466,8 @@ __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHe
         return;
     }
   }
-  if (ff) {
-    switch (Hc.mode() * 64 + Hc.k() * 16 + Hc.nlev()) {
+  if (Hc.fast_full) {
+    switch (Hc.mode * 64 + Hc.k * 16 + Hc.nlev) {
 #define DDSG_P1(MD, LV) \
   case MD * 64 + 16 + LV: \
     leaf_full1<kExact, MD, LV>(table, x0, acc); \
@@ -602,8 +599,6 @@ __global__ void __launch_bounds__(kPoints, 1)
 
   double xc0 = xt[static_cast<int64_t>(sdims[0]) * n + pc];
   double xc1 = xt[static_cast<int64_t>(sdims[1]) * n + pc];
-  // dims of block a+1, read from shared memory one block ahead of their use
-  int nd0 = n_active > 1 ? sdims[2] : 0, nd1 = n_active > 1 ? sdims[3] : 0;
   const int c0 = cb * kCols;
 
   // ring position of slot a (st) and of slot a-1 (pst), with their phase
@@ -626,8 +621,7 @@ __global__ void __launch_bounds__(kPoints, 1)
     const SlotHeader& H = *reinterpret_cast<const SlotHeader*>(blk);
     const HeaderCore Hc = load_core(blk);
     double acc[kCols];
-    const int b_kind = Hc.b_kind();
-    if (kCarry && (b_kind & kBCont)) {  // a later stored-order run of the same slot: resume its sum
+    if (kCarry && (Hc.b_kind & kBCont)) {  // a later stored-order run of the same slot: resume its sum
       const double2* cs = carry + tid;
 #pragma unroll
       for (int q = 0; q < kCols / 2; ++q) {
@@ -639,33 +633,29 @@ __global__ void __launch_bounds__(kPoints, 1)
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
     }
-    const int k = Hc.k();
+    const int k = Hc.k;
     const double x0 = xc0, x1 = xc1;
     if (a + 1 < n_active) {  // prefetch the next block's coordinates
-      xc0 = xt[static_cast<int64_t>(nd0) * n + pc];
-      xc1 = xt[static_cast<int64_t>(nd1) * n + pc];
-    }
-    if (a + 2 < n_active) {
-      nd0 = sdims[2 * (a + 2)];
-      nd1 = sdims[2 * (a + 2) + 1];
+      xc0 = xt[static_cast<int64_t>(sdims[2 * (a + 1)]) * n + pc];
+      xc1 = xt[static_cast<int64_t>(sdims[2 * (a + 1) + 1]) * n + pc];
     }
     bool leaf_done = true;
     if (k == 0) {
-      const double* r0 = reinterpret_cast<const double*>(blk + kTableOff);
+      const double* r0 = reinterpret_cast<const double*>(blk + Hc.table_off);
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = r0[c];
     } else {
       leaf_dispatch<kExact>(Hc, H, blk, x0, x1, acc, lanebits);
-      if (kCarry && (b_kind & kBMore)) {  // more runs of this slot follow: park the partial sum
+      if (kCarry && (Hc.b_kind & kBMore)) {  // more runs of this slot follow: park the partial sum
         double2* cs = carry + tid;
 #pragma unroll
         for (int q = 0; q < kCols / 2; ++q) cs[q * kPoints] = make_double2(acc[2 * q], acc[2 * q + 1]);
         leaf_done = false;
-      } else if ((b_kind & 3) == 0) {
+      } else if ((Hc.b_kind & 3) == 0) {
         const double b = Hc.b;
 #pragma unroll
         for (int c = 0; c < kCols; ++c) acc[c] = __dmul_rn(acc[c], b);
-      } else if ((b_kind & 3) == 2) {
+      } else if ((Hc.b_kind & 3) == 2) {
 #pragma unroll
         for (int c = 0; c < kCols; ++c) acc[c] = -acc[c];
       }
@@ -673,7 +663,7 @@ __global__ void __launch_bounds__(kPoints, 1)
     // pairwise tree (perfect-tree embedding): merge with the pending left
     // siblings at levels s.. while the position bit is set, then park.
     const int t = Hc.tree_t;
-    int i = Hc.tree_s();
+    int i = Hc.tree_s;
     if (!kCarry || leaf_done) {
       while (i < levels && ((t >> i) & 1)) {
         double v[kCols];
