@@ -1,22 +1,27 @@
 // Slot-staged HDMR evaluation kernel for low-order cut-HDMR programs
 // (every active slot of order <= 2): the B200 hot path for BASELINE configs 4-5.
 //
-// Design (DESIGN.md §Kernels):
+// Design (DESIGN.md §3.2):
 //  * One CTA = kWarps x 32 points (lanes = points) x one block of kCols output
-//    columns.  Every active slot's surplus block for that column block is a
-//    contiguous global region [header | rows x kStride doubles | slab], moved
-//    into a shared-memory ring by one TMA bulk copy (cp.async.bulk + mbarrier).
-//  * Each thread walks the slot's subspaces in canonical order (statically
-//    unrolled for order-1 levels <= kL1 and order-2 levels <= kL2), computes the
-//    candidate cell and the bit-exact weight, and gathers s[row][c] with
-//    LDS.128: lanes of a warp read the same column of (few) rows, so the
-//    shared-memory broadcast path delivers 256 B/clk/SM.
+//    columns.  Every staged block (an active slot, or one stored-order run of
+//    it) for that column block is a contiguous global region
+//    [header | row table | slab], moved into a shared-memory ring of up to
+//    kMaxStages stages by one TMA bulk copy (cp.async.bulk + mbarrier
+//    expect-tx; per-stage "empty" mbarriers let warps run ahead).
+//  * Each thread walks the block's subspaces in canonical order (statically
+//    unrolled for order-1 levels <= kL1 and order-2 level sums <= kL2 + 1),
+//    computes the candidate cell and the bit-exact weight, and gathers its
+//    row with LDS.64: rows of kStride (9) doubles, or for full 1-d blocks the
+//    rotated dual-copy rows of kRotStride doubles that keep every half-warp
+//    on distinct banks.  Adaptive blocks are padded to full grids with zero
+//    rows (same terms, static row bases).
 //  * Leaf (slot) values enter the reference's pairwise tree through a
 //    perfect-binary-tree embedding (leaf a at position t_a spanning 2^s_a):
-//    pending level 0 lives in registers, levels 1..8 in tensor memory (each
-//    thread owns its TMEM lane in the warp's lane quarter, 16 columns per
-//    level, tcgen05.st/ld 32x32b.x16 -- off the shared-memory pipe that the
-//    gathers saturate), the rarely touched levels >= 9 in shared memory.
+//    pending levels 0..7 live in tensor memory (each thread owns its TMEM
+//    lane in the warp's lane quarter, 16 columns per level,
+//    tcgen05.st/ld 32x32b.x16 -- off the shared-memory pipe that the gathers
+//    saturate), the rarely touched levels >= 8 in shared memory; the root is
+//    written to y directly.
 //  * EXACT mode: DMUL then DADD per term (bit-identical to the reference);
 //    FAST mode: one DFMA per term.
 #pragma once
