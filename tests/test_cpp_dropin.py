@@ -11,9 +11,12 @@ DRIVER = ROOT / "build" / "test_dropin"
 
 def _driver():
     if not DRIVER.exists():
-        from paper_2202_06555_b200.build import build_library
+        import sys
 
-        build_library()
+        sys.path.insert(0, str(ROOT))
+        import __graft_entry__
+
+        __graft_entry__._load_builder().build_library()
     return DRIVER
 
 
