@@ -368,7 +368,10 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
                            Scratch& xt_scratch) {
   if (n <= 0) return 0;
   const EvalParams P = prog.params(exact);
-  if (const PlainGrid* pg = prog.plain()) return pg->launch(exact, dx, n, base, dy, dbad, st);
+  if (const PlainGrid* pg = prog.plain()) {
+    const size_t wb = pg->workspace_bytes(n);
+    return pg->launch(exact, dx, n, base, dy, dbad, wb ? xt_scratch.get(wb) : nullptr, st);
+  }
   if (const FastHdmr* f = prog.fast()) {
     // chunk so the dim-major scratch stays <= ~1 GiB
     const int d = f->dim();

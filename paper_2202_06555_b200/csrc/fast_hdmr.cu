@@ -34,7 +34,7 @@ __global__ void transpose_check_kernel(const double* __restrict__ x, int64_t n, 
     const int j = j0 + tx;
     double v = 0.5;
     if (p < n && j < d) {
-      v = x[p * d + j];
+      v = __ldcs(x + p * d + j);  // read once
       if (!(v >= 0.0 && v <= 1.0)) atomicMin(bad, static_cast<unsigned long long>(base + p));
     }
     tile[r][tx] = v;
@@ -266,7 +266,8 @@ bool FastHdmr::build(const HostProgram& hp) {
   {
     int64_t per_cb = 0;
     for (const SlotPlan& P : plans) per_cb += P.bytes;
-    const int64_t budget = int64_t{64} << 20;  // staged tables kept L2-resident per CTA wave
+    int64_t budget = int64_t{64} << 20;  // staged tables kept L2-resident per CTA wave
+    if (const char* e = std::getenv("DDSG_CB_BUDGET_MB")) budget = std::max<int64_t>(1, std::atoll(e)) << 20;
     cb_group_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_cb_, budget / std::max<int64_t>(per_cb, 1))));
   }
   const int64_t deep_bytes = std::min(std::max(0, levels - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
