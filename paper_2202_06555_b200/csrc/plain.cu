@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
       const double xv = valid ? x[p * d + j] : 0.5;
       ok &= (xv >= 0.0 && xv <= 1.0);
       xr[j] = xv;
-      xi[j] = ok ? static_cast<uint32_t>(__dmul_rn(xv, 2147483648.0)) : 0u;
+      xi[j] = ok ? min(static_cast<uint32_t>(__dmul_rn(xv, 2147483648.0)), 0x7fffffffu) : 0u;  // factor(): clamped
     }
   }
   if (valid && !ok) atomicMin(bad, static_cast<unsigned long long>(base + p));

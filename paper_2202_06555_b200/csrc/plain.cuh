@@ -20,24 +20,32 @@ constexpr int kSortMinDim = 5;
 constexpr int64_t kSortMinPoints = 4096;
 
 // Exact 1-d factor of the candidate cell at (runtime) level l:
-// xi = floor(x 2^31), so floor(x 2^(l-1)) = xi >> (32 - l); clamped at x = 1.
+// xi = floor(x 2^31) clamped to 2^31 - 1, so xi >> (32 - l) is the candidate
+// cell floor(x 2^(l-1)), clamped at x = 1.  The value is
+// basis.cuh's restatement v = fl(A - |fl(x 2^l - B)|) with
+//  * x 2^l formed by adding l to the exponent field of x: exact for normal
+//    x; for x = 0 (or subnormal x) the result is a tiny t that rounds away
+//    against B >= 1 (hat) or against A = 2 (modified left edge, B = 0),
+//    exactly as t = 0 does;
+//  * B as a double by the 2^52 trick (one DADD, fixed latency, no I2F).
 template <int kMode>
 __device__ __forceinline__ void factor(double x, uint32_t xi, int l, uint32_t& kk, double& v) {
-  const uint32_t ncell = 1u << (l - 1);
-  kk = min(xi >> (32 - l), ncell - 1u);
+  kk = xi >> (32 - l);
   if (kMode == 1 && l == 1) {
     v = 1.0;
     return;
   }
-  const double t = __dmul_rn(x, __hiloint2double((1023 + l) << 20, 0));  // x 2^l, exact
+  const double t = __hiloint2double(__double2hiint(x) + (l << 20), __double2loint(x));
   uint32_t B = 2u * kk + 1u;
   double A = 1.0;
   if (kMode == 1) {
-    const bool left = kk == 0u, right = kk == ncell - 1u;
-    B = left ? 0u : (right ? 2u * ncell : B);
+    const uint32_t ncm1 = (1u << (l - 1)) - 1u;
+    const bool left = kk == 0u, right = kk == ncm1;
+    B = left ? 0u : (right ? 2u * ncm1 + 2u : B);
     A = (left || right) ? 2.0 : 1.0;
   }
-  v = __dadd_rn(A, -fabs(__dadd_rn(t, -static_cast<double>(B))));  // >= 0 at the candidate cell
+  const double Bd = __dadd_rn(__hiloint2double(0x43300000, static_cast<int>(B)), -4503599627370496.0);
+  v = __dadd_rn(A, -fabs(__dadd_rn(t, -Bd)));  // >= 0 at the candidate cell
 }
 
 }  // namespace plain
