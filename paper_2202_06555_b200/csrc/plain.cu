@@ -47,7 +47,7 @@ namespace plain {
 
 struct Params {
   int d, m, runs;
-  int run_off[kMaxRuns + 1];  // run r walks records [run_off[r], run_off[r+1])
+  const int* run_off;  // device array: run r walks records [run_off[r], run_off[r+1])
   const uint4* rec;        // [records][2]: per run, the subspaces holding nodes of that run
   const uint32_t* perm;    // thread p evaluates point perm[p] (Morton order), or p when null
   const int32_t* slab;     // partial subspaces: cell -> row or -1
@@ -58,7 +58,7 @@ struct Params {
 };
 
 template <int kDMax, int kMC, int kExact, int kMode, int kMultiRun>
-__global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
+__global__ void __launch_bounds__(kThreads, kDMax <= 10 ? 4 : 1) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
                                                          int64_t base, double* __restrict__ y,
                                                          unsigned long long* bad) {
   const int tid = threadIdx.x;
@@ -136,8 +136,9 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         row = use ? r : P.zero_row;
       };
       const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-      const uint4* rec = P.rec + 2 * P.run_off[run];
-      const int n_sub = P.run_off[run + 1] - P.run_off[run];
+      const int off0 = __ldg(P.run_off + run), off1 = __ldg(P.run_off + run + 1);
+      const uint4* rec = P.rec + 2 * off0;
+      const int n_sub = off1 - off0;
       if (n_sub == 0) continue;
       // subspace records are prefetched one iteration ahead of their use
       uint4 ra = __ldg(rec), rb = kDMax > 16 ? __ldg(rec + 1) : zero4;
@@ -167,6 +168,149 @@ __global__ void __launch_bounds__(kThreads) plain_kernel(Params P, const double*
         if (s + 2 < n_sub) {
           ra = __ldg(rec + 2 * (s + 2));
           if (kDMax > 16) rb = __ldg(rec + 2 * (s + 2) + 1);
+        }
+        double w_nxt = 0.0;
+        int row_nxt = P.zero_row;
+        if (s + 1 < n_sub) term(ua, ub, w_nxt, row_nxt);
+#pragma unroll
+        for (int c = 0; c < kMC; ++c)
+          acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[c]);
+        w_cur = w_nxt;
+        row_cur = row_nxt;
+      }
+    }
+    const int nc = min(kMC, P.m - c0);
+    double* yp = y + p * P.m + c0;
+#pragma unroll
+    for (int c = 0; c < kMC; ++c)
+      if (c < nc) yp[c] = acc[c];
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Sparse walk for modified-linear grids (config 3).  There the level-1 factor
+// is exactly 1 (basis.hpp:40), so the reference's dim-ordered product
+// w = ((1 * v_0) * v_1) * ... equals the product over the dims with l_j > 1
+// only, in dim order (multiplying by 1.0 is exact), and level-1 dims add no
+// bits to the cell index.  A subspace record then lists its <= kSparseNT
+// non-trivial (dim, level) pairs; the prefix caches hold kSparseNT entries
+// instead of d, and the coordinates live in shared memory (dim-major: a warp
+// reading one dim hits 32 consecutive words), which frees the registers that
+// held d-wide arrays: config 3 (d = 20, at most 4 non-trivial dims) runs at
+// a multiple of the occupancy of plain_kernel.
+constexpr int kSparseNT = 8;
+constexpr int kSparseThreads = 128;
+
+// record: x = first row (full) or slab offset; y = qs | nt << 4 | full << 8
+// (qs: pairs reused from the previous record of the run, < nt unless nt = 0);
+// z, w, [1].x, [1].y: pair k in 16 bits of word k / 2 (dim | level << 8)
+struct SparseParams {
+  int d, m, runs, ms, zero_row;
+  const int* run_off;  // device array (a dynamic index into a parameter array would copy it to local memory)
+  const uint4* rec;
+  const uint32_t* perm;
+  const int32_t* slab;
+  const int16_t* row_run;
+  const double* surplus;
+};
+
+template <int kMC, int kExact, int kMultiRun>
+__global__ void __launch_bounds__(kSparseThreads) sparse_kernel(SparseParams P, const double* __restrict__ x,
+                                                                int64_t n, int64_t base, double* __restrict__ y,
+                                                                unsigned long long* bad) {
+  extern __shared__ double xs[];  // [d][kSparseThreads] coordinates, then [d][kSparseThreads] fixed point
+  const int tid = threadIdx.x;
+  const int d = P.d;
+  uint32_t* xis = reinterpret_cast<uint32_t*>(xs + d * kSparseThreads);
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * kSparseThreads + tid;
+  const bool valid = t < n;
+  const int64_t p = valid && P.perm ? static_cast<int64_t>(P.perm[t]) : t;
+  bool ok = valid;
+  for (int j = 0; j < d; ++j) {
+    const double xv = valid ? x[p * d + j] : 0.5;
+    ok &= (xv >= 0.0 && xv <= 1.0);
+    xs[j * kSparseThreads + tid] = xv;
+    xis[j * kSparseThreads + tid] = ok ? min(static_cast<uint32_t>(__dmul_rn(xv, 2147483648.0)), 0x7fffffffu) : 0u;
+  }
+  if (valid && !ok) atomicMin(bad, static_cast<unsigned long long>(base + p));
+  if (!valid || !ok) return;  // each thread reads only its own coordinates: no barrier
+
+  for (int c0 = 0; c0 < P.m; c0 += kMC) {
+    double acc[kMC];
+#pragma unroll
+    for (int c = 0; c < kMC; ++c) acc[c] = 0.0;
+    for (int run = 0; run < (kMultiRun ? P.runs : 1); ++run) {
+      double pw[kSparseNT];
+      uint32_t pc[kSparseNT];
+#pragma unroll
+      for (int k = 0; k < kSparseNT; ++k) {
+        pw[k] = 1.0;
+        pc[k] = 0u;
+      }
+      auto term = [&](const uint4& r0, const uint4& r1, double& w, int& row) {
+        const uint32_t pairw[4] = {r0.z, r0.w, r1.x, r1.y};  // pair k: 16 bits of word k / 2
+        const int nt = static_cast<int>((r0.y >> 4) & 15u);
+        w = 1.0;
+        uint32_t cell = 0u;
+        switch (static_cast<int>(r0.y & 15u)) {
+#define DDSG_SDIM(K)                                                                           \
+  case K: {                                                                                    \
+    if ((K) >= nt) break;                                                                      \
+    const uint32_t pr = (pairw[(K) / 2] >> (16 * ((K) & 1))) & 0xffffu;                       \
+    const int dim = static_cast<int>(pr & 0xffu), l = static_cast<int>(pr >> 8);              \
+    uint32_t kk;                                                                               \
+    double v;                                                                                  \
+    factor<1>(xs[dim * kSparseThreads + tid], xis[dim * kSparseThreads + tid], l, kk, v);      \
+    if ((K) == 0) {                                                                            \
+      pw[0] = v;                                                                               \
+      pc[0] = kk;                                                                              \
+    } else {                                                                                   \
+      constexpr int kp = (K) > 0 ? (K) - 1 : 0;                                                \
+      pw[K] = __dmul_rn(pw[kp], v);                                                            \
+      pc[K] = (pc[kp] << (l - 1)) | kk;                                                        \
+    }                                                                                          \
+    if ((K) == nt - 1) {                                                                       \
+      w = pw[K];                                                                               \
+      cell = pc[K];                                                                            \
+    }                                                                                          \
+  }                                                                                            \
+    [[fallthrough]];
+          DDSG_SDIM(0) DDSG_SDIM(1) DDSG_SDIM(2) DDSG_SDIM(3) DDSG_SDIM(4) DDSG_SDIM(5) DDSG_SDIM(6) DDSG_SDIM(7)
+#undef DDSG_SDIM
+          default:
+            break;
+        }
+        int r = static_cast<int>(r0.x) + static_cast<int>(cell);
+        if (!((r0.y >> 8) & 1u)) r = __ldg(P.slab + r);
+        bool use = w != 0.0 && r >= 0;  // sparse_grid.hpp:123 (w == 0 skipped), absent node
+        if (kMultiRun) use = use && __ldg(P.row_run + r) == run;
+        row = use ? r : P.zero_row;
+      };
+      const int off0 = __ldg(P.run_off + run), off1 = __ldg(P.run_off + run + 1);
+      const uint4* rec = P.rec + 2 * off0;
+      const int n_sub = off1 - off0;
+      if (n_sub == 0) continue;
+      uint4 ra = __ldg(rec), rb = __ldg(rec + 1);
+      double w_cur;
+      int row_cur;
+      term(ra, rb, w_cur, row_cur);
+      if (n_sub > 1) {
+        ra = __ldg(rec + 2);
+        rb = __ldg(rec + 3);
+      }
+      for (int s = 0; s < n_sub; ++s) {
+        double sv[kMC];
+        const double* sr = P.surplus + static_cast<int64_t>(row_cur) * P.ms + c0;
+#pragma unroll
+        for (int c = 0; c < kMC; c += 4)
+          asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+              : "=d"(sv[c]), "=d"(sv[c + 1]), "=d"(sv[c + 2]), "=d"(sv[c + 3])
+              : "l"(sr + c));
+        const uint4 ua = ra, ub = rb;
+        if (s + 2 < n_sub) {
+          ra = __ldg(rec + 2 * (s + 2));
+          rb = __ldg(rec + 2 * (s + 2) + 1);
         }
         double w_nxt = 0.0;
         int row_nxt = P.zero_row;
@@ -262,6 +406,7 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
     }
     run_off_.push_back(static_cast<int>(rec.size() / 8));
   }
+  run_off_dev_ = put(run_off_);
   d_ = d;
   m_ = hp.m;
   mode_ = hp.slot_mode[0];
@@ -280,10 +425,73 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   slab_ = dev.slab;
   row_run_ = dev.row_run;
   usable_ = true;
+  build_sparse(hp);
   sort_ = d >= kSortMinDim;
   if (const char* e = std::getenv("DDSG_PLAIN_SORT"))
     if (std::atoi(e) == 0) sort_ = false;
   return true;
+}
+
+// Sparse-walk records (modified-linear grids, d >= 5, <= kSparseNT dims above
+// level 1 per subspace, d <= kSparseMaxDim): same subspaces and order as the
+// dense records.
+bool PlainGrid::build_sparse(const HostProgram& hp) {
+  sparse_ = false;
+  const int d = hp.d;
+  if (hp.slot_mode[0] != 1 || d < kSortMinDim || d > kSparseMaxDim || hp.m <= 1) return false;
+  if (const char* e = std::getenv("DDSG_PLAIN_SPARSE"))
+    if (std::atoi(e) == 0) return false;
+  const int s0 = hp.slot_sub_begin[0], s1 = hp.slot_sub_end[0];
+  const int runs = hp.slot_runs[0];
+  std::vector<uint32_t> rec;
+  srun_off_.assign(1, 0);
+  for (int run = 0; run < runs; ++run) {
+    const uint8_t* prev = nullptr;
+    for (int s = s0; s < s1; ++s) {
+      const uint8_t* lv = &hp.levels[hp.sub_lv_off[s]];
+      int64_t cells = 1;
+      int nt = 0;
+      for (int j = 0; j < d; ++j) {
+        cells <<= (lv[j] - 1);
+        nt += lv[j] > 1;
+      }
+      if (nt > kSparseNT) return false;
+      const int64_t slab_off = hp.sub_slab_off[s];
+      if (runs > 1) {  // the dense walk's run filter
+        bool has = false;
+        for (int64_t c = 0; c < cells && !has; ++c) {
+          const int32_t row = hp.slab[slab_off + c];
+          has = row >= 0 && hp.row_run[row] == run;
+        }
+        if (!has) continue;
+      }
+      int qq = 0;  // first dim differing from the previous record of the run
+      if (prev)
+        while (qq < d && prev[qq] == lv[qq]) ++qq;
+      prev = lv;
+      int qs = 0;  // non-trivial pairs below qq are unchanged
+      for (int j = 0; j < qq; ++j) qs += lv[j] > 1;
+      if (nt > 0) qs = std::min(qs, nt - 1);  // recompute >= 1 pair: the last one yields w
+      const bool is_full = hp.sub_nodes[s] == cells;
+      uint32_t r[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      r[0] = static_cast<uint32_t>(is_full ? hp.slab[slab_off] : slab_off);
+      r[1] = static_cast<uint32_t>(qs) | (static_cast<uint32_t>(nt) << 4) | (is_full ? 0x100u : 0u);
+      int k = 0;
+      for (int j = 0; j < d; ++j)
+        if (lv[j] > 1) {
+          r[2 + k / 2] |= (static_cast<uint32_t>(j) | (static_cast<uint32_t>(lv[j]) << 8)) << (16 * (k & 1));
+          ++k;
+        }
+      rec.insert(rec.end(), r, r + 8);
+    }
+    srun_off_.push_back(static_cast<int>(rec.size() / 8));
+  }
+  srec_ = reinterpret_cast<const uint4*>(put(rec));
+  srun_off_dev_ = put(srun_off_);
+  smc_ = hp.m <= 12 ? 12 : 24;
+  if (const char* e = std::getenv("DDSG_SPARSE_COLS")) smc_ = std::atoi(e) == 24 ? 24 : 12;
+  sparse_ = (ms_ % smc_) == 0;
+  return sparse_;
 }
 
 // Morton key of each point: `bits` bits per dim from the top of floor(x 2^31)
@@ -305,6 +513,35 @@ __global__ void morton_key_kernel(const double* __restrict__ x, int64_t n, int d
 }
 
 static int morton_bits(int d) { return std::max(1, std::min(16, 40 / d)); }
+
+template <int kMC, int kExact, int kMulti>
+static void launch_sparse_t(const SparseParams& S, unsigned grid, size_t smem, const double* x, int64_t n,
+                            int64_t base, double* y, unsigned long long* bad, cudaStream_t st) {
+  auto k = sparse_kernel<kMC, kExact, kMulti>;
+  if (smem > 48 * 1024)
+    DDSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k<<<grid, kSparseThreads, smem, st>>>(S, x, n, base, y, bad);
+}
+
+static void launch_sparse(int mc, int exact, bool multi, const SparseParams& S, unsigned grid, size_t smem,
+                          const double* x, int64_t n, int64_t base, double* y, unsigned long long* bad,
+                          cudaStream_t st) {
+  if (mc == 24) {
+    if (exact)
+      multi ? launch_sparse_t<24, 1, 1>(S, grid, smem, x, n, base, y, bad, st)
+            : launch_sparse_t<24, 1, 0>(S, grid, smem, x, n, base, y, bad, st);
+    else
+      multi ? launch_sparse_t<24, 0, 1>(S, grid, smem, x, n, base, y, bad, st)
+            : launch_sparse_t<24, 0, 0>(S, grid, smem, x, n, base, y, bad, st);
+  } else {
+    if (exact)
+      multi ? launch_sparse_t<12, 1, 1>(S, grid, smem, x, n, base, y, bad, st)
+            : launch_sparse_t<12, 1, 0>(S, grid, smem, x, n, base, y, bad, st);
+    else
+      multi ? launch_sparse_t<12, 0, 1>(S, grid, smem, x, n, base, y, bad, st)
+            : launch_sparse_t<12, 0, 0>(S, grid, smem, x, n, base, y, bad, st);
+  }
+}
 
 template <int kDMax, int kMC, int kMode, int kMulti>
 static void launch_plain(const Params& P, int exact, const double* x, int64_t n, int64_t base, double* y,
@@ -358,12 +595,33 @@ int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, d
     perm = vb.Current();
     launches = 2;  // key kernel + evaluation kernel (the sort's kernels are CUB's)
   }
+  if (sparse_) {
+    SparseParams S{};
+    S.d = d_;
+    S.m = m_;
+    S.runs = runs_;
+    S.ms = ms_;
+    S.zero_row = zero_row_;
+    S.run_off = srun_off_dev_;
+    S.rec = srec_;
+    S.perm = perm;
+    S.slab = slab_;
+    S.row_run = row_run_;
+    S.surplus = surplus_;
+    const unsigned grid = static_cast<unsigned>((n + kSparseThreads - 1) / kSparseThreads);
+    const size_t smem = static_cast<size_t>(d_) * kSparseThreads * 12;
+    kernel_timer().begin(st);
+    launch_sparse(smc_, exact, runs_ > 1, S, grid, smem, x, n, base, y, bad, st);
+    kernel_timer().end(st);
+    DDSG_CUDA(cudaGetLastError());
+    return launches;
+  }
   Params P{};
   P.perm = perm;
   P.d = d_;
   P.m = m_;
   P.runs = runs_;
-  for (int r = 0; r <= runs_; ++r) P.run_off[r] = run_off_[r];
+  P.run_off = run_off_dev_;
   P.rec = rec_;
   P.slab = slab_;
   P.row_run = row_run_;

@@ -17,6 +17,7 @@ constexpr int kMaxRuns = 15;
 // Morton pre-sort of the points (plain.cu): only for d >= 5 (config 1's
 // small grid is launch-bound) and batches of >= 4096 points
 constexpr int kSortMinDim = 5;
+constexpr int kSparseMaxDim = 64;  // sparse walk: coordinates of 128 points x d dims in shared memory
 constexpr int64_t kSortMinPoints = 4096;
 
 // Exact 1-d factor of the candidate cell at (runtime) level l:
@@ -72,8 +73,15 @@ class PlainGrid {
  private:
   bool usable_ = false;
   bool sort_ = false;  // Morton pre-sort of large batches
+  bool build_sparse(const HostProgram& hp);
+  bool sparse_ = false;  // modified-linear grids: sparse walk over the non-trivial dims
+  int smc_ = 12;         // sparse walk: columns per pass
+  std::vector<int> srun_off_;
+  const uint4* srec_ = nullptr;
+  const int* srun_off_dev_ = nullptr;
   int d_ = 0, m_ = 0, ms_ = 0, mc_ = 1, mode_ = 0, runs_ = 1, zero_row_ = 0;
   std::vector<int> run_off_;
+  const int* run_off_dev_ = nullptr;
   const uint4* rec_ = nullptr;  // [n_sub][2] packed subspace records
   const int32_t* slab_ = nullptr;
   const int16_t* row_run_ = nullptr;

@@ -18,23 +18,26 @@ from paper_2202_06555_b200.ddsg import (FAST, MODIFIED_LINEAR, ZERO_BOUNDARY, Do
 pytestmark = pytest.mark.gpu
 
 
-def _copy(g: SparseGridFunction, sort: bool, canonical: bool = False) -> SparseGridFunction:
+def _copy(g: SparseGridFunction, sort: bool, canonical: bool = False, sparse: bool = True) -> SparseGridFunction:
     """Same nodes (same order unless canonical), evaluated with (sort=True) or
-    without the Morton pre-sort of the points."""
+    without the Morton pre-sort of the points, and for modified-linear grids
+    on the sparse walk (sparse=True) or the dense walk."""
     keys, sur = g.nodes()
     if canonical:
         p = canonical_perm(keys)
         keys, sur = keys[p], sur[p]
-    old = os.environ.get("DDSG_PLAIN_SORT")
-    os.environ["DDSG_PLAIN_SORT"] = "1" if sort else "0"
+    env = {"DDSG_PLAIN_SORT": "1" if sort else "0", "DDSG_PLAIN_SPARSE": "1" if sparse else "0"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         h = SparseGridFunction.from_nodes(g.dim, g.out_dim, g.max_level, g.eps_gamma, g.boundary_mode, keys, sur)
-        h.interpolate(np.full((1, g.dim), 0.5))  # uploads the device program under this setting
+        h.interpolate(np.full((1, g.dim), 0.5))  # uploads the device program under these settings
     finally:
-        if old is None:
-            del os.environ["DDSG_PLAIN_SORT"]
-        else:
-            os.environ["DDSG_PLAIN_SORT"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
     return h
 
 
@@ -73,11 +76,12 @@ def test_config2_sorted_matches_direct_and_oracle(config2):
     assert np.array_equal(bits(yt[:160]), bits(_oracle(config2, x[:160])))
 
 
-def test_config3_multirun_sorted_matches_direct_and_oracle(config3):
-    """Config 3's adaptive build: 2 stored-order runs, partial subspaces
-    (slab lookups in the staging), modified-linear boundary."""
+@pytest.mark.parametrize("sparse", [True, False])
+def test_config3_multirun_sorted_matches_direct_and_oracle(config3, sparse):
+    """Config 3's adaptive build: 2 stored-order runs, partial subspaces,
+    modified-linear boundary; sparse and dense walks, sorted and unsorted."""
     cfg = W.CONFIGS[3]
-    gt, gd = _copy(config3, True), _copy(config3, False)
+    gt, gd = _copy(config3, True, sparse=sparse), _copy(config3, False, sparse=not sparse)
     x = W.points(cfg, n=6000, seed=12)
     yt = _eval_sorted(gt, x)
     assert np.array_equal(bits(yt), bits(gd.interpolate(x)))
@@ -94,7 +98,7 @@ def test_sorted_edge_points(mode, m):
     keys, sur = g1.nodes()  # adaptive, stored order; m output columns
     sur_m = np.concatenate([sur * (1.0 + 0.1 * j) - 0.01 * j for j in range(m)], axis=1)
     g0 = SparseGridFunction.from_nodes(7, m, g1.max_level, g1.eps_gamma, mode, keys, sur_m)
-    gt, gd = _copy(g0, True), _copy(g0, False)
+    gt, gd = _copy(g0, True), _copy(g0, False, sparse=False)
     n = 5000 + 123
     x = uniform_points(321, n, 7)
     edges = np.array([0.0, 1.0, 0.5, 0.25, 0.75, 0.125, 0.875, 1 - 2**-53, 2**-30, 2**-4])
