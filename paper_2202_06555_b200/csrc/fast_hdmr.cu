@@ -244,9 +244,11 @@ bool FastHdmr::build(const HostProgram& hp) {
             H.full = all;
             H.fast_full = 1;
           }
-          // full single-run 1-d blocks use the rotated layout (conflict-free
-          // deep levels, see leaf_full1_rot); DDSG_SLOT_ROT=0 disables it
-          if (H.fast_full == 1 && k == 1 && runs == 1 && rot_enabled &&
+          // full single-run 1-d blocks, and 2-d blocks of max level 6 (32
+          // candidate rows at level sum 7), use the rotated layout
+          // (conflict-free deep levels, see leaf_full1_rot / leaf_full2_rot);
+          // DDSG_SLOT_ROT=0 disables it
+          if (H.fast_full == 1 && (k == 1 || (k == 2 && nlev == 6)) && runs == 1 && rot_enabled &&
               static_cast<int64_t>(P.rows.size() + 1) * kRotStride * 8 <= kMaxRotBytes)
             H.fast_full = 2;
         }

@@ -54,7 +54,7 @@ constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
 constexpr int kTableOff = 256;         // byte offset of the row table in a staged block (128-B aligned rows)
 constexpr int kRotStride = 2 * kCols;  // doubles per row of the rotated layout (two copies of the 8 columns)
 constexpr int kMaxPaddedBytes = 96 * 1024;  // largest row table an adaptive block is padded to
-constexpr int kMaxRotBytes = 40 * 1024;     // largest rotated table (1-d levels <= 8: 32 KB)
+constexpr int kMaxRotBytes = 48 * 1024;     // largest rotated table (1-d levels <= 8: 32 KB; 2-d level 6: 41 KB)
 constexpr int kBCont = 4;   // b_kind flag: continue the previous block's accumulation (later run)
 constexpr int kBMore = 8;   // b_kind flag: another run of the same slot follows
 

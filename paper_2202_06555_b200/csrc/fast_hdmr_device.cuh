@@ -327,6 +327,23 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
 // instead of 3.9-5.5 (profiles/r1_lds_rotate.json).  The slot starts from a
 // zero accumulator (rotation-free) and un-rotates it once at the end
 // (3 conditional swap stages).  q0 = shared address of row 0 | lane bits.
+// Rotated layout: accumulator slot j holds column c0 ^ j (c0 = this lane's
+// rotation, bits 3-5 of q0); swap back in three conditional stages.
+__device__ __forceinline__ void unrotate(uint32_t q0, double (&acc)[kCols]) {
+  const uint32_t c0 = (q0 >> 3) & 7u;
+#pragma unroll
+  for (int b = 1; b < kCols; b <<= 1) {
+    const bool flip = (c0 & static_cast<uint32_t>(b)) != 0u;
+#pragma unroll
+    for (int c = 0; c < kCols; ++c)
+      if (!(c & b)) {
+        const double lo = acc[c], hi = acc[c | b];
+        acc[c] = flip ? hi : lo;
+        acc[c | b] = flip ? lo : hi;
+      }
+  }
+}
+
 template <int kExact, int kMode, int L>
 __device__ __forceinline__ void leaf_full1_rot(uint32_t q0, double x, double (&acc)[kCols]) {
   double w[L];
@@ -358,19 +375,7 @@ __device__ __forceinline__ void leaf_full1_rot(uint32_t q0, double x, double (&a
     }
     fma_row<kExact>(acc, w[i], buf[i & 1]);
   }
-  // slot j holds column c0 ^ j: swap back (c0 = this lane's rotation)
-  const uint32_t c0 = (q0 >> 3) & 7u;
-#pragma unroll
-  for (int b = 1; b < kCols; b <<= 1) {
-    const bool flip = (c0 & static_cast<uint32_t>(b)) != 0u;
-#pragma unroll
-    for (int c = 0; c < kCols; ++c)
-      if (!(c & b)) {
-        const double lo = acc[c], hi = acc[c | b];
-        acc[c] = flip ? hi : lo;
-        acc[c | b] = flip ? lo : hi;
-      }
-  }
+  unrotate(q0, acc);
 }
 
 // Full order-2 slot with max level L per dim (level sum <= L + 1), canonical
@@ -429,6 +434,66 @@ __device__ __forceinline__ void leaf_full2(const unsigned char* table, double x0
   }
 }
 
+// Full order-2 slot in the rotated layout (fast_full == 2; max level L >= 6,
+// whose level-sum-7 subspaces have 32 candidate rows and conflict in the
+// stride-9 layout): leaf_full2's terms and order, leaf_full1_rot's loads.
+template <int kExact, int kMode, int L>
+__device__ __forceinline__ void leaf_full2_rot(uint32_t q0, double x0, double x1, double (&acc)[kCols]) {
+  double v0[L], v1[L];
+  uint32_t k0[L], k1[L];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    switch (l) {
+#define DDSG_F(LV)                                  \
+  case LV:                                          \
+    factor_full<LV, kMode>(x0, k0[l - 1], v0[l - 1]); \
+    factor_full<LV, kMode>(x1, k1[l - 1], v1[l - 1]); \
+    break;
+      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4) DDSG_F(5) DDSG_F(6)
+#undef DDSG_F
+      default:
+        break;
+    }
+  }
+  constexpr int kN = L * (L + 1) / 2;
+  auto term = [&](int i, double& w, uint32_t& addr) {
+    int idx = 0;
+#pragma unroll
+    for (int s = 2; s <= L + 1; ++s)
+#pragma unroll
+      for (int l1 = 1; l1 < s; ++l1) {
+        const int l2 = s - l1;
+        if (idx == i) {
+          if (kMode == 1 && l1 == 1)
+            w = v1[l2 - 1];
+          else if (kMode == 1 && l2 == 1)
+            w = v0[l1 - 1];
+          else
+            w = __dmul_rn(v0[l1 - 1], v1[l2 - 1]);
+          addr = q0 + ((static_cast<uint32_t>(base2(l1, l2)) + ((k0[l1 - 1] << (l2 - 1)) | k1[l2 - 1])) << 7);
+        }
+        ++idx;
+      }
+  };
+  double wb[2];
+  uint32_t ab[2];
+  term(0, wb[0], ab[0]);
+  double buf[2][kCols];  // static ping-pong
+#pragma unroll
+  for (int j = 0; j < kCols; ++j) buf[0][j] = lds_f64(ab[0] ^ static_cast<uint32_t>(j << 3));
+#pragma unroll
+  for (int i = 0; i < kN; ++i) {
+    if (i + 1 < kN) {
+      term(i + 1, wb[(i + 1) & 1], ab[(i + 1) & 1]);
+#pragma unroll
+      for (int j = 0; j < kCols; ++j)
+        buf[(i + 1) & 1][j] = lds_f64(ab[(i + 1) & 1] ^ static_cast<uint32_t>(j << 3));
+    }
+    fma_row<kExact>(acc, wb[i & 1], buf[i & 1]);
+  }
+  unrotate(q0, acc);
+}
+
 // The header fields every slot needs, fetched with four 16-byte loads.
 struct HeaderCore {
   int32_t k, mode, nlev, d0, d1, tree_t, tree_s, b_kind;
@@ -452,6 +517,13 @@ __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHe
   const unsigned char* table = blk + Hc.table_off;
   if (Hc.fast_full == 2) {
     const uint32_t q0 = smem_u32(table) | lanebits;
+    if (Hc.k == 2) {
+      if (Hc.mode == 1)
+        leaf_full2_rot<kExact, 1, 6>(q0, x0, x1, acc);
+      else
+        leaf_full2_rot<kExact, 0, 6>(q0, x0, x1, acc);
+      return;
+    }
     switch (Hc.mode * 16 + Hc.nlev) {
 #define DDSG_R1(MD, LV) \
   case MD * 16 + LV: \

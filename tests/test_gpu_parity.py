@@ -182,16 +182,18 @@ def test_hdmr_config_exact_bitwise(cid, config4, config5):
     assert np.array_equal(nnz, nnz_o) and np.array_equal(h, h_o)
 
 
+@pytest.mark.parametrize("cid", [4, 5])
 @pytest.mark.parametrize("env", [{"DDSG_SLOT_ROT": "0"}, {"DDSG_SLOT_ROT": "1"}])
-def test_hdmr_slot_layouts_bitwise(env, config5, monkeypatch):
-    """Both staged-row layouts of full 1-d blocks (stride 9; rotated dual
-    copies, the default) give the reference's bits; the layout is chosen when
-    the device program is built."""
-    cfg, parts, slots, _ = config5
+def test_hdmr_slot_layouts_bitwise(env, cid, config4, config5, monkeypatch):
+    """Both staged-row layouts (stride 9; rotated dual copies, the default for
+    full 1-d blocks and for 2-d blocks of max level 6 -- config 4's pairs)
+    give the reference's bits; the layout is chosen when the device program
+    is built."""
+    cfg, parts, slots, _ = config4 if cid == 4 else config5
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     vec = make_vectorized(cfg.d, cfg.m, parts.f_anchor, slots, cfg.level_1d)
-    x = W.points(cfg, n=96, seed=77)
+    x = W.points(cfg, n=192 if cid == 4 else 96, seed=77)
     rc, want, _ = O.port_hdmr_eval(cfg.d, cfg.m, parts.f_anchor, slots, x)
     assert rc == 0 and vec.uses_slot_kernel()
     assert np.array_equal(bits(vec.evaluate_batch(x)), bits(want))
