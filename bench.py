@@ -329,6 +329,18 @@ def run_ours(args, rank, world, local_rank, dist):
                 "kernel_ms": kernel_ms, "kernel_share": kernel_ms / ms_per_step,
                 "flops_per_step": flops, "nnz_per_point": nnz_total / n_local,
                 "exact_mode_cap_frac": 0.5}
+    # The resource that binds the slot kernel: every term of
+    # every point needs its own 8-byte surplus word per column in registers,
+    # and the shared-memory pipe delivers 128 B/clk/SM to lanes (16 doubles;
+    # profiles/r1_lds_gather.json) -> 2 * 16 FLOP-equivalents/clk/SM.
+    sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+    mhz = float(clk.get("sm_mhz") or 0.0) or 1965.0
+    smem_peak = 2.0 * 16 * sms * mhz * 1e6 / 1e12
+    roofline["binding_resource"] = {
+        "resource": "shared-memory gather: 16 surplus doubles/clk/SM (LDS pipe, 128 B/clk/SM)",
+        "achieved": achieved, "peak": smem_peak, "unit": "TFLOP/s (2 FLOP per gathered double)",
+        "frac": achieved / smem_peak,
+        "peak_source": "profiles/r1_lds_gather.json microbenchmark x %d SMs x %.0f MHz (median SM clock in the timed region)" % (sms, mhz)}
 
     # e2e through the same API with pinned host buffers
     e2e = None

@@ -244,11 +244,13 @@ bool FastHdmr::build(const HostProgram& hp) {
             H.full = all;
             H.fast_full = 1;
           }
-          // full single-run 1-d blocks, and 2-d blocks of max level 6 (32
-          // candidate rows at level sum 7), use the rotated layout
-          // (conflict-free deep levels, see leaf_full1_rot / leaf_full2_rot);
-          // DDSG_SLOT_ROT=0 disables it
-          if (H.fast_full == 1 && (k == 1 || (k == 2 && nlev == 6)) && runs == 1 && rot_enabled &&
+          // full single-run blocks whose deepest level has >= 32 candidate
+          // rows (1-d max level >= 6, 2-d max level 6: level sum 7) use the
+          // rotated layout (conflict-free deep levels, see leaf_full1_rot /
+          // leaf_full2_rot).  Shallower blocks keep stride 9, conflict-free
+          // up to 16 rows and a 1-wavefront broadcast for level 1, which the
+          // rotation would turn into 2.  DDSG_SLOT_ROT=0 disables it.
+          if (H.fast_full == 1 && nlev >= 6 && runs == 1 && rot_enabled &&
               static_cast<int64_t>(P.rows.size() + 1) * kRotStride * 8 <= kMaxRotBytes)
             H.fast_full = 2;
         }
