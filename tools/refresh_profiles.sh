@@ -13,3 +13,5 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-refine > gpurun_out/ncu_launch.log 2>&1; echo "launch list rc=$?"
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:fast_hdmr_kernel -c 1 \
   -o gpurun_out/prof_final_config5 python tools/profile_run.py 5 447392 1 > gpurun_out/ncu_full.log 2>&1; echo "full capture rc=$?"
+timeout 900 python bench.py --workload euler > gpurun_out/bench_euler.json 2> gpurun_out/bench_euler.err; tail -c 200 gpurun_out/bench_euler.json
+timeout 900 python bench.py --workload jacobian > gpurun_out/bench_jacobian.json 2> gpurun_out/bench_jacobian.err; tail -c 200 gpurun_out/bench_jacobian.json

@@ -24,6 +24,10 @@ def main():
     ref = (OUT / "bench_ref.json").read_text().strip().splitlines()
     if ref:
         (PROF / f"{tag}_bench_reference_arm.json").write_text(ref[-1] + "\n")
+    for wl in ("euler", "jacobian"):
+        f = OUT / f"bench_{wl}.json"
+        if f.exists() and f.read_text().strip():
+            (PROF / f"{tag}_bench_irbc_{wl}_N150.json").write_text(f.read_text().strip().splitlines()[-1] + "\n")
     launches = OUT / "launches.csv"
     if launches.exists():
         (PROF / f"{tag}_launches_config5.csv").write_text(launches.read_text())
