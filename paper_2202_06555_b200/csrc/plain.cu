@@ -57,6 +57,12 @@ struct Params {
   int zero_row;
 };
 
+// Opaque to the compiler: the record words stay in ordinary registers up to
+// this point (see the walk loops).
+__device__ __forceinline__ void pin_record(uint4& r) {
+  asm volatile("" : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w));
+}
+
 template <int kDMax, int kMC, int kExact, int kMode, int kMultiRun>
 __global__ void __launch_bounds__(kThreads, kDMax <= 10 ? 4 : 1) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
                                                          int64_t base, double* __restrict__ y,
@@ -164,10 +170,17 @@ __global__ void __launch_bounds__(kThreads, kDMax <= 10 ? 4 : 1) plain_kernel(Pa
                 : "=d"(sv[c]), "=d"(sv[c + 1]), "=d"(sv[c + 2]), "=d"(sv[c + 3])
                 : "l"(sr + c));
         }
+        // the record loaded one iteration ago: the empty asm keeps it in
+        // ordinary registers until here (otherwise the compiler moves it to
+        // uniform registers right after its load and the warp waits out the
+        // load latency there -- 18 % of all stall samples on config 2)
+        pin_record(ra);
+        if (kDMax > 16) pin_record(rb);
         const uint4 ua = ra, ub = rb;
-        if (s + 2 < n_sub) {
-          ra = __ldg(rec + 2 * (s + 2));
-          if (kDMax > 16) rb = __ldg(rec + 2 * (s + 2) + 1);
+        {  // unconditional (clamped) prefetch: a conditional one is merged through uniform registers
+          const int nx = min(s + 2, n_sub - 1);
+          ra = __ldg(rec + 2 * nx);
+          if (kDMax > 16) rb = __ldg(rec + 2 * nx + 1);
         }
         double w_nxt = 0.0;
         int row_nxt = P.zero_row;
@@ -307,10 +320,13 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_kernel(SparseParams P, 
           asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
               : "=d"(sv[c]), "=d"(sv[c + 1]), "=d"(sv[c + 2]), "=d"(sv[c + 3])
               : "l"(sr + c));
+        pin_record(ra);  // see plain_kernel
+        pin_record(rb);
         const uint4 ua = ra, ub = rb;
-        if (s + 2 < n_sub) {
-          ra = __ldg(rec + 2 * (s + 2));
-          rb = __ldg(rec + 2 * (s + 2) + 1);
+        {  // unconditional (clamped) prefetch, see plain_kernel
+          const int nx = min(s + 2, n_sub - 1);
+          ra = __ldg(rec + 2 * nx);
+          rb = __ldg(rec + 2 * nx + 1);
         }
         double w_nxt = 0.0;
         int row_nxt = P.zero_row;
