@@ -64,7 +64,7 @@ __device__ __forceinline__ void pin_record(uint4& r) {
 }
 
 template <int kDMax, int kMC, int kExact, int kMode, int kMultiRun>
-__global__ void __launch_bounds__(kThreads, kDMax <= 10 ? 4 : 1) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
+__global__ void __launch_bounds__(kThreads, (kMC <= 12 && kDMax <= 10) ? 4 : 1) plain_kernel(Params P, const double* __restrict__ x, int64_t n,
                                                          int64_t base, double* __restrict__ y,
                                                          unsigned long long* bad) {
   const int tid = threadIdx.x;
