@@ -50,8 +50,8 @@ struct Params {
   const int* run_off;  // device array: run r walks records [run_off[r], run_off[r+1])
   const uint4* rec;        // [records][2]: per run, the subspaces holding nodes of that run
   const uint32_t* perm;    // thread p evaluates point perm[p] (Morton order), or p when null
-  const int32_t* slab;     // partial subspaces: cell -> row or -1
-  const int16_t* row_run;  // [rows]
+  const int32_t* slab;     // [runs][slab_len]: cell -> row of that stored-order run, or -1
+  int64_t slab_len;
   const double* surplus;   // [rows + 1][ms] (ms = m rounded up to even: 16-byte rows); row `zero_row` = 0
   int ms;
   int zero_row;
@@ -96,6 +96,9 @@ __global__ void __launch_bounds__(kThreads, (kMC <= 12 && kDMax <= 10) ? 4 : 1) 
 #pragma unroll
     for (int c = 0; c < kMC; ++c) acc[c] = 0.0;
     for (int run = 0; run < (kMultiRun ? P.runs : 1); ++run) {
+      const int32_t* slab_run = P.slab + (kMultiRun ? run * P.slab_len : 0);
+      // sparse_grid.hpp:123: w == 0 terms and absent nodes add nothing (zero row)
+      auto resolve_row = [&](double w, int r) { return (w != 0.0 && r >= 0) ? r : P.zero_row; };
       double pw[kDMax];
       uint32_t pc[kDMax];
 #pragma unroll
@@ -135,22 +138,24 @@ __global__ void __launch_bounds__(kThreads, (kMC <= 12 && kDMax <= 10) ? 4 : 1) 
             break;
         }
         w = pw[kDMax - 1];
-        int r = static_cast<int>(r0.x) + static_cast<int>(pc[kDMax - 1]);
-        if (!((r0.y >> 8) & 1u)) r = __ldg(P.slab + r);
-        bool use = w != 0.0 && r >= 0;  // sparse_grid.hpp:123 (w == 0 skipped), absent node
-        if (kMultiRun) use = use && __ldg(P.row_run + r) == run;
-        row = use ? r : P.zero_row;
+        // full subspace: its row; otherwise this run's slab entry (-1: no
+        // node of the run), resolved by resolve_row() after the current
+        // term's multiply-adds so the lookup's latency is covered
+        row = static_cast<int>(r0.x) + static_cast<int>(pc[kDMax - 1]);
+        if (!((r0.y >> 8) & 1u)) row = __ldg(slab_run + row);
       };
       const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
       const int off0 = __ldg(P.run_off + run), off1 = __ldg(P.run_off + run + 1);
       const uint4* rec = P.rec + 2 * off0;
       const int n_sub = off1 - off0;
       if (n_sub == 0) continue;
+
       // subspace records are prefetched one iteration ahead of their use
       uint4 ra = __ldg(rec), rb = kDMax > 16 ? __ldg(rec + 1) : zero4;
       double w_cur;
       int row_cur;
       term(ra, rb, w_cur, row_cur);
+      row_cur = resolve_row(w_cur, row_cur);
       if (n_sub > 1) {
         ra = __ldg(rec + 2);
         rb = kDMax > 16 ? __ldg(rec + 3) : zero4;
@@ -188,8 +193,8 @@ __global__ void __launch_bounds__(kThreads, (kMC <= 12 && kDMax <= 10) ? 4 : 1) 
 #pragma unroll
         for (int c = 0; c < kMC; ++c)
           acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[c]);
+        row_cur = resolve_row(w_nxt, row_nxt);  // after the multiply-adds: the slab lookup's latency is covered
         w_cur = w_nxt;
-        row_cur = row_nxt;
       }
     }
     const int nc = min(kMC, P.m - c0);
@@ -223,8 +228,8 @@ struct SparseParams {
   const int* run_off;  // device array (a dynamic index into a parameter array would copy it to local memory)
   const uint4* rec;
   const uint32_t* perm;
-  const int32_t* slab;
-  const int16_t* row_run;
+  const int32_t* slab;  // [runs][slab_len], as in Params
+  int64_t slab_len;
   const double* surplus;
 };
 
@@ -254,6 +259,9 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_kernel(SparseParams P, 
 #pragma unroll
     for (int c = 0; c < kMC; ++c) acc[c] = 0.0;
     for (int run = 0; run < (kMultiRun ? P.runs : 1); ++run) {
+      const int32_t* slab_run = P.slab + (kMultiRun ? run * P.slab_len : 0);
+      // sparse_grid.hpp:123: w == 0 terms and absent nodes add nothing (zero row)
+      auto resolve_row = [&](double w, int r) { return (w != 0.0 && r >= 0) ? r : P.zero_row; };
       double pw[kSparseNT];
       uint32_t pc[kSparseNT];
 #pragma unroll
@@ -294,20 +302,19 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_kernel(SparseParams P, 
           default:
             break;
         }
-        int r = static_cast<int>(r0.x) + static_cast<int>(cell);
-        if (!((r0.y >> 8) & 1u)) r = __ldg(P.slab + r);
-        bool use = w != 0.0 && r >= 0;  // sparse_grid.hpp:123 (w == 0 skipped), absent node
-        if (kMultiRun) use = use && __ldg(P.row_run + r) == run;
-        row = use ? r : P.zero_row;
+        row = static_cast<int>(r0.x) + static_cast<int>(cell);  // see plain_kernel
+        if (!((r0.y >> 8) & 1u)) row = __ldg(slab_run + row);
       };
       const int off0 = __ldg(P.run_off + run), off1 = __ldg(P.run_off + run + 1);
       const uint4* rec = P.rec + 2 * off0;
       const int n_sub = off1 - off0;
       if (n_sub == 0) continue;
+
       uint4 ra = __ldg(rec), rb = __ldg(rec + 1);
       double w_cur;
       int row_cur;
       term(ra, rb, w_cur, row_cur);
+      row_cur = resolve_row(w_cur, row_cur);
       if (n_sub > 1) {
         ra = __ldg(rec + 2);
         rb = __ldg(rec + 3);
@@ -334,8 +341,8 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_kernel(SparseParams P, 
 #pragma unroll
         for (int c = 0; c < kMC; ++c)
           acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[c]);
+        row_cur = resolve_row(w_nxt, row_nxt);  // after the multiply-adds: the slab lookup's latency is covered
         w_cur = w_nxt;
-        row_cur = row_nxt;
       }
     }
     const int nc = min(kMC, P.m - c0);
@@ -412,7 +419,9 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
       if (prev)
         while (qq < d && prev[qq] == lv[qq]) ++qq;
       prev = lv;
-      const bool is_full = hp.sub_nodes[s] == cells;
+      // several stored-order runs: every term goes through the run's slab
+      // (a complete subspace may hold nodes of several runs)
+      const bool is_full = hp.sub_nodes[s] == cells && runs == 1;
       uint32_t r[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
       r[0] = static_cast<uint32_t>(is_full ? hp.slab[slab_off] : slab_off);
       r[1] = static_cast<uint32_t>(qq) | (is_full ? 0x100u : 0u);
@@ -438,8 +447,20 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   for (int64_t r = 0; r < hp.rows; ++r)
     std::copy(hp.surplus.begin() + r * hp.m, hp.surplus.begin() + (r + 1) * hp.m, pad.begin() + r * ms_);
   surplus_ = put(pad);
-  slab_ = dev.slab;
-  row_run_ = dev.row_run;
+  // per-run slabs: run r's copy keeps only the rows of run r (-1 elsewhere),
+  // so a term needs one lookup, not a slab and a row_run lookup
+  slab_len_ = static_cast<int64_t>(hp.slab.size());
+  if (runs == 1) {
+    slab_ = dev.slab;
+  } else {
+    std::vector<int32_t> sr(static_cast<size_t>(slab_len_) * runs);
+    for (int run = 0; run < runs; ++run)
+      for (int64_t c = 0; c < slab_len_; ++c) {
+        const int32_t row = hp.slab[c];
+        sr[run * slab_len_ + c] = (row >= 0 && hp.row_run[row] == run) ? row : -1;
+      }
+    slab_ = put(sr);
+  }
   usable_ = true;
   build_sparse(hp);
   sort_ = d >= kSortMinDim;
@@ -488,7 +509,7 @@ bool PlainGrid::build_sparse(const HostProgram& hp) {
       int qs = 0;  // non-trivial pairs below qq are unchanged
       for (int j = 0; j < qq; ++j) qs += lv[j] > 1;
       if (nt > 0) qs = std::min(qs, nt - 1);  // recompute >= 1 pair: the last one yields w
-      const bool is_full = hp.sub_nodes[s] == cells;
+      const bool is_full = hp.sub_nodes[s] == cells && runs == 1;  // see build()
       uint32_t r[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
       r[0] = static_cast<uint32_t>(is_full ? hp.slab[slab_off] : slab_off);
       r[1] = static_cast<uint32_t>(qs) | (static_cast<uint32_t>(nt) << 4) | (is_full ? 0x100u : 0u);
@@ -622,7 +643,7 @@ int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, d
     S.rec = srec_;
     S.perm = perm;
     S.slab = slab_;
-    S.row_run = row_run_;
+    S.slab_len = slab_len_;
     S.surplus = surplus_;
     const unsigned grid = static_cast<unsigned>((n + kSparseThreads - 1) / kSparseThreads);
     const size_t smem = static_cast<size_t>(d_) * kSparseThreads * 12;
@@ -640,7 +661,7 @@ int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, d
   P.run_off = run_off_dev_;
   P.rec = rec_;
   P.slab = slab_;
-  P.row_run = row_run_;
+  P.slab_len = slab_len_;
   P.surplus = surplus_;
   P.ms = ms_;
   P.zero_row = zero_row_;

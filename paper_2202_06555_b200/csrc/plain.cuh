@@ -83,8 +83,8 @@ class PlainGrid {
   std::vector<int> run_off_;
   const int* run_off_dev_ = nullptr;
   const uint4* rec_ = nullptr;  // [n_sub][2] packed subspace records
-  const int32_t* slab_ = nullptr;
-  const int16_t* row_run_ = nullptr;
+  const int32_t* slab_ = nullptr;  // [runs][slab_len_] per-run slabs (the program's slab when 1 run)
+  int64_t slab_len_ = 0;
   const double* surplus_ = nullptr;
   std::vector<void*> allocs_;
   template <typename T>
