@@ -152,3 +152,19 @@ def test_sorted_device_buffers_and_permutation_invariance(config2):
     yd = torch.empty((len(x), config2.out_dim), dtype=torch.float64, device="cuda")
     gt.interpolate(xd, out=yd)
     assert np.array_equal(bits(yd.cpu().numpy()), bits(y[p]))
+
+
+@pytest.mark.timeout(900)
+def test_config3_level6_grid_exact():
+    """Config 3's target refined to level 6 (1,262,721 nodes, 238 MB of
+    surpluses; the reference's O(N^2) build cannot reach it, ours replays it
+    in about 30 s): the Morton-sorted sparse walk against the oracle."""
+    import dataclasses
+
+    cfg = dataclasses.replace(W.CONFIGS[3], max_level=6)
+    g = W.build_grid(cfg)
+    assert g.size() == 1262721
+    x = W.points(cfg, n=8192, seed=6)
+    y = _eval_sorted(g, x)
+    sel = np.r_[0:24, 8192 - 8:8192]
+    assert np.array_equal(bits(y[sel]), bits(_oracle(g, x[sel])))
