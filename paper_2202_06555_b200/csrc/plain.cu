@@ -234,7 +234,7 @@ struct SparseParams {
 };
 
 template <int kMC, int kExact, int kMultiRun>
-__global__ void __launch_bounds__(kSparseThreads) sparse_kernel(SparseParams P, const double* __restrict__ x,
+__global__ void __launch_bounds__(kSparseThreads, kMC % 8 == 0 ? 4 : 1) sparse_kernel(SparseParams P, const double* __restrict__ x,
                                                                 int64_t n, int64_t base, double* __restrict__ y,
                                                                 unsigned long long* bad) {
   extern __shared__ double xs[];  // [d][kSparseThreads] coordinates, then [d][kSparseThreads] fixed point
@@ -319,14 +319,22 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_kernel(SparseParams P, 
         ra = __ldg(rec + 2);
         rb = __ldg(rec + 3);
       }
-      for (int s = 0; s < n_sub; ++s) {
-        double sv[kMC];
-        const double* sr = P.surplus + static_cast<int64_t>(row_cur) * P.ms + c0;
+      // The row is loaded in two halves: the first flies while the next
+      // term's weight is formed, the second after the first half is
+      // accumulated, so only half a row of registers is in flight (config 3:
+      // 24 columns, 128 registers, 16 warps per SM instead of 12).
+      constexpr int kH = kMC % 8 == 0 ? kMC / 2 : kMC;  // halves of whole 32-byte loads, else no split
+      auto load_half = [&](const double* sr, double (&sv)[kH]) {
 #pragma unroll
-        for (int c = 0; c < kMC; c += 4)
+        for (int c = 0; c < kH; c += 4)
           asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
               : "=d"(sv[c]), "=d"(sv[c + 1]), "=d"(sv[c + 2]), "=d"(sv[c + 3])
               : "l"(sr + c));
+      };
+      for (int s = 0; s < n_sub; ++s) {
+        double sv[kH];
+        const double* sr = P.surplus + static_cast<int64_t>(row_cur) * P.ms + c0;
+        load_half(sr, sv);
         pin_record(ra);  // see plain_kernel
         pin_record(rb);
         const uint4 ua = ra, ub = rb;
@@ -339,9 +347,18 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_kernel(SparseParams P, 
         int row_nxt = P.zero_row;
         if (s + 1 < n_sub) term(ua, ub, w_nxt, row_nxt);
 #pragma unroll
-        for (int c = 0; c < kMC; ++c)
+        for (int c = 0; c < kH; ++c)
           acc[c] = kExact ? __dadd_rn(acc[c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[c]);
+        if (kH < kMC) load_half(sr + (kH < kMC ? kH : 0), sv);
         row_cur = resolve_row(w_nxt, row_nxt);  // after the multiply-adds: the slab lookup's latency is covered
+        if (kH < kMC) {
+#pragma unroll
+          for (int c = 0; c < kH; ++c) {
+            constexpr int kOff = kH < kMC ? kH : 0;
+            acc[kOff + c] =
+                kExact ? __dadd_rn(acc[kOff + c], __dmul_rn(w_cur, sv[c])) : __fma_rn(w_cur, sv[c], acc[kOff + c]);
+          }
+        }
         w_cur = w_nxt;
       }
     }
