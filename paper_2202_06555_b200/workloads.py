@@ -127,6 +127,22 @@ def build_hdmr_parts(cfg: Config) -> HdmrParts:
     return parts
 
 
+class GridTarget:
+    """A plain-grid config's target (configs 1-3) as a numpy batch function
+    xs[n][d] -> values[n][m] (the C evaluator the builds use)."""
+
+    def __init__(self, cfg: Config):
+        self.cfg = cfg
+        self._fn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)(N.wl_fn(cfg.target))
+
+    def __call__(self, xs: np.ndarray) -> np.ndarray:
+        xs = np.ascontiguousarray(xs, dtype=np.float64).reshape(-1, self.cfg.d)
+        out = np.empty((xs.shape[0], self.cfg.m))
+        if xs.shape[0] and self._fn(xs.ctypes.data, xs.shape[0], out.ctypes.data, None) != 0:
+            raise RuntimeError(f"{self.cfg.target} failed")
+        return out
+
+
 class CutTarget:
     """The config target restricted to the cut through the center anchor along
     `dims` (hdmr.hpp:248-259), as a C evaluator (address + ctx) and a numpy
@@ -139,6 +155,8 @@ class CutTarget:
         self._anchor = np.full(cfg.d, 0.5)
         self.ctx = wl.wl_cut_new(N.wl_fn(cfg.target), None, cfg.d, cfg.m, len(dims), self._dims.ctypes.data,
                                  self._anchor.ctypes.data)
+        if not self.ctx:
+            raise ValueError(f"cut of {len(dims)} dims not supported (1..16)")
         self.addr = N.wl_fn("wl_cut_eval")
         self._fn = wl.wl_cut_eval
         self._fn.restype = C.c_int

@@ -106,3 +106,32 @@ def test_refine_step_gpu_hierarchize_equals_next_level_build():
         k2, s2 = h.nodes()
         assert np.array_equal(k1, k2)
         assert np.array_equal(bits(s1), bits(s2))
+
+
+def _config3_step(level: int, device: bool):
+    """Config 3 (d = 20, adaptive, 2 stored-order runs at level 5) refined from
+    `level` to `level + 1` by one refine_step: the reference's build caps the
+    level sum at max_level + d - 1, so the next level is exactly one more
+    batch (sparse_grid.hpp:84-108)."""
+    import dataclasses
+
+    lo = dataclasses.replace(W.CONFIGS[3], max_level=level)
+    hi = dataclasses.replace(W.CONFIGS[3], max_level=level + 1)
+    g = W.build_grid(lo)
+    f = W.GridTarget(lo)
+    stats = refine_step([g], [lo.max_level + lo.d - 1], lambda gi, xs: f(xs), dist=None, device=device)
+    h = W.build_grid(hi)
+    k1, s1 = g.nodes()
+    k2, s2 = h.nodes()
+    assert stats.new_nodes == h.size() - W.build_grid(lo).size() > 0
+    assert np.array_equal(k1, k2)
+    assert np.array_equal(bits(s1), bits(s2))
+
+
+def test_refine_step_plain_grid_d20_host():
+    _config3_step(3, device=False)
+
+
+@pytest.mark.gpu
+def test_refine_step_plain_grid_d20_gpu_hierarchize():
+    _config3_step(4, device=True)
