@@ -3,6 +3,8 @@
 // round exactly like the reference's Release build (mul then add, no FMA).
 #include "grid_host.hpp"
 
+#include <cstring>
+
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -48,17 +50,96 @@ static int level_sum_of(const uint32_t* key, int dim) {
   return s;
 }
 
+static inline uint64_t key_hash(const uint32_t* k, int dim) {
+  uint64_t h = 0xcbf29ce484222325ull;  // FNV-1a (grid_index.hpp:60-69)
+  for (int j = 0; j < dim; ++j) {
+    h ^= k[j];
+    h *= 0x100000001b3ull;
+  }
+  return h ^ (h >> 29);
+}
+
+// Flat open-addressing set of dim-word keys stored in an arena (next_candidates).
+namespace {
+struct KeySet {
+  int dim;
+  std::vector<uint32_t> arena;
+  std::vector<int64_t> table = std::vector<int64_t>(1024, -1);
+  int64_t n = 0;
+  explicit KeySet(int d) : dim(d) {}
+  bool contains(const uint32_t* k) const {
+    const uint64_t mask = table.size() - 1;
+    for (uint64_t h = key_hash(k, dim) & mask;; h = (h + 1) & mask) {
+      const int64_t id = table[h];
+      if (id < 0) return false;
+      if (std::memcmp(&arena[id * dim], k, sizeof(uint32_t) * dim) == 0) return true;
+    }
+  }
+  bool insert(const uint32_t* k) {  // false if present
+    if ((n + 1) * 2 > static_cast<int64_t>(table.size())) grow();
+    const uint64_t mask = table.size() - 1;
+    uint64_t h = key_hash(k, dim) & mask;
+    for (;; h = (h + 1) & mask) {
+      const int64_t id = table[h];
+      if (id < 0) break;
+      if (std::memcmp(&arena[id * dim], k, sizeof(uint32_t) * dim) == 0) return false;
+    }
+    arena.insert(arena.end(), k, k + dim);
+    table[h] = n++;
+    return true;
+  }
+  void grow() {
+    std::vector<int64_t> t(table.size() * 2, -1);
+    const uint64_t mask = t.size() - 1;
+    for (int64_t id = 0; id < n; ++id) {
+      uint64_t h = key_hash(&arena[id * dim], dim) & mask;
+      while (t[h] >= 0) h = (h + 1) & mask;
+      t[h] = id;
+    }
+    table.swap(t);
+  }
+};
+}  // namespace
+
+void HostGrid::rebuild_index(int64_t n_nodes) {
+  size_t cap = 1024;
+  while (cap < static_cast<size_t>(n_nodes) * 2) cap *= 2;
+  table_.assign(cap, -1);
+  indexed_ = 0;
+  for (int64_t i = 0; i < n_nodes; ++i) index_node(i);
+}
+
 void HostGrid::index_node(int64_t i) {
-  std::vector<uint32_t> k(keys.begin() + i * dim, keys.begin() + (i + 1) * dim);
-  if (!lookup_.emplace(std::move(k), i).second)
-    fail(DDSG_INVALID_ARGUMENT, "sparse grid: duplicate node key");
+  if ((indexed_ + 1) * 2 > static_cast<int64_t>(table_.size())) {
+    const int64_t n = indexed_;
+    size_t cap = std::max<size_t>(1024, table_.size() * 2);
+    table_.assign(cap, -1);
+    indexed_ = 0;
+    for (int64_t r = 0; r < n; ++r) index_node(r);
+  }
+  const uint32_t* k = &keys[i * dim];
+  const uint64_t mask = table_.size() - 1;
+  uint64_t h = key_hash(k, dim) & mask;
+  for (;; h = (h + 1) & mask) {
+    const int64_t id = table_[h];
+    if (id < 0) break;
+    if (std::memcmp(&keys[id * dim], k, sizeof(uint32_t) * dim) == 0)
+      fail(DDSG_INVALID_ARGUMENT, "sparse grid: duplicate node key");
+  }
+  table_[h] = i;
+  ++indexed_;
 }
 
 bool HostGrid::contains(const uint32_t* key) const { return find(key) >= 0; }
 
 int64_t HostGrid::find(const uint32_t* key) const {
-  auto it = lookup_.find(std::vector<uint32_t>(key, key + dim));
-  return it == lookup_.end() ? -1 : it->second;
+  if (table_.empty()) return -1;
+  const uint64_t mask = table_.size() - 1;
+  for (uint64_t h = key_hash(key, dim) & mask;; h = (h + 1) & mask) {
+    const int64_t id = table_[h];
+    if (id < 0) return -1;
+    if (std::memcmp(&keys[id * dim], key, sizeof(uint32_t) * dim) == 0) return id;
+  }
 }
 
 static void validate_keys(int dim, int64_t n, const uint32_t* keys) {
@@ -85,8 +166,7 @@ HostGrid HostGrid::from_nodes(int dim, int m, int mode, int max_level, double ep
   g.eps_gamma = eps_gamma;
   g.keys.assign(keys, keys + n * dim);
   g.surplus.assign(surplus, surplus + n * m);
-  g.lookup_.reserve(static_cast<size_t>(n) * 2);
-  for (int64_t i = 0; i < n; ++i) g.index_node(i);
+  g.rebuild_index(n);
   return g;
 }
 
@@ -101,11 +181,9 @@ void HostGrid::append(int64_t n, const uint32_t* k, const double* s) {
       index_node(base + i);
     } catch (...) {
       // roll back so the grid stays consistent
-      for (int64_t r = 0; r < i; ++r)
-        lookup_.erase(std::vector<uint32_t>(keys.begin() + (base + r) * dim,
-                                            keys.begin() + (base + r + 1) * dim));
       keys.resize(base * dim);
       surplus.resize(base * m);
+      rebuild_index(base);
       throw;
     }
   }
@@ -182,23 +260,21 @@ void HostGrid::interpolate_at_node(const uint32_t* key, int64_t upto, double* ou
 
 std::vector<std::vector<uint32_t>> HostGrid::next_candidates(int s, std::vector<char>& refined) {
   // sparse_grid.hpp:215-254.
-  std::unordered_set<std::vector<uint32_t>, VecHash> seen;
-  std::vector<std::vector<uint32_t>> out;
-  auto have = [&](const std::vector<uint32_t>& k) { return contains(k.data()) || seen.count(k); };
-  auto push_missing_ancestors = [&](const std::vector<uint32_t>& key) {
-    std::vector<std::vector<uint32_t>> stack{key};
+  KeySet seen(dim);  // the candidates, flat in generation order (arena) and indexed
+  std::vector<uint32_t> stack, p(dim), c(dim);  // ancestor walk, dim words per entry
+  auto push_missing_ancestors = [&](const uint32_t* key) {
+    stack.assign(key, key + dim);
     while (!stack.empty()) {
-      std::vector<uint32_t> cur = std::move(stack.back());
-      stack.pop_back();
+      const size_t top = stack.size() - dim;
       for (int j = 0; j < dim; ++j) {
-        if (cur[j] <= 1u) continue;
-        std::vector<uint32_t> p = cur;
-        p[j] = cur[j] >> 1;
-        if (have(p)) continue;
-        seen.insert(p);
-        out.push_back(p);
-        stack.push_back(std::move(p));
+        if (stack[top + j] <= 1u) continue;
+        std::copy(stack.begin() + top, stack.begin() + top + dim, p.begin());
+        p[j] >>= 1;
+        if (contains(p.data()) || !seen.insert(p.data())) continue;
+        stack.insert(stack.end(), p.begin(), p.end());  // walked after this entry's dims
       }
+      // drop the entry just expanded (its pushed parents sit above it)
+      stack.erase(stack.begin() + top, stack.begin() + top + dim);
     }
   };
   const int64_t n = size();
@@ -210,9 +286,9 @@ std::vector<std::vector<uint32_t>> HostGrid::next_candidates(int s, std::vector<
       double g = 0.0;
       const double* sp = &surplus[i * m];
       if (norm == DDSG_NORM_INF) {
-        for (int c = 0; c < m; ++c) g = std::max(g, std::abs(sp[c]));
+        for (int cc = 0; cc < m; ++cc) g = std::max(g, std::abs(sp[cc]));
       } else {
-        for (int c = 0; c < m; ++c) g += sp[c] * sp[c];
+        for (int cc = 0; cc < m; ++cc) g += sp[cc] * sp[cc];
         g = std::sqrt(g);
       }
       significant = g > eps_gamma;
@@ -221,19 +297,27 @@ std::vector<std::vector<uint32_t>> HostGrid::next_candidates(int s, std::vector<
     refined[i] = 1;
     for (int j = 0; j < dim; ++j) {
       for (uint32_t child : {key[j] * 2u, key[j] * 2u + 1u}) {
-        std::vector<uint32_t> c(key, key + dim);
+        std::copy(key, key + dim, c.begin());
         c[j] = child;
-        if (contains(c.data()) || !seen.insert(c).second) continue;
-        out.push_back(c);
-        push_missing_ancestors(c);
+        if (contains(c.data()) || !seen.insert(c.data())) continue;
+        push_missing_ancestors(c.data());
       }
     }
   }
-  std::sort(out.begin(), out.end(), [&](const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
-    const int sa = level_sum_of(a.data(), dim), sb = level_sum_of(b.data(), dim);
-    if (sa != sb) return sa < sb;
-    return a < b;
+  // batch order: (level sum, key lexicographic) -- a total order, so the
+  // generation order above does not matter
+  const int64_t nc = seen.n;
+  const uint32_t* ar = seen.arena.data();
+  std::vector<int> ls(nc);
+  for (int64_t i = 0; i < nc; ++i) ls[i] = level_sum_of(ar + i * dim, dim);
+  std::vector<int64_t> ord(nc);
+  std::iota(ord.begin(), ord.end(), int64_t{0});
+  std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+    if (ls[a] != ls[b]) return ls[a] < ls[b];
+    return std::lexicographical_compare(ar + a * dim, ar + (a + 1) * dim, ar + b * dim, ar + (b + 1) * dim);
   });
+  std::vector<std::vector<uint32_t>> out(nc);
+  for (int64_t i = 0; i < nc; ++i) out[i].assign(ar + ord[i] * dim, ar + (ord[i] + 1) * dim);
   return out;
 }
 

@@ -80,18 +80,13 @@ class HostGrid {
   void interpolate_at_node(const uint32_t* key, int64_t upto, double* out) const;
 
  private:
-  struct VecHash {
-    size_t operator()(const std::vector<uint32_t>& k) const noexcept {
-      size_t h = 0xcbf29ce484222325ull;  // FNV-1a as NodeKeyHash (grid_index.hpp:60-69)
-      for (uint32_t v : k) {
-        h ^= v;
-        h *= 0x100000001b3ull;
-      }
-      return h;
-    }
-  };
-  std::unordered_map<std::vector<uint32_t>, int64_t, VecHash> lookup_;
+  // Node index: open-addressing table of node ids over the flat `keys`
+  // array (FNV-1a over the dim words, as NodeKeyHash, grid_index.hpp:60-69);
+  // no allocation per lookup.
+  std::vector<int64_t> table_;  // -1 = empty; size a power of two, load <= 1/2
+  int64_t indexed_ = 0;
   void index_node(int64_t i);
+  void rebuild_index(int64_t n_nodes);
   std::vector<std::vector<uint32_t>> next_candidates(int s, std::vector<char>& refined);
   void insert_batch(const std::vector<std::vector<uint32_t>>& batch, const BatchEval& f);
 };
