@@ -69,3 +69,7 @@ def test_bench_default_line_on_gpu():
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     rf = d["roofline"]
     assert rf["bound"] in ("fp64", "hbm", "tensor") and 0 < rf["frac"] < 1 and rf["peak"] > 0
+    # the resource that binds the slot kernel: the shared-memory gather ceiling
+    br = rf["binding_resource"]
+    assert 0 < br["frac"] < 1 and br["peak"] > 0 and abs(br["achieved"] - rf["achieved"]) < 1e-9
+    assert br["peak"] < rf["peak"]  # 16 doubles/clk/SM is below the DFMA rate
