@@ -342,9 +342,10 @@ def run_ours(args, rank, world, local_rank, dist):
         except Exception:
             hbm_tbs = 6.55  # B200_PROFILING.md fallback
         roofline["traffic_note"] = (
-            "DRAM traffic is %.1fx the algorithmic bytes (L2 misses when point tiles re-stage the slot tables and "
-            "re-read their points) at %.2f TB/s of %.2f; the kernel is not HBM-bound: its time is flat while a "
-            "column-block grouping sweep varies DRAM reads 2.7x (profiles/r1_l2_budget_sweep_config5.json)"
+            "DRAM traffic is %.1fx the algorithmic bytes (mostly L2 misses on point coordinates: a CTA re-reads "
+            "each dim's coordinates for the ~2.7 slots that use it, and the tiles in flight hold 178 MB of them) at "
+            "%.2f TB/s of %.2f; the kernel is not HBM-bound: its time is flat while column-block grouping and L2 "
+            "persisting windows vary DRAM reads 2.7x (profiles/r1_l2_budget_sweep_config5.json)"
             % (traffic / alg_bytes, traffic / (kernel_ms / 1e3) / 1e12, hbm_tbs))
     roofline["binding_resource"] = {
         "resource": "shared-memory gather: 16 surplus doubles/clk/SM (LDS pipe, 128 B/clk/SM)",
