@@ -313,6 +313,10 @@ __device__ __forceinline__ void leaf_full1(const unsigned char* table, double x,
   }
 }
 
+__device__ __forceinline__ void lds_f64x2(uint32_t addr, double& a, double& b) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr));
+}
+
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
@@ -320,26 +324,29 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
 }
 
 // Full order-1 slot in the rotated layout (fast_full == 2): rows of 16
-// doubles holding the 8 columns twice (bank pairs 0-7 and 8-15).  Lane l
-// reads copy (l >> 3) & 1 and, at step j, column (l & 7) ^ j into slot j, so
-// the 16 lanes of a half-warp hit 16 distinct bank pairs whatever their rows:
-// the deep levels' 32-128 candidate rows cost 2 wavefronts per warp load
-// instead of 3.9-5.5 (profiles/r1_lds_rotate.json).  The slot starts from a
-// zero accumulator (rotation-free) and un-rotates it once at the end
-// (3 conditional swap stages).  q0 = shared address of row 0 | lane bits.
-// Rotated layout: accumulator slot j holds column c0 ^ j (c0 = this lane's
-// rotation, bits 3-5 of q0); swap back in three conditional stages.
+// doubles holding the 8 columns twice (two 64-byte copies).  Lane l reads
+// copy (l >> 2) & 1 and, at step j, column pair (l & 3) ^ j into slot pair j
+// with one LDS.128, so the 8 lanes of a quarter-warp hit the row's 8
+// distinct 16-byte units whatever their rows: the deep levels' 32-128
+// candidate rows cost 2 wavefronts per column instead of 3.9-5.5
+// (profiles/r1_lds_rotate.json).  The slot starts from a zero accumulator
+// (rotation-free) and un-rotates it once at the end.  q0 = shared address of
+// row 0 | lane bits.
 __device__ __forceinline__ void unrotate(uint32_t q0, double (&acc)[kCols]) {
-  const uint32_t c0 = (q0 >> 3) & 7u;
+  // slot pair j holds column pair p0 ^ j (p0 = this lane's rotation, bits 4-5 of q0)
+  const uint32_t p0 = (q0 >> 4) & 3u;
 #pragma unroll
-  for (int b = 1; b < kCols; b <<= 1) {
-    const bool flip = (c0 & static_cast<uint32_t>(b)) != 0u;
+  for (int b = 1; b < kCols / 2; b <<= 1) {
+    const bool flip = (p0 & static_cast<uint32_t>(b)) != 0u;
 #pragma unroll
-    for (int c = 0; c < kCols; ++c)
-      if (!(c & b)) {
-        const double lo = acc[c], hi = acc[c | b];
-        acc[c] = flip ? hi : lo;
-        acc[c | b] = flip ? lo : hi;
+    for (int j = 0; j < kCols / 2; ++j)
+      if (!(j & b)) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double lo = acc[2 * j + h], hi = acc[2 * (j | b) + h];
+          acc[2 * j + h] = flip ? hi : lo;
+          acc[2 * (j | b) + h] = flip ? lo : hi;
+        }
       }
   }
 }
@@ -366,12 +373,14 @@ __device__ __forceinline__ void leaf_full1_rot(uint32_t q0, double x, double (&a
   }
   double buf[2][kCols];  // static ping-pong: term i+1 loads while term i accumulates
 #pragma unroll
-  for (int j = 0; j < kCols; ++j) buf[0][j] = lds_f64(row[0] ^ static_cast<uint32_t>(j << 3));
+  for (int j = 0; j < kCols / 2; ++j)
+    lds_f64x2(row[0] ^ static_cast<uint32_t>(j << 4), buf[0][2 * j], buf[0][2 * j + 1]);
 #pragma unroll
   for (int i = 0; i < L; ++i) {
     if (i + 1 < L) {
 #pragma unroll
-      for (int j = 0; j < kCols; ++j) buf[(i + 1) & 1][j] = lds_f64(row[i + 1] ^ static_cast<uint32_t>(j << 3));
+      for (int j = 0; j < kCols / 2; ++j)
+        lds_f64x2(row[i + 1] ^ static_cast<uint32_t>(j << 4), buf[(i + 1) & 1][2 * j], buf[(i + 1) & 1][2 * j + 1]);
     }
     fma_row<kExact>(acc, w[i], buf[i & 1]);
   }
@@ -480,14 +489,16 @@ __device__ __forceinline__ void leaf_full2_rot(uint32_t q0, double x0, double x1
   term(0, wb[0], ab[0]);
   double buf[2][kCols];  // static ping-pong
 #pragma unroll
-  for (int j = 0; j < kCols; ++j) buf[0][j] = lds_f64(ab[0] ^ static_cast<uint32_t>(j << 3));
+  for (int j = 0; j < kCols / 2; ++j)
+    lds_f64x2(ab[0] ^ static_cast<uint32_t>(j << 4), buf[0][2 * j], buf[0][2 * j + 1]);
 #pragma unroll
   for (int i = 0; i < kN; ++i) {
     if (i + 1 < kN) {
       term(i + 1, wb[(i + 1) & 1], ab[(i + 1) & 1]);
 #pragma unroll
-      for (int j = 0; j < kCols; ++j)
-        buf[(i + 1) & 1][j] = lds_f64(ab[(i + 1) & 1] ^ static_cast<uint32_t>(j << 3));
+      for (int j = 0; j < kCols / 2; ++j)
+        lds_f64x2(ab[(i + 1) & 1] ^ static_cast<uint32_t>(j << 4), buf[(i + 1) & 1][2 * j],
+                  buf[(i + 1) & 1][2 * j + 1]);
     }
     fma_row<kExact>(acc, wb[i & 1], buf[i & 1]);
   }
@@ -641,8 +652,10 @@ __global__ void __launch_bounds__(kPoints, 1)
   const int cb = grp * cb_group + static_cast<int>(rem - tile * gsize);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  // rotated-layout blocks: this lane's table copy (bit 6) and column rotation (bits 3-5)
-  const uint32_t lanebits = static_cast<uint32_t>((((tid >> 3) & 1) << 6) | ((tid & 7) << 3));
+  // rotated-layout lane bits: copy (bit 6) = (lane >> 2) & 1, column-pair
+  // rotation (bits 4-5) = lane & 3 -- the 8 lanes of a quarter-warp hit the 8
+  // distinct 16-byte units of a 128-byte row in every LDS.128
+  const uint32_t lanebits = static_cast<uint32_t>((((tid >> 2) & 1) << 6) | ((tid & 3) << 4));
   const int64_t p = static_cast<int64_t>(tile) * kPoints + tid;
   const bool valid = p < n;
   const int64_t pc = valid ? p : n - 1;
