@@ -323,15 +323,7 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   return v;
 }
 
-// Full order-1 slot in the rotated layout (fast_full == 2): rows of 16
-// doubles holding the 8 columns twice (two 64-byte copies).  Lane l reads
-// copy (l >> 2) & 1 and, at step j, column pair (l & 3) ^ j into slot pair j
-// with one LDS.128, so the 8 lanes of a quarter-warp hit the row's 8
-// distinct 16-byte units whatever their rows: the deep levels' 32-128
-// candidate rows cost 2 wavefronts per column instead of 3.9-5.5
-// (profiles/r1_lds_rotate.json).  The slot starts from a zero accumulator
-// (rotation-free) and un-rotates it once at the end.  q0 = shared address of
-// row 0 | lane bits.
+// Rotated layout: un-rotate an accumulator (see leaf_full1_rot).
 __device__ __forceinline__ void unrotate(uint32_t q0, double (&acc)[kCols]) {
   // slot pair j holds column pair p0 ^ j (p0 = this lane's rotation, bits 4-5 of q0)
   const uint32_t p0 = (q0 >> 4) & 3u;
@@ -351,6 +343,15 @@ __device__ __forceinline__ void unrotate(uint32_t q0, double (&acc)[kCols]) {
   }
 }
 
+// Full order-1 slot in the rotated layout (fast_full == 2): rows of 16
+// doubles holding the 8 columns twice (two 64-byte copies).  Lane l reads
+// copy (l >> 2) & 1 and, at step j, column pair (l & 3) ^ j into slot pair j
+// with one LDS.128, so the 8 lanes of a quarter-warp hit the row's 8
+// distinct 16-byte units whatever their rows: the deep levels' 32-128
+// candidate rows cost 2 wavefronts per column instead of 3.9-5.5
+// (profiles/r1_lds_rotate.json).  The slot starts from a zero accumulator
+// (rotation-free) and un-rotates it once at the end.  q0 = shared address of
+// row 0 | lane bits.
 template <int kExact, int kMode, int L>
 __device__ __forceinline__ void leaf_full1_rot(uint32_t q0, double x, double (&acc)[kCols]) {
   double w[L];
