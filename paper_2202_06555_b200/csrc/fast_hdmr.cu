@@ -123,6 +123,10 @@ bool FastHdmr::build(const HostProgram& hp) {
     const char* e = std::getenv("DDSG_SLOT_ROT");
     return !(e && std::atoi(e) == 0);
   }();
+  const int rot_min_level = [] {  // shallowest max level that takes the rotated layout
+    const char* e = std::getenv("DDSG_SLOT_ROT_MIN");
+    return e ? std::max(2, std::atoi(e)) : 6;
+  }();
   std::vector<SlotPlan> plans;
   std::vector<int16_t> dims16;
   int64_t max_bytes = 0;
@@ -250,7 +254,7 @@ bool FastHdmr::build(const HostProgram& hp) {
           // leaf_full2_rot).  Shallower blocks keep stride 9, conflict-free
           // up to 16 rows and a 1-wavefront broadcast for level 1, which the
           // rotation would turn into 2.  DDSG_SLOT_ROT=0 disables it.
-          if (H.fast_full == 1 && nlev >= 6 && runs == 1 && rot_enabled &&
+          if (H.fast_full == 1 && nlev >= rot_min_level && runs == 1 && rot_enabled &&
               static_cast<int64_t>(P.rows.size() + 1) * kRotStride * 8 <= kMaxRotBytes)
             H.fast_full = 2;
         }

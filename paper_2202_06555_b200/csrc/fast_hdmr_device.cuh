@@ -530,11 +530,17 @@ __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHe
   if (Hc.fast_full == 2) {
     const uint32_t q0 = smem_u32(table) | lanebits;
     if (Hc.k == 2) {
-      if (Hc.mode == 1)
-        leaf_full2_rot<kExact, 1, 6>(q0, x0, x1, acc);
-      else
-        leaf_full2_rot<kExact, 0, 6>(q0, x0, x1, acc);
-      return;
+      switch (Hc.mode * 16 + Hc.nlev) {
+#define DDSG_R2(MD, LV) \
+  case MD * 16 + LV: \
+    leaf_full2_rot<kExact, MD, LV>(q0, x0, x1, acc); \
+    return;
+        DDSG_R2(0, 2) DDSG_R2(0, 3) DDSG_R2(0, 4) DDSG_R2(0, 5) DDSG_R2(0, 6)
+        DDSG_R2(1, 2) DDSG_R2(1, 3) DDSG_R2(1, 4) DDSG_R2(1, 5) DDSG_R2(1, 6)
+#undef DDSG_R2
+        default:
+          return;
+      }
     }
     switch (Hc.mode * 16 + Hc.nlev) {
 #define DDSG_R1(MD, LV) \
