@@ -334,7 +334,7 @@ def run_ours(args, rank, world, local_rank, dist):
     # and the shared-memory pipe delivers 128 B/clk/SM to lanes (16 doubles;
     # profiles/r1_lds_gather.json) -> 2 * 16 FLOP-equivalents/clk/SM.
     sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
-    mhz = float(clk.get("sm_mhz") or 0.0) or 1965.0
+    mhz = float((clk or {}).get("sm_mhz") or 0.0) or 1965.0  # no samples in a very short timed region
     smem_peak = 2.0 * 16 * sms * mhz * 1e6 / 1e12
     if traffic:
         try:
