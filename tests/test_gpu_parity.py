@@ -183,11 +183,11 @@ def test_hdmr_config_exact_bitwise(cid, config4, config5):
 
 
 @pytest.mark.parametrize("cid", [4, 5])
-@pytest.mark.parametrize("env", [{"DDSG_SLOT_ROT": "0"}, {"DDSG_SLOT_ROT": "1"}])
+@pytest.mark.parametrize("env", [{"DDSG_SLOT_ROT": "0"}, {"DDSG_SLOT_ROT": "1"}, {"DDSG_SLOT_ROT_MIN": "4"}])
 def test_hdmr_slot_layouts_bitwise(env, cid, config4, config5, monkeypatch):
-    """Both staged-row layouts (stride 9; rotated dual copies, the default for
-    full 1-d blocks and for 2-d blocks of max level 6 -- config 4's pairs)
-    give the reference's bits; the layout is chosen when the device program
+    """Every staged-row layout (stride 9; rotated dual copies, the default for
+    deep full blocks; rotation of shallower blocks too, DDSG_SLOT_ROT_MIN=4)
+    gives the reference's bits; the layout is chosen when the device program
     is built."""
     cfg, parts, slots, _ = config4 if cid == 4 else config5
     for k, v in env.items():
