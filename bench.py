@@ -662,7 +662,9 @@ def main():
             run_reference(args, rank, world)
         return
     dist = None
-    if world > 1:
+    # DDSG_BENCH_FORCE_DIST=1 (under torchrun): a one-rank NCCL group, so the
+    # collective code path (the refinement all-gather) runs on a single GPU
+    if world > 1 or os.environ.get("DDSG_BENCH_FORCE_DIST") == "1":
         import torch
         import torch.distributed as tdist
 
