@@ -402,14 +402,24 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   usable_ = false;
   if (!hp.plain || hp.slot_k.size() != 1) return false;
   const int d = hp.d;
-  if (d > kMaxDim) return false;
+  // the dense walk takes d <= 20; modified-linear grids up to kSparseMaxDim
+  // dims can still take the sparse walk (build_sparse decides)
+  const bool dense_ok = d <= kMaxDim;
+  if (!dense_ok && !(hp.slot_mode[0] == 1 && d <= kSparseMaxDim && hp.m > 1)) return false;
   const int s0 = hp.slot_sub_begin[0], s1 = hp.slot_sub_end[0];
   const int n_sub = s1 - s0;
   if (n_sub == 0) return false;
   int lmax = 1;
-  for (int s = s0; s < s1; ++s)
-    for (int j = 0; j < d; ++j) lmax = std::max<int>(lmax, hp.levels[hp.sub_lv_off[s] + j]);
-  if (lmax > 15) return false;  // 4-bit level nibbles
+  int64_t max_bits = 0;  // bits of the concatenated cell index (a uint32 in the kernels)
+  for (int s = s0; s < s1; ++s) {
+    int64_t bits = 0;
+    for (int j = 0; j < d; ++j) {
+      lmax = std::max<int>(lmax, hp.levels[hp.sub_lv_off[s] + j]);
+      bits += hp.levels[hp.sub_lv_off[s] + j] - 1;
+    }
+    max_bits = std::max(max_bits, bits);
+  }
+  if (lmax > 15 || max_bits > 31) return false;  // 4-bit level nibbles, 32-bit cell index
   // Per stored-order run, the subspaces that hold at least one node of the
   // run, in canonical order (a run's walk skips the others: config 3's two
   // runs touch 1,771 and 9,995 of its 10,626 subspaces).
@@ -417,7 +427,7 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   if (runs > kMaxRuns) return false;
   std::vector<uint32_t> rec;
   run_off_.assign(1, 0);
-  for (int run = 0; run < runs; ++run) {
+  for (int run = 0; run < (dense_ok ? runs : 0); ++run) {
     const uint8_t* prev = nullptr;
     for (int s = s0; s < s1; ++s) {
       const uint8_t* lv = &hp.levels[hp.sub_lv_off[s]];
@@ -480,6 +490,10 @@ bool PlainGrid::build(const HostProgram& hp, const EvalParams& dev) {
   }
   usable_ = true;
   build_sparse(hp);
+  if (!dense_ok && !sparse_) {
+    usable_ = false;  // the generic kernel takes it
+    return false;
+  }
   sort_ = d >= kSortMinDim;
   if (const char* e = std::getenv("DDSG_PLAIN_SORT"))
     if (std::atoi(e) == 0) sort_ = false;

@@ -168,3 +168,22 @@ def test_config3_level6_grid_exact():
     y = _eval_sorted(g, x)
     sel = np.r_[0:24, 8192 - 8:8192]
     assert np.array_equal(bits(y[sel]), bits(_oracle(g, x[sel])))
+
+
+@pytest.mark.parametrize("dim", [24, 40])
+def test_sparse_walk_beyond_20_dims(dim):
+    """Modified-linear plain grids with 21..64 dims take the sparse walk (the
+    dense walk stops at 20): against the generic kernel and the oracle."""
+    keep, ctx = int_ctx(dim)
+    g1 = SparseGridFunction.build(wl("wl_coupled"), dim, 1, 3, 1e-3, MODIFIED_LINEAR, ctx=ctx)
+    keys, sur = g1.nodes()
+    sur3 = np.concatenate([sur * (1.0 + 0.25 * j) for j in range(3)], axis=1)
+    g0 = SparseGridFunction.from_nodes(dim, 3, g1.max_level, g1.eps_gamma, MODIFIED_LINEAR, keys, sur3)
+    gs, gg = _copy(g0, True), _copy(g0, True, sparse=False)  # sparse walk / generic kernel
+    x = uniform_points(77 + dim, 6000, dim)
+    ys = _eval_sorted(gs, x)
+    yg = gg.interpolate(x)
+    assert last_eval_stats()[0] == 1  # the generic kernel, one launch
+    assert np.array_equal(bits(ys), bits(yg))
+    sel = np.r_[0:40, 5990:6000]
+    assert np.array_equal(bits(ys[sel]), bits(_oracle(g0, x[sel])))
