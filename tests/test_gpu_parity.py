@@ -294,3 +294,43 @@ def test_hdmr_stored_order_grids_exact():
     rc, want, _ = O.port_hdmr_eval(int(z["d"]), int(z["m"]), z["f_anchor"], shuffled, z["x"])
     assert vec.uses_slot_kernel()
     assert np.array_equal(bits(vec.evaluate_batch(z["x"])), bits(want))
+
+
+@pytest.mark.parametrize("cid,n", [(4, 65536), (5, 16384)])
+def test_hdmr_large_sample_vs_reference_evaluate_batch(cid, n, config4, config5):
+    """A large seeded sample straight against the reference's own
+    VectorizedDdsg::evaluate_batch (oracle/_ref, all host threads), same
+    canonical node bits on both sides: bit-identical."""
+    import os
+
+    cfg, parts, slots, vec = config4 if cid == 4 else config5
+    grids, keep = [], []
+    for (u, b, g), (_, _, gpart) in zip(slots, parts.slots):
+        if g is None:
+            grids.append(None)
+            continue
+        mode, keys, sur = g
+        grids.append(O.ref_from_nodes(len(u), cfg.m, mode, gpart.max_level, gpart.eps_gamma, keys, sur))
+    ref = O.RefHdmr(cfg.d, cfg.m, parts.f_anchor, [(u, b) for u, b, _ in slots], grids)
+    x = W.points(cfg, n=n, seed=4242 + cid)
+    rc, want = ref.eval(x, workers=os.cpu_count() or 1, flat=False)
+    assert rc == 0
+    assert np.array_equal(bits(vec.evaluate_batch(x)), bits(want))
+
+
+@pytest.mark.parametrize("cid,n", [(2, 8192), (3, 4096)])
+def test_grid_large_sample_vs_reference_interpolate(cid, n):
+    """Plain configs straight against the reference's SparseGridFunction::
+    interpolate over a large seeded sample (oracle/_ref, all host threads),
+    in the grid's stored node order (config 3: two stored-order runs), through
+    the Morton-sorted sparse / dense walks: bit-identical."""
+    import os
+
+    cfg = W.CONFIGS[cid]
+    g = W.build_grid(cfg)
+    keys, sur = g.nodes()
+    ref = O.ref_from_nodes(cfg.d, cfg.m, cfg.mode, g.max_level, g.eps_gamma, keys, sur)
+    x = W.points(cfg, n=n, seed=777 + cid)
+    rc, want = ref.eval(x, cfg.m, workers=os.cpu_count() or 1)
+    assert rc == 0
+    assert np.array_equal(bits(g.interpolate(x)), bits(want))
