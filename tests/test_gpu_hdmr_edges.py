@@ -69,6 +69,7 @@ def check(vec, d, m, fa, slots_o, x, nan_ok=False):
 def pts(d, n=700, seed=5):
     x = uniform_points(seed, n, d)
     x[:6] = np.array([0.0, 1.0, 0.5, 0.25, 1 - 2.0 ** -53, 2.0 ** -40])[:, None]
+    x[6:9] = np.array([5e-324, 1e-310, 2.0 ** -1022])[:, None]  # subnormal / smallest normal coordinates
     return x
 
 

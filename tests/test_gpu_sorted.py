@@ -101,7 +101,11 @@ def test_sorted_edge_points(mode, m):
     gt, gd = _copy(g0, True), _copy(g0, False, sparse=False)
     n = 5000 + 123
     x = uniform_points(321, n, 7)
-    edges = np.array([0.0, 1.0, 0.5, 0.25, 0.75, 0.125, 0.875, 1 - 2**-53, 2**-30, 2**-4])
+    # dyadic cell boundaries, the ends, and subnormal / tiny coordinates (the
+    # exponent-add scaling of factor() is exact for normal x and rounds away
+    # exactly like 0 for subnormal x)
+    edges = np.array([0.0, 1.0, 0.5, 0.25, 0.75, 0.125, 0.875, 1 - 2**-53, 2**-30, 2**-4,
+                      5e-324, 1e-310, 2.0**-1022, 2**-60])
     rng = np.random.default_rng(5)
     x[:600] = edges[rng.integers(0, len(edges), size=(600, 7))]
     x[600:1200] = x[17]  # a whole tile's worth of one point
