@@ -355,10 +355,16 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   kernel_timer().begin(st);
   const KernelArgs args{static_cast<const unsigned char*>(blocks_), block_off_, block_len_, slot_dims_, n_blocks_,
                         n_cb_, cb_group_, levels_, xt, n, m_, y, block_bytes_, n_stages_};
-  if (exact)
+  // The dynamic shared-memory limit is a property of the kernel function,
+  // shared by every program: set this program's own size before launching
+  // (a program built later with smaller stages would otherwise have lowered it).
+  if (exact) {
+    DDSG_CUDA((has_carry_ ? fast_attr_11 : fast_attr_10)(static_cast<int>(smem)));
     (has_carry_ ? fast_launch_11 : fast_launch_10)(grid, smem, st, args);
-  else
+  } else {
+    DDSG_CUDA((has_carry_ ? fast_attr_01 : fast_attr_00)(static_cast<int>(smem)));
     (has_carry_ ? fast_launch_01 : fast_launch_00)(grid, smem, st, args);
+  }
   kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());
   return 2;

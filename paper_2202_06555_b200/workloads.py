@@ -10,6 +10,7 @@ are fixed here and recorded in DESIGN.md §Workloads.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Tuple
 
@@ -111,19 +112,24 @@ def build_hdmr_parts(cfg: Config) -> HdmrParts:
     parts = HdmrParts(cfg.d, cfg.m, fa)
     f_addr = N.wl_fn(cfg.target)
     cut_addr = N.wl_fn("wl_cut_eval")
-    for u, bu in zip(fam, b):
-        if not u:
-            parts.slots.append((u, bu, None))
-            continue
+
+    def build_cut(u):
         dims = np.array(u, dtype=np.int32)
         cut = wl.wl_cut_new(f_addr, None, cfg.d, cfg.m, len(u), dims.ctypes.data, anchor.ctypes.data)
         try:
             lvl = cfg.level_1d if len(u) == 1 else cfg.level_2d
             eps = cfg.eps_1d if len(u) == 1 else cfg.eps_2d
-            g = SparseGridFunction.build(cut_addr, len(u), cfg.m, lvl, eps, cfg.mode, ctx=cut)
+            return SparseGridFunction.build(cut_addr, len(u), cfg.m, lvl, eps, cfg.mode, ctx=cut)
         finally:
             wl.wl_cut_free(C.c_void_p(cut))
-        parts.slots.append((u, bu, g))
+
+    # the cut builds are independent host C calls (ctypes releases the GIL;
+    # the target's tables were initialised by the anchor evaluation above)
+    import concurrent.futures as cf
+
+    with cf.ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        grids = list(ex.map(lambda u: build_cut(u) if u else None, fam))
+    parts.slots.extend((u, bu, g) for u, bu, g in zip(fam, b, grids))
     return parts
 
 

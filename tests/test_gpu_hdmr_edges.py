@@ -171,3 +171,16 @@ def test_order2_subspace_beyond_max_single_level(mode):
     vec = VectorizedDdsg.compile(d, m, fa, slots_g)
     assert vec.uses_slot_kernel()
     check(vec, d, m, fa, slots_o, pts(d))
+
+
+def test_programs_with_different_stage_sizes_coexist():
+    """The slot kernel's dynamic shared-memory limit belongs to the kernel
+    function, not the program: a program with large stages must still launch
+    after a program with small stages was built (and vice versa)."""
+    d, m = 3, 9
+    big, fa_b, so_b = make(d, m, family_1d_2d(d, [(0, 2)]), {1: 10, 2: 4}, seed=1)
+    small, fa_s, so_s = make(d, m, family_1d_2d(d, []), {1: 2, 2: 2}, seed=2)
+    assert big.uses_slot_kernel() and small.uses_slot_kernel()
+    check(big, d, m, fa_b, so_b, pts(d, 300))
+    check(small, d, m, fa_s, so_s, pts(d, 300))
+    check(big, d, m, fa_b, so_b, pts(d, 300, seed=9))
