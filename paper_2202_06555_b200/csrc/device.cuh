@@ -93,6 +93,12 @@ struct KernelTimer {
 };
 KernelTimer& kernel_timer();
 
+// Raise-only cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the
+// current device: the attribute belongs to the kernel function, shared by
+// every program and host thread, so it is never lowered (a lowered limit
+// would break another program's launch, possibly on another host thread).
+void ensure_dynamic_smem(const void* fn, size_t bytes);
+
 // Evaluates the program over n points.  x/y may be host or device memory.
 // Returns the lowest out-of-domain point index or -1.
 int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,

@@ -12,6 +12,8 @@
 // mul-then-add (EXACT) or FMA (FAST).  Partial slot sums live on a
 // per-thread stack driven by the precompiled merge schedule.
 #include <cuda_runtime.h>
+#include <mutex>
+#include <map>
 
 #include <algorithm>
 #include <climits>
@@ -60,6 +62,18 @@ double KernelTimer::collect() {
   g_timer.used = 0;
   return total;
 }
+void ensure_dynamic_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> set_to;
+  int dev = 0;
+  DDSG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = set_to[{dev, fn}];
+  if (bytes <= cur) return;
+  DDSG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  cur = bytes;
+}
+
 KernelTimer& kernel_timer() {
   static thread_local KernelTimer t;
   return t;

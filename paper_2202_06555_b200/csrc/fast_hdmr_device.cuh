@@ -812,7 +812,8 @@ struct KernelArgs {
                                                         a.n, a.m, a.y, a.stage_bytes, a.n_stages);        \
   }                                                                                                       \
   cudaError_t fast_attr_##E##C(int smem) {                                                                \
-    return cudaFuncSetAttribute(fast_hdmr_kernel<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+    ensure_dynamic_smem(reinterpret_cast<const void*>(fast_hdmr_kernel<E, C>), static_cast<size_t>(smem));  \
+    return cudaSuccess;                                                                                   \
   }
 
 void fast_launch_00(dim3, size_t, cudaStream_t, const KernelArgs&);

@@ -586,8 +586,7 @@ template <int kMC, int kExact, int kMulti>
 static void launch_sparse_t(const SparseParams& S, unsigned grid, size_t smem, const double* x, int64_t n,
                             int64_t base, double* y, unsigned long long* bad, cudaStream_t st) {
   auto k = sparse_kernel<kMC, kExact, kMulti>;
-  if (smem > 48 * 1024)
-    DDSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (smem > 48 * 1024) ensure_dynamic_smem(reinterpret_cast<const void*>(k), smem);
   k<<<grid, kSparseThreads, smem, st>>>(S, x, n, base, y, bad);
 }
 
