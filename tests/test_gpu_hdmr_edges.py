@@ -184,3 +184,33 @@ def test_programs_with_different_stage_sizes_coexist():
     check(big, d, m, fa_b, so_b, pts(d, 300))
     check(small, d, m, fa_s, so_s, pts(d, 300))
     check(big, d, m, fa_b, so_b, pts(d, 300, seed=9))
+
+
+def test_concurrent_programs_on_host_threads():
+    """Two programs with different stage sizes evaluated concurrently from
+    two host threads (per-thread scratch and streams; the shared-memory limit
+    of the shared kernel is only ever raised): every result stays bit-identical
+    to its single-threaded evaluation."""
+    import threading
+
+    d, m = 3, 9
+    big, fa_b, so_b = make(d, m, family_1d_2d(d, [(0, 2)]), {1: 10, 2: 4}, seed=3)
+    small, fa_s, so_s = make(d, m, family_1d_2d(d, [(1, 2)]), {1: 3, 2: 2}, seed=4)
+    xb, xs = pts(d, 5000, seed=11), pts(d, 5000, seed=12)
+    want_b, want_s = bits(big.evaluate_batch(xb)), bits(small.evaluate_batch(xs))
+    errors = []
+
+    def run(vec, x, want):
+        try:
+            for _ in range(20):
+                if not np.array_equal(bits(vec.evaluate_batch(x)), want):
+                    errors.append("mismatch")
+        except Exception as e:  # surfaced below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=run, args=a) for a in ((big, xb, want_b), (small, xs, want_s))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:3]
