@@ -73,3 +73,27 @@ def test_bench_default_line_on_gpu():
     br = rf["binding_resource"]
     assert 0 < br["frac"] < 1 and br["peak"] > 0 and abs(br["achieved"] - rf["achieved"]) < 1e-9
     assert br["peak"] < rf["peak"]  # 16 doubles/clk/SM is below the DFMA rate
+
+
+@pytest.mark.gpu
+def test_bench_under_torchrun_nccl_one_rank():
+    """The multi-GPU launch path on one GPU: torchrun, a one-rank NCCL group
+    (DDSG_BENCH_FORCE_DIST=1), the refinement's surplus all-gather over NCCL,
+    then the timed evaluation and the usual JSON line."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    e = dict(os.environ, DDSG_BENCH_FORCE_DIST="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+           "--gpus", "1", "--steps", "2", "--warmup", "3", "--points", "65536", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=e)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0
+    assert d["refinement"]["collective"] == "all_gather_into_tensor (NCCL)"
+    assert d["refinement"]["allgather_bytes"] == d["refinement"]["new_nodes"] * d["config"]["m"] * 8
