@@ -14,9 +14,11 @@
  *  - Points are row-major x[n][dim], outputs row-major y[n][m] (replacing the
  *    reference's vector<vector<double>>, ddsg_eval.hpp:130-139).
  *  - x / y may be host or device pointers (detected with
- *    cudaPointerGetAttributes).  Host buffers are copied in pipelined chunks
- *    (pinned host memory gives full PCIe bandwidth); device buffers are used
- *    in place.
+ *    cudaPointerGetAttributes).  Device buffers are used in place; pinned
+ *    host buffers are copied in pipelined chunks over three streams;
+ *    ordinary (pageable) host buffers -- std::vector, numpy -- are staged
+ *    through pinned buffers in pipelined chunks (the same path as the
+ *    EvalWorkspace calls below).
  *  - Heap keys follow grid_index.hpp:1-38: a 1-d node (l, i) is packed as
  *    hk = 2^(l-1) + (i-1)/2, l in [1, 30].
  *  - Objects are immutable after creation except through ddsg_grid_append
@@ -51,10 +53,14 @@ typedef enum { DDSG_ZERO_BOUNDARY = 0, DDSG_MODIFIED_LINEAR = 1 } ddsg_boundary_
 /* sparse_grid.hpp:53 SurplusNorm. */
 typedef enum { DDSG_NORM_INF = 0, DDSG_NORM_L2 = 1 } ddsg_surplus_norm;
 
-/* Evaluation arithmetic.  EXACT reproduces the reference rounding sequence
- * bit for bit (mul then add per node in canonical order, x b, pairwise slot
- * sum).  FAST contracts the per-node mul+add into one FMA (same order); it is
- * within 1e-14 abs + 1e-12 rel of the reference on well-conditioned grids. */
+/* Evaluation arithmetic.  EXACT (the default) reproduces the reference
+ * rounding sequence bit for bit (mul then add per node in canonical order,
+ * x b, pairwise slot sum).  FAST contracts the per-node mul+add into one FMA
+ * (same order).  FAST carries NO tolerance guarantee: its per-slot rounding
+ * differs from the reference's by up to ~n u |row| and HDMR sums cancel
+ * (sum |b_s row_s| is ~10^2-10^3 x |y| on the BASELINE configs), so it can
+ * exceed 1e-14 abs + 1e-12 rel on a small fraction of outputs (measured
+ * rates: DESIGN.md §3.1).  Use it only where that is acceptable. */
 typedef enum { DDSG_EVAL_EXACT = 0, DDSG_EVAL_FAST = 1 } ddsg_eval_mode;
 
 typedef struct ddsg_grid ddsg_grid_t; /* SparseGridFunction (sparse_grid.hpp:72) */
@@ -171,6 +177,86 @@ ddsg_status ddsg_eval_hdmr(const ddsg_hdmr_t* h, const double* x, int64_t n, dou
 
 /* VectorizedDdsg::quadrature (ddsg_eval.hpp:143-151), host. */
 ddsg_status ddsg_hdmr_quadrature(const ddsg_hdmr_t* h, double* out);
+
+/* Slot s of the table in coeff_b order (VectorizedDdsg::slots(),
+ * ddsg_eval.hpp:77; the empty index first): its order, dims (caller buffer
+ * of >= order entries, may be NULL), coefficient b, and a NEW grid handle
+ * holding a copy of its grid (NULL for the empty index; the caller destroys
+ * it; pass grid == NULL to skip the copy).  OUT_OF_RANGE if s is outside
+ * [0, n_slots). */
+ddsg_status ddsg_hdmr_slot(const ddsg_hdmr_t* h, int s, int* order, int32_t* dims, int32_t* b, ddsg_grid_t** grid);
+
+/* --------------------------------------------------------- JSON documents
+ *
+ * The reference's versioned documents (serialize.hpp, schema_version 1):
+ * surpluses and coordinates are JSON numbers written with shortest
+ * round-trip digits, so save/load is bit-exact (serialize.hpp:3-5).  Text in,
+ * text out (the caller owns the file I/O, like load_json / save_json,
+ * serialize.hpp:147-160).  `len` < 0 means NUL-terminated.  Writers: call
+ * with buf == NULL to get the size in *len_out (bytes, without the NUL),
+ * then with a buffer of at least *len_out + 1 bytes; the text is the
+ * reference's save_json layout (dump(2) plus a newline). */
+
+/* sparse_grid_from_json (serialize.hpp:54-77) -> a grid handle.  Errors:
+ * INVALID_ARGUMENT on malformed JSON, a missing key, a wrong schema version
+ * or type tag, a bad heap key (grid_index.hpp:32-39) or from_nodes'
+ * checks (sparse_grid.hpp:168-175). */
+ddsg_status ddsg_grid_from_json(const char* text, int64_t len, ddsg_grid_t** out);
+/* to_json(SparseGridFunction) (serialize.hpp:31-52), nodes in stored order. */
+ddsg_status ddsg_grid_to_json(const ddsg_grid_t* g, char* buf, int64_t cap, int64_t* len_out);
+
+/* The reference's ddsg_from_json, serialize.hpp:112-145, then VectorizedDdsg::compile
+ * (ddsg_eval.hpp:40-74): the document's policy as an evaluator, slots in
+ * coeff_b order.  The document's k_max, anchor coordinates, rejected set and
+ * cut quadratures are kept for ddsg_hdmr_to_json / ddsg_hdmr_document.
+ * Errors: as ddsg_grid_from_json, plus compile's (coefficient for a
+ * non-accepted index, missing subset, no empty slot). */
+ddsg_status ddsg_hdmr_from_json(const char* text, int64_t len, ddsg_hdmr_t** out);
+/* to_json(DdsgFunction) (serialize.hpp:84-110).  Needs the document fields:
+ * INVALID_ARGUMENT without anchor coordinates, OUT_OF_RANGE without the cut
+ * quadratures (the reference's cut_quadrature throws std::out_of_range,
+ * hdmr.hpp:213-218); set them with ddsg_hdmr_set_document. */
+ddsg_status ddsg_hdmr_to_json(const ddsg_hdmr_t* h, char* buf, int64_t cap, int64_t* len_out);
+
+/* Document fields of DdsgFunction that evaluation does not use (hdmr.hpp:
+ * k_max, anchor().coords, rejected(), cut_quadrature(u)):
+ *   anchor_coords   [d] (NULL keeps the current value)
+ *   rejected        n_rejected indices: rejected_order[r] = |u_r|, dims
+ *                   concatenated in rejected_dims (sorted and validated like
+ *                   ComponentIndex::make)
+ *   cut_quadratures [n_slots][m] in slot order, or NULL (none) */
+ddsg_status ddsg_hdmr_set_document(ddsg_hdmr_t* h, int k_max, const double* anchor_coords, int n_rejected,
+                                   const int32_t* rejected_order, const int32_t* rejected_dims,
+                                   const double* cut_quadratures);
+/* Reads them back, plus the anchor values f_anchor [m] (any output may be
+ * NULL; call first with the arrays NULL to get n_rejected / n_rejected_dims).
+ * anchor_coords defaults to 0.5 when never set; *has_quadratures = 0 when no
+ * quadratures are held. */
+ddsg_status ddsg_hdmr_document(const ddsg_hdmr_t* h, int* k_max, double* anchor_coords, double* f_anchor,
+                               int* n_rejected, int64_t* n_rejected_dims, int32_t* rejected_order,
+                               int32_t* rejected_dims, int* has_quadratures, double* cut_quadratures);
+
+/* ---------------------------------------------------- evaluation workspace
+ *
+ * EvalWorkspace (ddsg_eval.hpp:21-24): reusable buffers for allocation-free
+ * evaluation in hot loops.  A workspace owns pinned host staging, device
+ * buffers and a stream on the device current at first use; x / y passed to
+ * the _ws calls are ordinary (pageable) host memory, staged through the
+ * pinned buffers in pipelined chunks.  A workspace is not thread-safe (the
+ * reference keeps one per thread: thread_local EvalWorkspace,
+ * time_iteration.hpp:88). */
+typedef struct ddsg_workspace ddsg_workspace_t;
+ddsg_status ddsg_workspace_create(ddsg_workspace_t** out);
+ddsg_status ddsg_workspace_destroy(ddsg_workspace_t* ws);
+/* VectorizedDdsg::evaluate(x, out, ws, interp_calls) (ddsg_eval.hpp:83-113)
+ * over n host points: y[i] = evaluate(x[i]); *interp_calls (may be NULL) is
+ * incremented by n x the number of active non-empty slots, the reference's
+ * per-point count of cut interpolations.  Errors as ddsg_eval_hdmr. */
+ddsg_status ddsg_eval_hdmr_ws(const ddsg_hdmr_t* h, ddsg_workspace_t* ws, const double* x, int64_t n, double* y,
+                              int64_t* bad_index, uint64_t* interp_calls);
+/* SparseGridFunction::interpolate over n host points through a workspace. */
+ddsg_status ddsg_eval_grid_ws(const ddsg_grid_t* g, ddsg_workspace_t* ws, const double* x, int64_t n, double* y,
+                              int64_t* bad_index);
 
 /* --------------------------------------------------------------- controls */
 

@@ -8,7 +8,9 @@
 //
 //   SparseGridFunction   sparse_grid.hpp:72-351
 //   DdsgFunction         hdmr.hpp:195-356   (from_parts only; decompose is out of scope)
+//   EvalWorkspace        ddsg_eval.hpp:21-24
 //   VectorizedDdsg       ddsg_eval.hpp:28-165
+//   JSON documents       serialize.hpp:17-160 (JsonDocument stands in for nlohmann::json)
 //   build_error          sparse_grid.hpp:40-48
 //   task_error           runtime.hpp:71-92
 #pragma once
@@ -17,6 +19,8 @@
 #include <cmath>
 #include <cstdint>
 #include <exception>
+#include <fstream>
+#include <sstream>
 #include <functional>
 #include <map>
 #include <memory>
@@ -227,6 +231,8 @@ class SparseGridFunction {
   }
 
   const ddsg_grid_t* handle() const { return h_.get(); }
+  // Takes ownership of a C-ABI grid handle (e.g. from ddsg_grid_from_json).
+  static SparseGridFunction adopt(ddsg_grid_t* g) { return SparseGridFunction(g); }
 
  private:
   struct Del {
@@ -259,6 +265,25 @@ struct ComponentIndex {  // component_index.hpp:16-54
     if (dims.size() != o.dims.size()) return dims.size() < o.dims.size();
     return dims < o.dims;
   }
+  bool contains(int d) const { return std::binary_search(dims.begin(), dims.end(), d); }
+  bool is_superset_of(const ComponentIndex& sub) const {
+    return std::includes(dims.begin(), dims.end(), sub.dims.begin(), sub.dims.end());
+  }
+  std::string to_string() const {
+    if (dims.empty()) return "{}";
+    std::string s = "{";
+    for (std::size_t i = 0; i < dims.size(); ++i) s += (i ? "," : "") + std::to_string(dims[i]);
+    return s + "}";
+  }
+  static ComponentIndex make(std::vector<int> dims, int d) {
+    ComponentIndex u{std::move(dims)};
+    std::sort(u.dims.begin(), u.dims.end());
+    if (std::adjacent_find(u.dims.begin(), u.dims.end()) != u.dims.end())
+      throw std::invalid_argument("component index: duplicate dimension");
+    if (!u.dims.empty() && (u.dims.front() < 0 || u.dims.back() >= d))
+      throw std::invalid_argument("component index: dimension id out of range");
+    return u;
+  }
 };
 
 struct AnchorPoint {  // hdmr.hpp:27-30
@@ -280,25 +305,53 @@ class DdsgFunction {  // hdmr.hpp:195-356
  public:
   int dim() const { return dim_; }
   int out_dim() const { return out_dim_; }
+  int k_max() const { return opt_.k_max; }
+  bool exact_cuts() const { return opt_.exact_cuts; }
+  const DdsgOptions& options() const { return opt_; }
   const AnchorPoint& anchor() const { return anchor_; }
   const std::map<ComponentIndex, SparseGridFunction>& accepted() const { return accepted_; }
+  const std::set<ComponentIndex>& rejected() const { return rejected_; }
   const std::map<ComponentIndex, int>& coeff_b() const { return coeff_b_; }
+
+  // hdmr.hpp:213-218
+  const std::vector<double>& cut_quadrature(const ComponentIndex& u) const {
+    auto it = cut_quadratures_.find(u);
+    if (it == cut_quadratures_.end())
+      throw std::out_of_range("ddsg: no quadrature for component index " + u.to_string());
+    return it->second;
+  }
+  const std::map<ComponentIndex, std::vector<double>>& cut_quadratures() const { return cut_quadratures_; }
+
+  std::size_t total_grid_points() const {  // hdmr.hpp:245-250
+    std::size_t n = 1;
+    for (const auto& [u, grid] : accepted_)
+      if (!u.empty()) n += grid.size();
+    return n;
+  }
+  std::size_t order_reached() const { return order_reached_; }
+
+  void check_point(std::span<const double> x) const {  // hdmr.hpp:299-304
+    if (x.size() != static_cast<std::size_t>(dim_)) throw std::invalid_argument("ddsg: query dimension mismatch");
+    for (double v : x)
+      if (!(v >= 0.0 && v <= 1.0)) throw std::domain_error("ddsg: query outside unit cube");
+  }
 
   // hdmr.hpp:307-325
   static DdsgFunction from_parts(int dim, int out_dim, DdsgOptions opt, AnchorPoint anchor,
                                  std::map<ComponentIndex, SparseGridFunction> accepted,
                                  std::set<ComponentIndex> rejected, std::map<ComponentIndex, int> coeff_b,
                                  std::map<ComponentIndex, std::vector<double>> cut_quadratures) {
-    (void)rejected;
-    (void)cut_quadratures;  // recomputed from the grids (bit-identical to decompose's)
     DdsgFunction f;
     f.dim_ = dim;
     f.out_dim_ = out_dim;
     f.opt_ = opt;
-    f.opt_.exact_cuts = false;
+    f.opt_.exact_cuts = false;  // exact-cut closures are not serializable
     f.anchor_ = std::move(anchor);
     f.accepted_ = std::move(accepted);
+    f.rejected_ = std::move(rejected);
     f.coeff_b_ = std::move(coeff_b);
+    f.cut_quadratures_ = std::move(cut_quadratures);
+    for (const auto& [u, grid] : f.accepted_) f.order_reached_ = std::max(f.order_reached_, u.order());
     return f;
   }
 
@@ -307,7 +360,36 @@ class DdsgFunction {  // hdmr.hpp:195-356
   DdsgOptions opt_;
   AnchorPoint anchor_;
   std::map<ComponentIndex, SparseGridFunction> accepted_;
+  std::set<ComponentIndex> rejected_;
   std::map<ComponentIndex, int> coeff_b_;
+  std::map<ComponentIndex, std::vector<double>> cut_quadratures_;
+  std::size_t order_reached_ = 0;
+};
+
+// Reusable evaluation buffers (ddsg_eval.hpp:21-24): pinned host staging,
+// device buffers and a stream, created on first use on the current device.
+// Like the reference's, one workspace serves one thread at a time; copies
+// start with fresh buffers.
+class EvalWorkspace {
+ public:
+  EvalWorkspace() = default;
+  EvalWorkspace(const EvalWorkspace&) {}
+  EvalWorkspace& operator=(const EvalWorkspace&) { return *this; }
+  EvalWorkspace(EvalWorkspace&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  EvalWorkspace& operator=(EvalWorkspace&& o) noexcept {
+    std::swap(h_, o.h_);
+    return *this;
+  }
+  ~EvalWorkspace() {
+    if (h_) ddsg_workspace_destroy(h_);
+  }
+  ddsg_workspace_t* handle() {
+    if (!h_) detail::check(ddsg_workspace_create(&h_));
+    return h_;
+  }
+
+ private:
+  ddsg_workspace_t* h_ = nullptr;
 };
 
 class VectorizedDdsg {  // ddsg_eval.hpp:28-165
@@ -337,26 +419,50 @@ class VectorizedDdsg {  // ddsg_eval.hpp:28-165
         grids.push_back(it->second.handle());
       }
     }
+    if (source->anchor().f_anchor.size() != static_cast<std::size_t>(v.out_dim_))
+      throw std::invalid_argument("vectorized ddsg: anchor value length != out_dim");
     ddsg_hdmr_t* h = nullptr;
     detail::check(ddsg_hdmr_create(v.dim_, v.out_dim_, source->anchor().f_anchor.data(),
                                    static_cast<int>(order.size()), order.data(), dims.data(), b.data(),
                                    grids.data(), &h));
     v.h_.reset(h, [](ddsg_hdmr_t* p) { ddsg_hdmr_destroy(p); });
+    for (const auto& [u, bu] : source->coeff_b()) {
+      Slot sl;
+      sl.index = u;
+      sl.b = bu;
+      if (!u.empty()) sl.grid = &source->accepted().find(u)->second;
+      v.slots_.push_back(std::move(sl));
+    }
     return v;
   }
 
+  struct Slot {  // ddsg_eval.hpp:30-34
+    ComponentIndex index;
+    int b = 0;
+    const SparseGridFunction* grid = nullptr;  // null for the empty index
+  };
+
   int dim() const { return dim_; }
   int out_dim() const { return out_dim_; }
+  const std::vector<Slot>& slots() const { return slots_; }  // ddsg_eval.hpp:77
   const DdsgFunction& source() const { return *source_; }
 
-  // ddsg_eval.hpp:83-113 (one point)
-  void evaluate(std::span<const double> x, std::span<double> out) const {
-    if (x.size() != static_cast<std::size_t>(dim_)) throw std::invalid_argument("ddsg: query dimension mismatch");
+  // ddsg_eval.hpp:83-113 (one point, the reference's hot-loop entry): the
+  // point is staged through `ws`; `interp_calls`, when given, counts cut
+  // evaluations (one per active non-empty slot).
+  void evaluate(std::span<const double> x, std::span<double> out, EvalWorkspace& ws,
+                std::uint64_t* interp_calls = nullptr) const {
+    source_->check_point(x);  // dimension, then domain (hdmr.hpp:299-304)
     if (out.size() != static_cast<std::size_t>(out_dim_))
       throw std::invalid_argument("vectorized ddsg: output length mismatch");
     int64_t bad = -1;
-    const ddsg_status s = ddsg_eval_hdmr(h_.get(), x.data(), 1, out.data(), &bad, nullptr);
+    const ddsg_status s = ddsg_eval_hdmr_ws(h_.get(), ws.handle(), x.data(), 1, out.data(), &bad, interp_calls);
     if (s != DDSG_OK) detail::raise(s);
+  }
+  // ddsg_eval.hpp:115-119
+  void evaluate(std::span<const double> x, std::span<double> out, std::uint64_t* interp_calls = nullptr) const {
+    thread_local EvalWorkspace ws;
+    evaluate(x, out, ws, interp_calls);
   }
   std::vector<double> evaluate(std::span<const double> x) const {
     std::vector<double> out(static_cast<std::size_t>(out_dim_));
@@ -403,8 +509,145 @@ class VectorizedDdsg {  // ddsg_eval.hpp:28-165
  private:
   std::shared_ptr<const DdsgFunction> source_;
   std::shared_ptr<ddsg_hdmr_t> h_;
+  std::vector<Slot> slots_;
   int dim_ = 0, out_dim_ = 0;
 };
+
+// ------------------------------------------------------------ JSON documents
+// serialize.hpp:17-160 with JsonDocument in place of nlohmann::json: the
+// text of a schema-version-1 document; load_json / save_json do the file
+// I/O and the C-ABI (ddsg_*_from_json / ddsg_*_to_json) parses and writes.
+struct JsonDocument {
+  std::string text;
+  std::string dump(int = 2) const { return text; }
+};
+
+inline constexpr int kSchemaVersion = 1;  // serialize.hpp:17
+
+inline std::string to_string(BoundaryMode mode) {  // serialize.hpp:19-21
+  return mode == BoundaryMode::zero_boundary ? "zero_boundary" : "modified_linear";
+}
+inline BoundaryMode boundary_mode_from_string(const std::string& s) {  // serialize.hpp:23-27
+  if (s == "zero_boundary") return BoundaryMode::zero_boundary;
+  if (s == "modified_linear") return BoundaryMode::modified_linear;
+  throw std::invalid_argument("unknown boundary mode: " + s);
+}
+
+namespace detail {
+template <typename F>
+JsonDocument read_text(F&& writer) {
+  int64_t len = 0;
+  check(writer(nullptr, 0, &len));
+  std::string text(static_cast<std::size_t>(len) + 1, '\0');
+  check(writer(text.data(), len + 1, &len));
+  text.resize(static_cast<std::size_t>(len));
+  return JsonDocument{std::move(text)};
+}
+}  // namespace detail
+
+inline JsonDocument to_json(const SparseGridFunction& g) {  // serialize.hpp:31-52
+  return detail::read_text(
+      [&](char* b, int64_t cap, int64_t* len) { return ddsg_grid_to_json(g.handle(), b, cap, len); });
+}
+
+inline SparseGridFunction sparse_grid_from_json(const JsonDocument& doc) {  // serialize.hpp:54-77
+  ddsg_grid_t* g = nullptr;
+  detail::check(ddsg_grid_from_json(doc.text.data(), static_cast<int64_t>(doc.text.size()), &g));
+  return SparseGridFunction::adopt(g);
+}
+
+inline JsonDocument to_json(const DdsgFunction& f) {  // serialize.hpp:84-110
+  if (f.exact_cuts()) throw std::invalid_argument("ddsg document: exact-cut decompositions are not serializable");
+  std::vector<int32_t> order, dims, b;
+  std::vector<const ddsg_grid_t*> grids;
+  std::vector<double> quads;
+  for (const auto& [u, bu] : f.coeff_b()) {
+    order.push_back(static_cast<int32_t>(u.order()));
+    for (int dd : u.dims) dims.push_back(dd);
+    b.push_back(bu);
+    auto it = f.accepted().find(u);
+    grids.push_back(u.empty() ? nullptr : (it == f.accepted().end() ? nullptr : it->second.handle()));
+    const auto& q = f.cut_quadrature(u);  // std::out_of_range when absent, like the reference
+    quads.insert(quads.end(), q.begin(), q.end());
+  }
+  ddsg_hdmr_t* h = nullptr;
+  detail::check(ddsg_hdmr_create(f.dim(), f.out_dim(), f.anchor().f_anchor.data(), static_cast<int>(order.size()),
+                                 order.data(), dims.data(), b.data(), grids.data(), &h));
+  std::unique_ptr<ddsg_hdmr_t, ddsg_status (*)(ddsg_hdmr_t*)> hold(h, ddsg_hdmr_destroy);
+  std::vector<int32_t> rorder, rdims;
+  for (const auto& u : f.rejected()) {
+    rorder.push_back(static_cast<int32_t>(u.order()));
+    for (int dd : u.dims) rdims.push_back(dd);
+  }
+  if (f.anchor().coords.size() != static_cast<std::size_t>(f.dim()))
+    throw std::invalid_argument("ddsg document: anchor coordinates length != dim");
+  detail::check(ddsg_hdmr_set_document(h, f.k_max(), f.anchor().coords.data(), static_cast<int>(rorder.size()),
+                                       rorder.data(), rdims.data(), quads.data()));
+  return detail::read_text([&](char* buf, int64_t cap, int64_t* len) { return ddsg_hdmr_to_json(h, buf, cap, len); });
+}
+
+inline DdsgFunction ddsg_from_json(const JsonDocument& doc) {  // serialize.hpp:112-145
+  ddsg_hdmr_t* h = nullptr;
+  detail::check(ddsg_hdmr_from_json(doc.text.data(), static_cast<int64_t>(doc.text.size()), &h));
+  std::unique_ptr<ddsg_hdmr_t, ddsg_status (*)(ddsg_hdmr_t*)> hold(h, ddsg_hdmr_destroy);
+  int d = 0, m = 0, n_slots = 0;
+  detail::check(ddsg_hdmr_info(h, &d, &m, &n_slots, nullptr, nullptr));
+  int k_max = 1, n_rej = 0, has_q = 0;
+  int64_t n_rej_dims = 0;
+  detail::check(ddsg_hdmr_document(h, &k_max, nullptr, nullptr, &n_rej, &n_rej_dims, nullptr, nullptr, &has_q,
+                                   nullptr));
+  AnchorPoint anchor;
+  anchor.coords.resize(static_cast<std::size_t>(d));
+  anchor.f_anchor.resize(static_cast<std::size_t>(m));
+  std::vector<int32_t> rorder(static_cast<std::size_t>(n_rej)), rdims(static_cast<std::size_t>(n_rej_dims));
+  std::vector<double> quads(has_q ? static_cast<std::size_t>(n_slots) * static_cast<std::size_t>(m) : 0);
+  detail::check(ddsg_hdmr_document(h, nullptr, anchor.coords.data(), anchor.f_anchor.data(), nullptr, nullptr,
+                                   rorder.data(), rdims.data(), nullptr, has_q ? quads.data() : nullptr));
+  DdsgOptions opt;
+  opt.k_max = k_max;
+  std::map<ComponentIndex, SparseGridFunction> accepted;
+  std::map<ComponentIndex, int> coeff_b;
+  std::map<ComponentIndex, std::vector<double>> cut_q;
+  std::vector<int32_t> sd(static_cast<std::size_t>(d));
+  for (int s = 0; s < n_slots; ++s) {
+    int order = 0;
+    int32_t bu = 0;
+    ddsg_grid_t* g = nullptr;
+    detail::check(ddsg_hdmr_slot(h, s, &order, sd.data(), &bu, &g));
+    ComponentIndex u{std::vector<int>(sd.begin(), sd.begin() + order)};
+    coeff_b[u] = bu;
+    if (has_q)
+      cut_q[u] = std::vector<double>(quads.begin() + static_cast<std::ptrdiff_t>(s) * m,
+                                     quads.begin() + static_cast<std::ptrdiff_t>(s + 1) * m);
+    if (g) {
+      SparseGridFunction grid = SparseGridFunction::adopt(g);
+      opt.max_level = grid.max_level();  // serialize.hpp:124-127
+      opt.eps_gamma = grid.eps_gamma();
+      opt.mode = grid.boundary_mode();
+      accepted.emplace(std::move(u), std::move(grid));
+    }
+  }
+  std::set<ComponentIndex> rejected;
+  for (std::size_t r = 0, off = 0; r < rorder.size(); off += static_cast<std::size_t>(rorder[r]), ++r)
+    rejected.insert(ComponentIndex{std::vector<int>(rdims.begin() + static_cast<std::ptrdiff_t>(off),
+                                                    rdims.begin() + static_cast<std::ptrdiff_t>(off + rorder[r]))});
+  return DdsgFunction::from_parts(d, m, opt, std::move(anchor), std::move(accepted), std::move(rejected),
+                                  std::move(coeff_b), std::move(cut_q));
+}
+
+inline void save_json(const JsonDocument& doc, const std::string& path) {  // serialize.hpp:147-152
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot open for writing: " + path);
+  out << doc.text;  // already dump(2) + "\n"
+}
+
+inline JsonDocument load_json(const std::string& path) {  // serialize.hpp:154-160
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open for reading: " + path);
+  std::ostringstream ss;
+  ss << in.rdbuf();
+  return JsonDocument{ss.str()};
+}
 
 }  // namespace ddsg_b200
 

@@ -63,6 +63,17 @@ SIGNATURES = {
     "ddsg_hdmr_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
     "ddsg_grid_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
     "ddsg_uniform_points": (None, [C.c_uint64, _i64, _i, _p]),
+    "ddsg_hdmr_slot": (_i, [_p, _i, C.POINTER(_i), _p, C.POINTER(C.c_int32), C.POINTER(_p)]),
+    "ddsg_grid_from_json": (_i, [C.c_char_p, _i64, C.POINTER(_p)]),
+    "ddsg_grid_to_json": (_i, [_p, _p, _i64, C.POINTER(_i64)]),
+    "ddsg_hdmr_from_json": (_i, [C.c_char_p, _i64, C.POINTER(_p)]),
+    "ddsg_hdmr_to_json": (_i, [_p, _p, _i64, C.POINTER(_i64)]),
+    "ddsg_hdmr_set_document": (_i, [_p, _i, _p, _i, _p, _p, _p]),
+    "ddsg_hdmr_document": (_i, [_p, C.POINTER(_i), _p, _p, C.POINTER(_i), C.POINTER(_i64), _p, _p, C.POINTER(_i), _p]),
+    "ddsg_workspace_create": (_i, [C.POINTER(_p)]),
+    "ddsg_workspace_destroy": (_i, [_p]),
+    "ddsg_eval_hdmr_ws": (_i, [_p, _p, _pd, _i64, _pd, C.POINTER(_i64), C.POINTER(C.c_uint64)]),
+    "ddsg_eval_grid_ws": (_i, [_p, _p, _pd, _i64, _pd, C.POINTER(_i64)]),
     "ddsg_irbc_refresh_derived": (_i, [_p, _i]),
     "ddsg_irbc_steady_state_lambda": (_i, [_p, C.POINTER(_d)]),
     "ddsg_irbc_foc_residuals": (_i, [_p, _p, _p, _i64, _pd, _pd, _pd, _pd, _pd, C.POINTER(_i64), _p]),

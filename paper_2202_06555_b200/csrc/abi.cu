@@ -17,113 +17,98 @@
 #include "../../include/ddsg_b200.h"
 #include "device.cuh"
 #include "grid_host.hpp"
+#include "handles.hpp"
 #include "irbc.cuh"
 #include "program.hpp"
 
 using namespace ddsg_b200;
 
-namespace {
+using namespace ddsg_b200::abi;
 
-thread_local std::string g_last_error;
-thread_local std::vector<double> g_last_build_point;
-
-ddsg_status set_error(ddsg_status s, const std::string& msg) {
-  g_last_error = msg;
-  return s;
-}
-
-template <typename F>
-ddsg_status guarded(F&& f) {
-  try {
-    f();
-    return DDSG_OK;
-  } catch (const BuildError& e) {
-    g_last_build_point = e.point;
-    return set_error(e.status, e.what());
-  } catch (const Error& e) {
-    return set_error(e.status, e.what());
-  } catch (const std::bad_alloc&) {
-    return set_error(DDSG_OUT_OF_MEMORY, "host allocation failed");
-  } catch (const std::exception& e) {
-    return set_error(DDSG_INVALID_ARGUMENT, e.what());
-  } catch (...) {
-    return set_error(DDSG_INVALID_ARGUMENT, "unknown error");
-  }
-}
-
-int current_device() {
-  int dev = 0;
-  DDSG_CUDA(cudaGetDevice(&dev));
-  return dev;
-}
-
-// Device copies of a program, one per CUDA device that evaluated it.
-struct DeviceCache {
-  std::mutex mu;
-  std::map<int, std::unique_ptr<DeviceProgram>> per_device;
-  const DeviceProgram& get(const HostProgram& hp) {
-    const int dev = current_device();
-    std::lock_guard<std::mutex> lock(mu);
-    auto& slot = per_device[dev];
-    if (!slot) {
-      auto p = std::make_unique<DeviceProgram>();
-      p->upload(hp);
-      slot = std::move(p);
+std::unique_ptr<ddsg_hdmr> ddsg_b200::abi::make_hdmr(int d, int m, const double* f_anchor, int n_slots,
+                                                     const int32_t* slot_order, const int32_t* slot_dims,
+                                                     const int32_t* b, const HostGrid* const* grids,
+                                                     const std::vector<std::vector<int32_t>>& extra_accepted_dims) {
+  {
+    if (d < 1 || m < 1) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: d and m must be >= 1");
+    if (n_slots < 1 || !slot_order || !b || !f_anchor)
+      fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: inconsistent accepted family");
+    auto h = std::make_unique<ddsg_hdmr>();
+    h->d = d;
+    h->m = m;
+    h->f_anchor.assign(f_anchor, f_anchor + m);
+    int64_t dim_off = 0;
+    std::set<std::vector<int32_t>> accepted;
+    for (int s = 0; s < n_slots; ++s) {
+      const int k = slot_order[s];
+      if (k < 0 || k > d) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: slot order out of range");
+      ddsg_hdmr::Slot slot;
+      slot.dims.assign(slot_dims ? slot_dims + dim_off : nullptr, slot_dims ? slot_dims + dim_off + k : nullptr);
+      if (k > 0 && !slot_dims) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: null slot dims");
+      dim_off += k;
+      for (int j = 0; j < k; ++j) {
+        if (slot.dims[j] < 0 || slot.dims[j] >= d)
+          fail(DDSG_INVALID_ARGUMENT, "component index: dimension id out of range");
+        if (j > 0 && slot.dims[j] <= slot.dims[j - 1])
+          fail(DDSG_INVALID_ARGUMENT, "component index: dims must be strictly increasing");
+      }
+      slot.b = b[s];
+      if (s == 0 && k != 0) fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: inconsistent accepted family");
+      if (s > 0) {
+        // (order, lexicographic) ordering, strictly increasing (component_index.hpp:25-28)
+        const auto& prev = h->slots.back().dims;
+        const bool less = prev.size() != slot.dims.size() ? prev.size() < slot.dims.size() : prev < slot.dims;
+        if (!less) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: slots must be sorted by (order, lex) without duplicates");
+      }
+      if (k > 0) {
+        if (!grids || !grids[s])
+          fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: coefficient for a non-accepted index");
+        const HostGrid& G = *grids[s];
+        if (G.dim != k) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: grid dimension != slot order");
+        if (G.m != m) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: grid output length != m");
+        slot.grid = static_cast<int>(h->grids.size());
+        h->grids.push_back(G);
+        accepted.insert(slot.dims);
+      }
+      h->slots.push_back(std::move(slot));
     }
-    return *slot;
-  }
-  void invalidate() {
-    std::lock_guard<std::mutex> lock(mu);
-    per_device.clear();
-  }
-};
-
-}  // namespace
-
-struct ddsg_grid {
-  HostGrid g;
-  int eval_mode = DDSG_EVAL_EXACT;
-  std::mutex prog_mu;
-  std::unique_ptr<HostProgram> prog;
-  DeviceCache dev;
-
-  const HostProgram& program() {
-    std::lock_guard<std::mutex> lock(prog_mu);
-    if (!prog) {
-      auto hp = std::make_unique<HostProgram>();
-      hp->d = g.dim;
-      hp->m = g.m;
-      hp->plain = 1;
-      hp->f_anchor.assign(g.m, 0.0);
-      std::vector<int32_t> dims(g.dim);
-      for (int j = 0; j < g.dim; ++j) dims[j] = j;
-      hp->add_grid_slot(0, g, dims, 1.0);
-      hp->finish();
-      prog = std::move(hp);
+    for (const auto& u : extra_accepted_dims) accepted.insert(u);
+    // closure: every non-empty proper subset of an accepted index is accepted (ddsg_eval.hpp:63-70)
+    for (const auto& u : accepted) {
+      const size_t k = u.size();
+      for (size_t mask = 1; mask + 1 < (size_t{1} << k); ++mask) {
+        std::vector<int32_t> sub;
+        for (size_t j = 0; j < k; ++j)
+          if (mask & (size_t{1} << j)) sub.push_back(u[j]);
+        if (!accepted.count(sub)) {
+          auto str = [](const std::vector<int32_t>& v) {
+            std::string s = "{";
+            for (size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+            return s + "}";
+          };
+          fail(DDSG_INVALID_ARGUMENT,
+               "vectorized ddsg: accepted family misses subset " + str(sub) + " of " + str(u));
+        }
+      }
     }
-    return *prog;
+    HostProgram& hp = h->prog;
+    hp.d = d;
+    hp.m = m;
+    hp.plain = 0;
+    hp.f_anchor = h->f_anchor;
+    for (int s = 0; s < n_slots; ++s) {
+      const auto& slot = h->slots[s];
+      if (slot.b == 0) continue;
+      if (slot.dims.empty())
+        hp.add_empty_slot(s, static_cast<double>(slot.b));
+      else
+        hp.add_grid_slot(s, h->grids[slot.grid], slot.dims, static_cast<double>(slot.b));
+    }
+    hp.finish();
+    return h;
   }
-  void invalidate() {
-    std::lock_guard<std::mutex> lock(prog_mu);
-    prog.reset();
-    dev.invalidate();
-  }
-};
+}
 
-struct ddsg_hdmr {
-  int d = 0, m = 0;
-  std::vector<double> f_anchor;
-  struct Slot {
-    std::vector<int32_t> dims;
-    int32_t b = 0;
-    int grid = -1;  // index into grids
-  };
-  std::vector<Slot> slots;
-  std::vector<HostGrid> grids;
-  HostProgram prog;
-  int eval_mode = DDSG_EVAL_EXACT;
-  DeviceCache dev;
-};
 
 extern "C" {
 
@@ -196,8 +181,8 @@ ddsg_status ddsg_hierarchize(const ddsg_grid_t* g, int64_t n_new, const uint32_t
     }
     std::vector<double> interp(static_cast<size_t>(n_new) * G.m);
     auto* self = const_cast<ddsg_grid_t*>(g);
-    const DeviceProgram& prog = self->dev.get(self->program());
-    const int64_t bad = evaluate(prog, 1, x.data(), n_new, interp.data(), nullptr);
+    const auto prog = self->device();
+    const int64_t bad = evaluate(*prog, 1, x.data(), n_new, interp.data(), nullptr);
     if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "hierarchize: node outside the unit cube");
     for (int64_t i = 0; i < n_new * G.m; ++i) surplus_out[i] = f_values[i] - interp[i];
   });
@@ -272,8 +257,8 @@ ddsg_status ddsg_eval_grid(const ddsg_grid_t* g, const double* x, int64_t n, dou
     if (n < 0) fail(DDSG_INVALID_ARGUMENT, "eval_grid: negative point count");
     if (n > 0 && (!x || !y)) fail(DDSG_INVALID_ARGUMENT, "eval_grid: null buffers");
     auto* self = const_cast<ddsg_grid_t*>(g);
-    const DeviceProgram& prog = self->dev.get(self->program());
-    const int64_t bad = evaluate(prog, g->eval_mode == DDSG_EVAL_EXACT, x, n, y,
+    const auto prog = self->device();
+    const int64_t bad = evaluate(*prog, g->eval_mode == DDSG_EVAL_EXACT, x, n, y,
                                  static_cast<cudaStream_t>(stream));
     if (bad >= 0) {
       if (bad_index) *bad_index = bad;
@@ -289,8 +274,8 @@ ddsg_status ddsg_grid_support(const ddsg_grid_t* g, const double* x, int64_t n, 
     if (!g) fail(DDSG_INVALID_ARGUMENT, "grid_support: null grid");
     if (n > 0 && (!x || !nnz || !hash)) fail(DDSG_INVALID_ARGUMENT, "grid_support: null buffers");
     auto* self = const_cast<ddsg_grid_t*>(g);
-    const DeviceProgram& prog = self->dev.get(self->program());
-    const int64_t bad = support(prog, x, n, nnz, hash, static_cast<cudaStream_t>(stream));
+    const auto prog = self->device();
+    const int64_t bad = support(*prog, x, n, nnz, hash, static_cast<cudaStream_t>(stream));
     if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "grid_support: query outside the unit cube");
   });
 }
@@ -311,81 +296,10 @@ ddsg_status ddsg_hdmr_create(int d, int m, const double* f_anchor, int n_slots, 
                              ddsg_hdmr_t** out) {
   return guarded([&] {
     if (!out) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: null output handle");
-    if (d < 1 || m < 1) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: d and m must be >= 1");
-    if (n_slots < 1 || !slot_order || !b || !f_anchor)
-      fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: inconsistent accepted family");
-    auto h = std::make_unique<ddsg_hdmr>();
-    h->d = d;
-    h->m = m;
-    h->f_anchor.assign(f_anchor, f_anchor + m);
-    int64_t dim_off = 0;
-    std::set<std::vector<int32_t>> accepted;
-    for (int s = 0; s < n_slots; ++s) {
-      const int k = slot_order[s];
-      if (k < 0 || k > d) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: slot order out of range");
-      ddsg_hdmr::Slot slot;
-      slot.dims.assign(slot_dims ? slot_dims + dim_off : nullptr, slot_dims ? slot_dims + dim_off + k : nullptr);
-      if (k > 0 && !slot_dims) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: null slot dims");
-      dim_off += k;
-      for (int j = 0; j < k; ++j) {
-        if (slot.dims[j] < 0 || slot.dims[j] >= d)
-          fail(DDSG_INVALID_ARGUMENT, "component index: dimension id out of range");
-        if (j > 0 && slot.dims[j] <= slot.dims[j - 1])
-          fail(DDSG_INVALID_ARGUMENT, "component index: dims must be strictly increasing");
-      }
-      slot.b = b[s];
-      if (s == 0 && k != 0) fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: inconsistent accepted family");
-      if (s > 0) {
-        // (order, lexicographic) ordering, strictly increasing (component_index.hpp:25-28)
-        const auto& prev = h->slots.back().dims;
-        const bool less = prev.size() != slot.dims.size() ? prev.size() < slot.dims.size() : prev < slot.dims;
-        if (!less) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: slots must be sorted by (order, lex) without duplicates");
-      }
-      if (k > 0) {
-        if (!grids || !grids[s])
-          fail(DDSG_INVALID_ARGUMENT, "vectorized ddsg: coefficient for a non-accepted index");
-        const HostGrid& G = grids[s]->g;
-        if (G.dim != k) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: grid dimension != slot order");
-        if (G.m != m) fail(DDSG_INVALID_ARGUMENT, "hdmr_create: grid output length != m");
-        slot.grid = static_cast<int>(h->grids.size());
-        h->grids.push_back(G);
-        accepted.insert(slot.dims);
-      }
-      h->slots.push_back(std::move(slot));
-    }
-    // closure: every non-empty proper subset of an accepted index is accepted (ddsg_eval.hpp:63-70)
-    for (const auto& u : accepted) {
-      const size_t k = u.size();
-      for (size_t mask = 1; mask + 1 < (size_t{1} << k); ++mask) {
-        std::vector<int32_t> sub;
-        for (size_t j = 0; j < k; ++j)
-          if (mask & (size_t{1} << j)) sub.push_back(u[j]);
-        if (!accepted.count(sub)) {
-          auto str = [](const std::vector<int32_t>& v) {
-            std::string s = "{";
-            for (size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
-            return s + "}";
-          };
-          fail(DDSG_INVALID_ARGUMENT,
-               "vectorized ddsg: accepted family misses subset " + str(sub) + " of " + str(u));
-        }
-      }
-    }
-    HostProgram& hp = h->prog;
-    hp.d = d;
-    hp.m = m;
-    hp.plain = 0;
-    hp.f_anchor = h->f_anchor;
-    for (int s = 0; s < n_slots; ++s) {
-      const auto& slot = h->slots[s];
-      if (slot.b == 0) continue;
-      if (slot.dims.empty())
-        hp.add_empty_slot(s, static_cast<double>(slot.b));
-      else
-        hp.add_grid_slot(s, h->grids[slot.grid], slot.dims, static_cast<double>(slot.b));
-    }
-    hp.finish();
-    *out = h.release();
+    std::vector<const HostGrid*> gs(n_slots > 0 ? static_cast<size_t>(n_slots) : 0, nullptr);
+    if (grids)
+      for (int s = 0; s < n_slots; ++s) gs[s] = grids[s] ? &grids[s]->g : nullptr;
+    *out = make_hdmr(d, m, f_anchor, n_slots, slot_order, slot_dims, b, gs.data()).release();
   });
 }
 
@@ -416,12 +330,62 @@ ddsg_status ddsg_eval_hdmr(const ddsg_hdmr_t* h, const double* x, int64_t n, dou
     if (n < 0) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr: negative point count");
     if (n > 0 && (!x || !y)) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr: null buffers");
     auto* self = const_cast<ddsg_hdmr_t*>(h);
-    const DeviceProgram& prog = self->dev.get(h->prog);
-    const int64_t bad = evaluate(prog, h->eval_mode == DDSG_EVAL_EXACT, x, n, y,
+    const auto prog = self->dev.get(h->prog);
+    const int64_t bad = evaluate(*prog, h->eval_mode == DDSG_EVAL_EXACT, x, n, y,
                                  static_cast<cudaStream_t>(stream));
     if (bad >= 0) {
       if (bad_index) *bad_index = bad;
       fail(DDSG_DOMAIN_ERROR, "task " + std::to_string(bad) + " failed: ddsg: query outside unit cube");
+    }
+  });
+}
+
+ddsg_status ddsg_workspace_create(ddsg_workspace_t** out) {
+  return guarded([&] {
+    if (!out) fail(DDSG_INVALID_ARGUMENT, "workspace_create: null output handle");
+    *out = new ddsg_workspace();
+  });
+}
+
+ddsg_status ddsg_workspace_destroy(ddsg_workspace_t* ws) {
+  return guarded([&] { delete ws; });
+}
+
+ddsg_status ddsg_eval_hdmr_ws(const ddsg_hdmr_t* h, ddsg_workspace_t* ws, const double* x, int64_t n, double* y,
+                              int64_t* bad_index, uint64_t* interp_calls) {
+  if (bad_index) *bad_index = -1;
+  return guarded([&] {
+    if (!h || !ws) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr_ws: null handle");
+    if (n < 0) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr_ws: negative point count");
+    if (n > 0 && (!x || !y)) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr_ws: null buffers");
+    auto* self = const_cast<ddsg_hdmr_t*>(h);
+    const auto prog = self->dev.get(h->prog);
+    const int64_t bad = evaluate_staged(*prog, h->eval_mode == DDSG_EVAL_EXACT, x, n, y, ws->ws);
+    if (bad >= 0) {
+      if (bad_index) *bad_index = bad;
+      fail(DDSG_DOMAIN_ERROR, "ddsg: query outside unit cube");
+    }
+    if (interp_calls) {  // ddsg_eval.hpp:103: one count per active non-empty slot and point
+      uint64_t per_point = 0;
+      for (int32_t k : h->prog.slot_k) per_point += k > 0 ? 1u : 0u;
+      *interp_calls += per_point * static_cast<uint64_t>(n);
+    }
+  });
+}
+
+ddsg_status ddsg_eval_grid_ws(const ddsg_grid_t* g, ddsg_workspace_t* ws, const double* x, int64_t n, double* y,
+                              int64_t* bad_index) {
+  if (bad_index) *bad_index = -1;
+  return guarded([&] {
+    if (!g || !ws) fail(DDSG_INVALID_ARGUMENT, "eval_grid_ws: null handle");
+    if (n < 0) fail(DDSG_INVALID_ARGUMENT, "eval_grid_ws: negative point count");
+    if (n > 0 && (!x || !y)) fail(DDSG_INVALID_ARGUMENT, "eval_grid_ws: null buffers");
+    auto* self = const_cast<ddsg_grid_t*>(g);
+    const auto prog = self->device();
+    const int64_t bad = evaluate_staged(*prog, g->eval_mode == DDSG_EVAL_EXACT, x, n, y, ws->ws);
+    if (bad >= 0) {
+      if (bad_index) *bad_index = bad;
+      fail(DDSG_DOMAIN_ERROR, "sparse grid: query outside the unit cube");
     }
   });
 }
@@ -432,8 +396,8 @@ ddsg_status ddsg_hdmr_support(const ddsg_hdmr_t* h, const double* x, int64_t n, 
     if (!h) fail(DDSG_INVALID_ARGUMENT, "hdmr_support: null handle");
     if (n > 0 && (!x || !nnz || !hash)) fail(DDSG_INVALID_ARGUMENT, "hdmr_support: null buffers");
     auto* self = const_cast<ddsg_hdmr_t*>(h);
-    const DeviceProgram& prog = self->dev.get(h->prog);
-    const int64_t bad = support(prog, x, n, nnz, hash, static_cast<cudaStream_t>(stream));
+    const auto prog = self->dev.get(h->prog);
+    const int64_t bad = support(*prog, x, n, nnz, hash, static_cast<cudaStream_t>(stream));
     if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "hdmr_support: query outside unit cube");
   });
 }
@@ -473,7 +437,7 @@ ddsg_status ddsg_hdmr_kernel_path(const ddsg_hdmr_t* h, int* fast_path) {
   return guarded([&] {
     if (!h || !fast_path) fail(DDSG_INVALID_ARGUMENT, "hdmr_kernel_path: null argument");
     auto* self = const_cast<ddsg_hdmr_t*>(h);
-    *fast_path = self->dev.get(h->prog).fast() != nullptr ? 1 : 0;
+    *fast_path = self->dev.get(h->prog)->fast() != nullptr ? 1 : 0;
   });
 }
 
@@ -523,19 +487,19 @@ irbc::PolicyFn irbc_policy(const ddsg_hdmr_t* h, const ddsg_grid_t* g, const irb
   if ((h == nullptr) == (g == nullptr))
     fail(DDSG_INVALID_ARGUMENT, "irbc: exactly one of policy_hdmr / policy_grid must be given");
   int d = 0, m = 0, exact = 1;
-  const DeviceProgram* prog = nullptr;
+  std::shared_ptr<const DeviceProgram> prog;
   if (h) {
     auto* self = const_cast<ddsg_hdmr_t*>(h);
     d = h->d;
     m = h->m;
     exact = h->eval_mode == DDSG_EVAL_EXACT;
-    prog = &self->dev.get(h->prog);
+    prog = self->dev.get(h->prog);
   } else {
     auto* self = const_cast<ddsg_grid_t*>(g);
     d = g->g.dim;
     m = g->g.m;
     exact = g->eval_mode == DDSG_EVAL_EXACT;
-    prog = &self->dev.get(self->program());
+    prog = self->device();
   }
   if (d != p.state_dim() || m != p.pdim())
     fail(DDSG_INVALID_ARGUMENT, "irbc: policy dimensions do not match the model (dim 2N, out_dim pdim)");

@@ -104,6 +104,28 @@ void ensure_dynamic_smem(const void* fn, size_t bytes);
 int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,
                  cudaStream_t stream);
 
+// Pinned-staging workspace for ordinary (pageable) host buffers
+// (EvalWorkspace, ddsg_eval.hpp:21-24): two pinned host slots, two device
+// slots and two streams on the device current at first use; chunk i's host
+// copy-in overlaps chunk i-1's transfers and kernels.
+class StagedWorkspace {
+ public:
+  StagedWorkspace();
+  ~StagedWorkspace();
+  StagedWorkspace(const StagedWorkspace&) = delete;
+  StagedWorkspace& operator=(const StagedWorkspace&) = delete;
+  struct Impl;
+  Impl* impl() { return impl_; }
+
+ private:
+  Impl* impl_;
+};
+
+// Evaluates n points held in pageable host memory through `ws`.  Returns the
+// lowest out-of-domain point index or -1.
+int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,
+                        StagedWorkspace& ws);
+
 // Support statistics (nnz and order-sensitive hash per point).
 int64_t support(const DeviceProgram& prog, const double* x, int64_t n, int64_t* nnz,
                 uint64_t* hash, cudaStream_t stream);

@@ -19,6 +19,8 @@
 #include <climits>
 #include <cstring>
 #include <memory>
+#include <thread>
+#include <vector>
 
 #include "basis.cuh"
 #include "device.cuh"
@@ -312,6 +314,17 @@ bool is_device_ptr(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// Ordinary (pageable) host memory: not device memory and not page-locked.
+bool is_pageable(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return attr.type == cudaMemoryTypeUnregistered;
+}
+
 struct Scratch {
   void* ptr = nullptr;
   size_t bytes = 0;
@@ -436,7 +449,17 @@ int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t 
     stats.main_ms = kernel_timer().collect();
     return bad == ULLONG_MAX ? -1 : static_cast<int64_t>(bad);
   }
-  // Host (or mixed) buffers: pipeline H2D -> kernel -> D2H over three streams.
+  if (!x_dev && !y_dev && is_pageable(x) && is_pageable(y)) {
+    // ordinary host memory (std::vector, numpy): stage through pinned buffers
+    DDSG_CUDA(cudaStreamSynchronize(stream));
+    static thread_local std::unique_ptr<StagedWorkspace> per_dev[kMaxDevices];
+    int dev = 0;
+    DDSG_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDevices) fail(DDSG_CUDA_ERROR, "device ordinal out of range");
+    if (!per_dev[dev]) per_dev[dev].reset(new StagedWorkspace());
+    return evaluate_staged(prog, exact, x, n, y, *per_dev[dev]);
+  }
+  // Pinned host (or mixed) buffers: pipeline H2D -> kernel -> D2H over three streams.
   DDSG_CUDA(cudaStreamSynchronize(stream));
   DDSG_CUDA(cudaMemcpy(dbad, &init, sizeof(init), cudaMemcpyHostToDevice));
   const int64_t bytes_per_pt = static_cast<int64_t>(d + m) * 8;
@@ -465,6 +488,131 @@ int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t 
   unsigned long long bad = 0;
   DDSG_CUDA(cudaMemcpy(&bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost));
   return bad == ULLONG_MAX ? -1 : static_cast<int64_t>(bad);
+}
+
+// ------------------------------------------------- pinned-staging workspace
+
+namespace {
+
+struct Pinned {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* get(size_t want) {
+    if (want > bytes) {
+      if (ptr) cudaFreeHost(ptr);
+      ptr = nullptr;
+      bytes = 0;
+      DDSG_CUDA(cudaMallocHost(&ptr, want));
+      bytes = want;
+    }
+    return ptr;
+  }
+  ~Pinned() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+};
+
+// memcpy of large host blocks on a few threads (one thread moves ~10 GB/s;
+// PCIe 5 moves ~50).
+void host_copy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPerThread = size_t{8} << 20;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>({bytes / kPerThread, 8, hw});
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const size_t part = (bytes + nt - 1) / nt;
+  for (size_t t = 0; t < nt; ++t) {
+    const size_t a = t * part, b = std::min(bytes, a + part);
+    if (a >= b) break;
+    pool.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+struct StagedWorkspace::Impl {
+  int device = -1;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  cudaEvent_t init = nullptr;
+  Pinned hx[2], hy[2], hbad;
+  Scratch dx[2], dy[2], bad, xt[2];
+  void bind() {
+    int dev = 0;
+    DDSG_CUDA(cudaGetDevice(&dev));
+    if (device == dev) return;
+    if (device >= 0) fail(DDSG_INVALID_ARGUMENT, "workspace used on a second device (create one per device)");
+    device = dev;
+    for (int b = 0; b < 2; ++b) {
+      DDSG_CUDA(cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking));
+      DDSG_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+    }
+    DDSG_CUDA(cudaEventCreateWithFlags(&init, cudaEventDisableTiming));
+  }
+  ~Impl() {
+    for (int b = 0; b < 2; ++b) {
+      if (st[b]) cudaStreamDestroy(st[b]);
+      if (done[b]) cudaEventDestroy(done[b]);
+    }
+    if (init) cudaEventDestroy(init);
+  }
+};
+
+StagedWorkspace::StagedWorkspace() : impl_(new Impl()) {}
+StagedWorkspace::~StagedWorkspace() { delete impl_; }
+
+int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,
+                        StagedWorkspace& wso) {
+  EvalStats& stats = last_stats();
+  stats = EvalStats{};
+  kernel_timer().collect();
+  if (n <= 0) return -1;
+  StagedWorkspace::Impl& ws = *wso.impl();
+  ws.bind();
+  const int d = prog.host().d, m = prog.host().m;
+  const int64_t bytes_per_pt = static_cast<int64_t>(d + m) * 8;
+  const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(1024, (int64_t{64} << 20) / bytes_per_pt));
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  auto* dbad = static_cast<unsigned long long*>(ws.bad.get(sizeof(unsigned long long)));
+  auto* hbad = static_cast<unsigned long long*>(ws.hbad.get(sizeof(unsigned long long)));
+  DDSG_CUDA(cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), ws.st[0]));  // ULLONG_MAX
+  DDSG_CUDA(cudaEventRecord(ws.init, ws.st[0]));
+  DDSG_CUDA(cudaStreamWaitEvent(ws.st[1], ws.init, 0));
+  const int nb = nchunks > 1 ? 2 : 1;
+  for (int b = 0; b < nb; ++b) {
+    ws.hx[b].get(static_cast<size_t>(chunk) * d * 8);
+    ws.hy[b].get(static_cast<size_t>(chunk) * m * 8);
+    ws.dx[b].get(static_cast<size_t>(chunk) * d * 8);
+    ws.dy[b].get(static_cast<size_t>(chunk) * m * 8);
+  }
+  auto drain = [&](int64_t i) {  // chunk i's outputs to the caller
+    const int b = static_cast<int>(i & 1);
+    const int64_t off = i * chunk, cnt = std::min(chunk, n - off);
+    DDSG_CUDA(cudaEventSynchronize(ws.done[b]));
+    host_copy(y + off * m, ws.hy[b].ptr, static_cast<size_t>(cnt) * m * 8);
+  };
+  for (int64_t i = 0; i < nchunks; ++i) {
+    const int b = static_cast<int>(i & 1);
+    const int64_t off = i * chunk, cnt = std::min(chunk, n - off);
+    if (i >= 2) drain(i - 2);  // frees slot b
+    host_copy(ws.hx[b].ptr, x + off * d, static_cast<size_t>(cnt) * d * 8);
+    cudaStream_t st = ws.st[b];
+    DDSG_CUDA(cudaMemcpyAsync(ws.dx[b].ptr, ws.hx[b].ptr, cnt * d * 8, cudaMemcpyHostToDevice, st));
+    stats.launches += launch_eval(prog, exact, static_cast<const double*>(ws.dx[b].ptr), cnt, off,
+                                  static_cast<double*>(ws.dy[b].ptr), dbad, st, ws.xt[b]);
+    DDSG_CUDA(cudaMemcpyAsync(ws.hy[b].ptr, ws.dy[b].ptr, cnt * m * 8, cudaMemcpyDeviceToHost, st));
+    DDSG_CUDA(cudaEventRecord(ws.done[b], st));
+  }
+  for (int64_t i = std::max<int64_t>(0, nchunks - 2); i < nchunks; ++i) drain(i);
+  // both streams are idle now; the lowest bad index is final
+  DDSG_CUDA(cudaMemcpyAsync(hbad, dbad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.st[0]));
+  DDSG_CUDA(cudaStreamSynchronize(ws.st[0]));
+  stats.main_ms = kernel_timer().collect();
+  return *hbad == ULLONG_MAX ? -1 : static_cast<int64_t>(*hbad);
 }
 
 int64_t support(const DeviceProgram& prog, const double* x, int64_t n, int64_t* nnz, uint64_t* hash,

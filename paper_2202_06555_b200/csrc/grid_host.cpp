@@ -187,6 +187,14 @@ void HostGrid::append(int64_t n, const uint32_t* k, const double* s) {
       throw;
     }
   }
+  // The reference's build caps the level sum at max_level + dim - 1
+  // (sparse_grid.hpp:89-107): a grid refined past that cap is the build of
+  // the level that admits its deepest level sum, so max_level follows it.
+  for (int64_t i = 0; i < n; ++i) {
+    int ls = 0;
+    for (int j = 0; j < dim; ++j) ls += level_of(k[i * dim + j]);
+    max_level = std::max(max_level, ls - dim + 1);
+  }
 }
 
 std::vector<double> HostGrid::quadrature() const {

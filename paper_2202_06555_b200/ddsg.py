@@ -100,6 +100,50 @@ def _as_points(x, dim: int):
     return t.contiguous(), t.shape[0], single
 
 
+def _check_out(out, arr, n: int, m: int) -> None:
+    """A caller-supplied output must be exactly what the C call writes:
+    [n][m] float64, C-contiguous, in the same memory (host / device) as x."""
+    if isinstance(out, np.ndarray):
+        if not isinstance(arr, np.ndarray):
+            raise InvalidArgument("out is host memory but the points are on the device")
+        if out.dtype != np.float64 or out.shape != (n, m) or not out.flags["C_CONTIGUOUS"]:
+            raise InvalidArgument(f"out must be a C-contiguous float64 array of shape ({n}, {m})")
+        return
+    if not hasattr(out, "data_ptr"):
+        raise InvalidArgument("out must be a numpy array or a torch tensor")
+    import torch
+
+    if isinstance(arr, np.ndarray) or out.device != arr.device:
+        raise InvalidArgument("out must be on the same device as the points")
+    if out.dtype != torch.float64 or tuple(out.shape) != (n, m) or not out.is_contiguous():
+        raise InvalidArgument(f"out must be a contiguous float64 tensor of shape ({n}, {m})")
+
+
+class _DeviceScope:
+    """For torch CUDA points: runs the C call on the tensor's device and, by
+    default, on torch's current stream of that device (torch pool streams are
+    non-blocking, so the legacy default stream would not order after them)."""
+
+    def __init__(self, arr, stream):
+        self.arr, self.stream, self.ctx = arr, stream, None
+
+    def __enter__(self) -> int:
+        if isinstance(self.arr, np.ndarray) or not getattr(self.arr, "is_cuda", False):
+            return int(self.stream or 0)
+        import torch
+
+        self.ctx = torch.cuda.device(self.arr.device)
+        self.ctx.__enter__()
+        if self.stream is None:
+            return int(torch.cuda.current_stream(self.arr.device).cuda_stream)
+        return int(self.stream)
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            self.ctx.__exit__(*exc)
+        return False
+
+
 def _alloc_out(like, n: int, m: int):
     if isinstance(like, np.ndarray):
         return np.empty((n, m), dtype=np.float64)
@@ -202,15 +246,24 @@ class SparseGridFunction:
         return q
 
     def append(self, keys: np.ndarray, surplus: np.ndarray) -> None:
+        """Appends refinement nodes; max_level follows the deepest level sum
+        (the level of the reference build that admits it)."""
         keys = np.ascontiguousarray(keys, dtype=np.uint32).reshape(-1, self.dim)
         surplus = np.ascontiguousarray(surplus, dtype=np.float64).reshape(-1, self.out_dim)
+        if keys.shape[0] != surplus.shape[0]:
+            raise InvalidArgument("grid append: keys and surplus row counts differ")
         _check(N.lib.ddsg_grid_append(self._h, keys.shape[0], _ptr(keys), _ptr(surplus)))
+        lvl = C.c_int()
+        _check(N.lib.ddsg_grid_info(self._h, None, None, None, C.byref(lvl), None, None))
+        self.max_level = lvl.value
 
     def hierarchize(self, keys: np.ndarray, f_values: np.ndarray, device: bool = True) -> np.ndarray:
         """surplus = f - interpolate(grid, x(key)) for new nodes (sparse_grid.hpp:264-276);
         device=True evaluates on the GPU, False on the host (both bit-identical)."""
         keys = np.ascontiguousarray(keys, dtype=np.uint32).reshape(-1, self.dim)
         f_values = np.ascontiguousarray(f_values, dtype=np.float64).reshape(-1, self.out_dim)
+        if f_values.shape[0] != keys.shape[0]:
+            raise InvalidArgument("hierarchize: f_values rows != keys rows")
         out = np.empty_like(f_values)
         fn = N.lib.ddsg_hierarchize if device else N.lib.ddsg_hierarchize_host
         _check(fn(self._h, keys.shape[0], _ptr(keys), _ptr(f_values), _ptr(out)))
@@ -230,13 +283,31 @@ class SparseGridFunction:
         _check(N.lib.ddsg_grid_set_eval_mode(self._h, mode))
 
     # --- evaluation
-    def interpolate(self, x, out=None, stream: int = 0):
+    def interpolate(self, x, out=None, stream: Optional[int] = None):
         arr, n, single = _as_points(x, self.dim)
-        y = _alloc_out(arr, n, self.out_dim) if out is None else out
+        if out is None:
+            y = _alloc_out(arr, n, self.out_dim)
+        else:
+            _check_out(out, arr, n, self.out_dim)
+            y = out
         bad = C.c_int64(-1)
-        st = N.lib.ddsg_eval_grid(self._h, _ptr(arr), n, _ptr(y), C.byref(bad), C.c_void_p(stream))
+        with _DeviceScope(arr, stream) as st_handle:
+            st = N.lib.ddsg_eval_grid(self._h, _ptr(arr), n, _ptr(y), C.byref(bad), C.c_void_p(st_handle))
         _check(st, bad.value)
         return y[0] if single else y
+
+    # --- JSON documents (serialize.hpp:31-77), through the C-ABI
+    @staticmethod
+    def from_json(text) -> "SparseGridFunction":
+        """sparse_grid_from_json (serialize.hpp:54-77)."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        out = C.c_void_p()
+        _check(N.lib.ddsg_grid_from_json(data, len(data), C.byref(out)))
+        return SparseGridFunction(out.value)
+
+    def to_json(self) -> str:
+        """to_json(SparseGridFunction) (serialize.hpp:31-52) as save_json's text."""
+        return _read_text(lambda buf, cap, n: N.lib.ddsg_grid_to_json(self._h, buf, cap, n))
 
     def support(self, x):
         arr, n, _ = _as_points(x, self.dim)
@@ -285,13 +356,81 @@ class VectorizedDdsg:
     def set_eval_mode(self, mode: int) -> None:
         _check(N.lib.ddsg_hdmr_set_eval_mode(self._h, mode))
 
-    def evaluate_batch(self, xs, out=None, stream: int = 0):
+    def evaluate_batch(self, xs, out=None, stream: Optional[int] = None):
         arr, n, single = _as_points(xs, self.d)
-        y = _alloc_out(arr, n, self.out_dim) if out is None else out
+        if out is None:
+            y = _alloc_out(arr, n, self.out_dim)
+        else:
+            _check_out(out, arr, n, self.out_dim)
+            y = out
         bad = C.c_int64(-1)
-        st = N.lib.ddsg_eval_hdmr(self._h, _ptr(arr), n, _ptr(y), C.byref(bad), C.c_void_p(stream))
+        with _DeviceScope(arr, stream) as st_handle:
+            st = N.lib.ddsg_eval_hdmr(self._h, _ptr(arr), n, _ptr(y), C.byref(bad), C.c_void_p(st_handle))
         _check(st, bad.value)
         return y[0] if single else y
+
+    # --- JSON documents (serialize.hpp:84-145), through the C-ABI
+    @staticmethod
+    def from_json(text) -> "VectorizedDdsg":
+        """ddsg_from_json (serialize.hpp:112-145) + compile.  .slots holds
+        (dims, b, grid or None) in coeff_b order."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        out = C.c_void_p()
+        _check(N.lib.ddsg_hdmr_from_json(data, len(data), C.byref(out)))
+        self = VectorizedDdsg.__new__(VectorizedDdsg)
+        self._h = out
+        info = self.info()
+        self.d, self.out_dim = info["d"], info["m"]
+        self.slots = [self.slot(s) for s in range(info["n_slots"])]
+        return self
+
+    def slot(self, s: int):
+        """Slot s (VectorizedDdsg::slots(), ddsg_eval.hpp:77): (dims, b, grid copy or None)."""
+        order, b, g = C.c_int(), C.c_int32(), C.c_void_p()
+        dims = np.zeros(max(self.d, 1), dtype=np.int32)
+        _check(N.lib.ddsg_hdmr_slot(self._h, s, C.byref(order), _ptr(dims), C.byref(b), C.byref(g)))
+        grid = SparseGridFunction(g.value) if g.value else None
+        return tuple(int(v) for v in dims[: order.value]), int(b.value), grid
+
+    def set_document(self, k_max: int, anchor_coords, rejected=(), cut_quadratures=None) -> None:
+        """DdsgFunction fields a document carries beyond evaluation (k_max,
+        anchor coords, rejected indices, cut quadratures [n_slots][m])."""
+        coords = np.ascontiguousarray(anchor_coords, dtype=np.float64)
+        if coords.shape != (self.d,):
+            raise InvalidArgument("anchor coordinates length != dim")
+        rej = [tuple(int(v) for v in u) for u in rejected]
+        rorder = np.array([len(u) for u in rej] or [0], dtype=np.int32)
+        rdims = np.array([v for u in rej for v in u] or [0], dtype=np.int32)
+        q = None
+        if cut_quadratures is not None:
+            q = np.ascontiguousarray(cut_quadratures, dtype=np.float64)
+            if q.shape != (len(self.slots), self.out_dim):
+                raise InvalidArgument("cut quadratures must be [n_slots][m]")
+        _check(N.lib.ddsg_hdmr_set_document(self._h, int(k_max), _ptr(coords), len(rej), _ptr(rorder), _ptr(rdims),
+                                            _ptr(q)))
+
+    def document(self):
+        """(k_max, anchor coords, f_anchor, rejected list, cut quadratures or None)."""
+        k, nr, nrd, hq = C.c_int(), C.c_int(), C.c_int64(), C.c_int()
+        _check(N.lib.ddsg_hdmr_document(self._h, C.byref(k), None, None, C.byref(nr), C.byref(nrd), None, None,
+                                        C.byref(hq), None))
+        coords = np.empty(self.d)
+        fa = np.empty(self.out_dim)
+        rorder = np.zeros(max(nr.value, 1), dtype=np.int32)
+        rdims = np.zeros(max(nrd.value, 1), dtype=np.int32)
+        q = np.empty((len(self.slots), self.out_dim)) if hq.value else None
+        _check(N.lib.ddsg_hdmr_document(self._h, None, _ptr(coords), _ptr(fa), None, None, _ptr(rorder), _ptr(rdims),
+                                        None, _ptr(q)))
+        rej, off = [], 0
+        for r in range(nr.value):
+            rej.append(tuple(int(v) for v in rdims[off: off + rorder[r]]))
+            off += int(rorder[r])
+        return k.value, coords, fa, rej, q
+
+    def to_json(self) -> str:
+        """to_json(DdsgFunction) (serialize.hpp:84-110) as save_json's text;
+        needs set_document (or a document-loaded object)."""
+        return _read_text(lambda buf, cap, n: N.lib.ddsg_hdmr_to_json(self._h, buf, cap, n))
 
     evaluate = evaluate_batch
 
@@ -311,6 +450,14 @@ class VectorizedDdsg:
         v = C.c_int()
         _check(N.lib.ddsg_hdmr_kernel_path(self._h, C.byref(v)))
         return bool(v.value)
+
+
+def _read_text(writer) -> str:
+    n = C.c_int64()
+    _check(writer(None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(writer(C.cast(buf, C.c_void_p), n.value + 1, C.byref(n)))
+    return buf.raw[: n.value].decode()
 
 
 def last_eval_stats():

@@ -30,7 +30,7 @@ from typing import List, Optional, Tuple
 import numpy as np
 
 from . import _native as N
-from .ddsg import InvalidArgument, SparseGridFunction, VectorizedDdsg, _check, _ptr, uniform_points
+from .ddsg import InvalidArgument, SparseGridFunction, VectorizedDdsg, _check, _DeviceScope, _ptr, uniform_points
 
 SMOOTH, NONSMOOTH = 0, 1  # irbc.hpp:25 Variant
 
@@ -161,7 +161,7 @@ def _empty(like, shape, dtype=np.float64):
     return torch.empty(shape, dtype=tdt, device=like.device)
 
 
-def foc_residuals(policy, p: IrbcParameters, a, k, candidate, stream: int = 0):
+def foc_residuals(policy, p: IrbcParameters, a, k, candidate, stream: Optional[int] = None):
     """Residuals [n][pdim] and clamped-successor counts [n] of n states."""
     Nc, pd = p.countries, p.policy_dim()
     a, n = _buf(a, Nc, "a")
@@ -174,13 +174,15 @@ def foc_residuals(policy, p: IrbcParameters, a, k, candidate, stream: int = 0):
     hd, gd = _handles(policy)
     s, g, t = p._c()
     bad = C.c_int64(-1)
-    st = N.lib.ddsg_irbc_foc_residuals(hd, gd, C.byref(s), n, _ptr(a), _ptr(k), _ptr(cand), _ptr(res),
-                                       _ptr(clamped), C.byref(bad), C.c_void_p(stream))
+    with _DeviceScope(a, stream) as sh:
+        st = N.lib.ddsg_irbc_foc_residuals(hd, gd, C.byref(s), n, _ptr(a), _ptr(k), _ptr(cand), _ptr(res),
+                                           _ptr(clamped), C.byref(bad), C.c_void_p(sh))
     _check(st, bad.value)
     return res, clamped
 
 
-def foc_jacobian(policy, p: IrbcParameters, a, k, z, r0, fd_epsilon: float = 1e-7, stream: int = 0):
+def foc_jacobian(policy, p: IrbcParameters, a, k, z, r0, fd_epsilon: float = 1e-7,
+                 stream: Optional[int] = None):
     """Forward-difference Newton matrices jac[n][pdim][pdim] (solver.hpp:129-165;
     SolverConfig::fd_epsilon default 1e-7, solver.hpp:40)."""
     Nc, pd = p.countries, p.policy_dim()
@@ -194,8 +196,9 @@ def foc_jacobian(policy, p: IrbcParameters, a, k, z, r0, fd_epsilon: float = 1e-
     hd, gd = _handles(policy)
     s, g, t = p._c()
     bad = C.c_int64(-1)
-    st = N.lib.ddsg_irbc_foc_jacobian(hd, gd, C.byref(s), n, _ptr(a), _ptr(k), _ptr(z), _ptr(r0),
-                                      float(fd_epsilon), _ptr(jac), C.byref(bad), C.c_void_p(stream))
+    with _DeviceScope(a, stream) as sh:
+        st = N.lib.ddsg_irbc_foc_jacobian(hd, gd, C.byref(s), n, _ptr(a), _ptr(k), _ptr(z), _ptr(r0),
+                                          float(fd_epsilon), _ptr(jac), C.byref(bad), C.c_void_p(sh))
     _check(st, bad.value)
     return jac
 
@@ -210,7 +213,7 @@ class EulerErrors:
     clamp_count: int = 0
 
 
-def euler_errors_at(policy, p: IrbcParameters, xs, stream: int = 0) -> EulerErrors:
+def euler_errors_at(policy, p: IrbcParameters, xs, stream: Optional[int] = None) -> EulerErrors:
     """euler_errors on caller-supplied canonical samples xs[n][2N]."""
     xs, n = _buf(xs, p.state_dim(), "xs")
     if n < 1:
@@ -220,8 +223,9 @@ def euler_errors_at(policy, p: IrbcParameters, xs, stream: int = 0) -> EulerErro
     hd, gd = _handles(policy)
     s, g, t = p._c()
     bad = C.c_int64(-1)
-    st = N.lib.ddsg_irbc_euler_errors(hd, gd, C.byref(s), n, _ptr(xs), _ptr(errs), C.byref(mean), C.byref(worst),
-                                      C.byref(cl), C.byref(bad), C.c_void_p(stream))
+    with _DeviceScope(xs, stream) as sh:
+        st = N.lib.ddsg_irbc_euler_errors(hd, gd, C.byref(s), n, _ptr(xs), _ptr(errs), C.byref(mean),
+                                          C.byref(worst), C.byref(cl), C.byref(bad), C.c_void_p(sh))
     _check(st, bad.value)
     # solver.hpp:431-432 (host log10, as the reference)
     m, w = mean.value, worst.value
@@ -230,7 +234,7 @@ def euler_errors_at(policy, p: IrbcParameters, xs, stream: int = 0) -> EulerErro
 
 
 def euler_errors(policy, p: IrbcParameters, n_samples: int, seed: int, workers: Optional[int] = None,
-                 stream: int = 0) -> EulerErrors:
+                 stream: Optional[int] = None) -> EulerErrors:
     """solver.hpp:377-436: samples from std::mt19937_64(seed) +
     uniform_real_distribution(0,1), drawn up front (``workers`` is accepted for
     signature parity; the result never depends on it)."""

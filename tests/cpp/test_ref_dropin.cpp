@@ -1,0 +1,258 @@
+// TEST INFRASTRUCTURE: the reference headers (ddsg::, compiled in place from
+// /root/reference/proj/include) beside the B200 shim (ddsg_b200::), driven
+// through the reference's own call shapes with only the namespace changed.
+// Built by `make -C oracle dropin` (where the reference exists) into
+// oracle/_ref/test_ref_dropin; run by tests/test_cpp_dropin.py on the GPU.
+//
+//   1. ddsg::decompose (hdmr.hpp:364) builds a vector-valued decomposition
+//      (adaptive cut grids, so stored node orders are not canonical);
+//   2. INTEGRATION.md's to_b200() -- #included verbatim (to_b200.inc) --
+//      converts it;
+//   3. compiled_evaluator (time_iteration.hpp:86-91) is written once per
+//      namespace, identical text; evaluate(x, out, ws, &calls)
+//      (tools/ddsg.cpp:376), evaluate(x, out) and evaluate_batch(xs,
+//      workers) must agree bit for bit, with equal interp_calls;
+//   4. the reference writes policy.json (save_json(to_json(...)),
+//      tools/ddsg.cpp:217); ddsg_b200::ddsg_from_json(load_json(path)) loads
+//      it through the C-ABI (tools/ddsg.cpp:261-268 shape) and evaluates it
+//      on the GPU bit-exactly; the shim's writer is read back by the
+//      reference's ddsg_from_json, same bits;
+//   5. slots(), cut quadratures, exception types.
+// Exit code = number of failed checks.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <functional>
+#include <memory>
+#include <random>
+#include <span>
+#include <string>
+#include <vector>
+
+#include <unistd.h>
+
+#include "ddsg/ddsg_eval.hpp"
+#include "ddsg/hdmr.hpp"
+#include "ddsg/serialize.hpp"
+#include "ddsg_b200.hpp"
+
+#include "to_b200.inc"  // INTEGRATION.md, BEGIN/END to_b200, verbatim
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    if (cond) {                                                            \
+      ++g_pass;                                                            \
+    } else {                                                               \
+      ++g_fail;                                                            \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+    }                                                                      \
+  } while (0)
+
+using PolicyEvaluator = std::function<void(std::span<const double>, std::span<double>)>;  // irbc.hpp:211
+
+// time_iteration.hpp:86-91, once per namespace (identical text)
+namespace ref_side {
+using namespace ddsg;
+inline PolicyEvaluator compiled_evaluator(std::shared_ptr<const VectorizedDdsg> vec) {
+  return [vec](std::span<const double> x, std::span<double> out) {
+    thread_local EvalWorkspace ws;
+    vec->evaluate(x, out, ws);
+  };
+}
+}  // namespace ref_side
+namespace b200_side {
+using namespace ddsg_b200;
+inline PolicyEvaluator compiled_evaluator(std::shared_ptr<const VectorizedDdsg> vec) {
+  return [vec](std::span<const double> x, std::span<double> out) {
+    thread_local EvalWorkspace ws;
+    vec->evaluate(x, out, ws);
+  };
+}
+}  // namespace b200_side
+
+static bool same_bits(const std::vector<double>& a, const std::vector<double>& b) {
+  return a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * sizeof(double)) == 0;
+}
+
+template <typename E, typename F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+// A kinked vector-valued target on [0,1]^6 (3 outputs) with sparse
+// coupling: the cut grids refine adaptively, pairs without interaction are
+// rejected by eta, and the coefficients include zero and negative b.
+static void target(std::span<const double> x, std::span<double> out) {
+  out[0] = std::exp(-0.5 * (x[0] + x[1])) + 0.3 * x[2] * x[3];
+  out[1] = std::max(0.0, x[0] + x[4] - 1.1) + 0.1 * x[5] * x[5];
+  out[2] = std::log(1.0 + x[3] + 0.5 * x[4]) + x[1];
+}
+
+int main() {
+  const int d = 6, m = 3;
+  ddsg::AnchorPoint anchor;
+  anchor.coords.assign(d, 0.5);
+  ddsg::DdsgOptions opt;
+  opt.k_max = 2;
+  opt.max_level = 5;
+  opt.eps_gamma = 1e-3;
+  opt.eps_eta = 1e-8;  // prunes the non-interacting pairs: a non-trivial rejected set
+  opt.mode = ddsg::BoundaryMode::modified_linear;
+  opt.workers = 4;
+  auto dd = std::make_shared<const ddsg::DdsgFunction>(ddsg::decompose(target, d, m, anchor, opt));
+  auto vec_ref = std::make_shared<const ddsg::VectorizedDdsg>(ddsg::VectorizedDdsg::compile(dd));
+  auto vec_gpu = std::make_shared<const ddsg_b200::VectorizedDdsg>(to_b200(*dd));
+  std::printf("decompose: %zu accepted, %zu rejected, %zu slots\n", dd->accepted().size(), dd->rejected().size(),
+              vec_ref->slots().size());
+  std::fflush(stdout);
+  CHECK(!dd->rejected().empty());
+
+  // seeded points, as oracles.hpp:45-53 (plus cell boundaries and the faces)
+  std::mt19937_64 rng(2022);
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  std::vector<std::vector<double>> pts(3000, std::vector<double>(d));
+  for (auto& x : pts)
+    for (auto& c : x) c = unif(rng);
+  for (int i = 0; i < 64; ++i)
+    for (int j = 0; j < d; ++j) pts[i][j] = static_cast<double>((i * 7 + j * 3) % 33) / 32.0;
+
+  // 3. compiled_evaluator, counted evaluate, two-argument evaluate, batch
+  {
+    auto f_ref = ref_side::compiled_evaluator(vec_ref);
+    auto f_gpu = b200_side::compiled_evaluator(vec_gpu);
+    std::vector<double> a(m), b(m);
+    int diff = 0;
+    for (const auto& x : pts) {
+      f_ref(x, a);
+      f_gpu(x, b);
+      diff += !same_bits(a, b);
+    }
+    CHECK(diff == 0);
+    std::printf("compiled_evaluator: %d of %zu points differ\n", diff, pts.size());
+
+    std::uint64_t calls_ref = 0, calls_gpu = 0;
+    ddsg::EvalWorkspace ws_ref;
+    ddsg_b200::EvalWorkspace ws_gpu;
+    diff = 0;
+    for (std::size_t i = 0; i < 256; ++i) {
+      vec_ref->evaluate(pts[i], a, ws_ref, &calls_ref);
+      vec_gpu->evaluate(pts[i], b, ws_gpu, &calls_gpu);
+      diff += !same_bits(a, b);
+    }
+    CHECK(diff == 0);
+    CHECK(calls_ref == calls_gpu && calls_ref > 0);
+    std::uint64_t c2r = 0, c2g = 0;
+    vec_ref->evaluate(pts[5], a, &c2r);
+    vec_gpu->evaluate(pts[5], b, &c2g);
+    CHECK(same_bits(a, b) && c2r == c2g);
+    vec_ref->evaluate(pts[6], a);
+    vec_gpu->evaluate(pts[6], b);
+    CHECK(same_bits(a, b));
+
+    const auto yr = vec_ref->evaluate_batch(pts, 4);
+    const auto yg = vec_gpu->evaluate_batch(pts, 4);
+    diff = 0;
+    for (std::size_t i = 0; i < pts.size(); ++i) diff += !same_bits(yr[i], yg[i]);
+    CHECK(diff == 0);
+    std::printf("evaluate_batch: %d differ; interp_calls %llu / %llu\n", diff,
+                static_cast<unsigned long long>(calls_ref), static_cast<unsigned long long>(calls_gpu));
+  }
+
+  // 5. slots(), quadratures, exceptions
+  {
+    const auto& sr = vec_ref->slots();
+    const auto& sg = vec_gpu->slots();
+    CHECK(sr.size() == sg.size());
+    bool ok = sr.size() == sg.size();
+    for (std::size_t i = 0; ok && i < sr.size(); ++i) {
+      ok = ok && sr[i].index.dims == sg[i].index.dims && sr[i].b == sg[i].b;
+      ok = ok && ((sr[i].grid == nullptr) == (sg[i].grid == nullptr));
+      if (sr[i].grid && sg[i].grid) ok = ok && sr[i].grid->size() == sg[i].grid->size();
+    }
+    CHECK(ok);
+    CHECK(same_bits(vec_ref->quadrature(), vec_gpu->quadrature()));
+    const auto& src = vec_gpu->source();
+    for (const auto& [u, b] : dd->coeff_b())
+      CHECK(same_bits(dd->cut_quadrature(u), src.cut_quadrature(ddsg_b200::ComponentIndex{u.dims})));
+    CHECK(src.rejected().size() == dd->rejected().size());
+    CHECK(throws<std::out_of_range>([&] { (void)src.cut_quadrature(ddsg_b200::ComponentIndex{{0, 1, 2}}); }));
+    std::vector<double> out(m), bad_x(d, 0.5), short_x(d - 1, 0.5);
+    bad_x[3] = 1.5;
+    ddsg_b200::EvalWorkspace ws;
+    CHECK(throws<std::domain_error>([&] { vec_ref->evaluate(bad_x, out); }));
+    CHECK(throws<std::domain_error>([&] { vec_gpu->evaluate(bad_x, out, ws); }));
+    CHECK(throws<std::invalid_argument>([&] { vec_ref->evaluate(short_x, out); }));
+    CHECK(throws<std::invalid_argument>([&] { vec_gpu->evaluate(short_x, out, ws); }));
+    std::vector<double> short_out(m - 1);
+    CHECK(throws<std::invalid_argument>([&] { vec_gpu->evaluate(pts[0], short_out, ws); }));
+  }
+
+  // 4. JSON documents: reference writes, B200 loads (C-ABI) and evaluates on
+  //    the GPU; B200 writes, reference loads.
+  {
+    namespace fs = std::filesystem;
+    const fs::path dir = fs::temp_directory_path() / ("ddsg_ref_dropin_" + std::to_string(::getpid()));
+    fs::create_directories(dir);
+    const std::string p_ref = (dir / "policy.json").string(), p_b200 = (dir / "policy_b200.json").string();
+    ddsg::save_json(ddsg::to_json(*dd), p_ref);  // tools/ddsg.cpp:217
+    auto loaded =
+        std::make_shared<const ddsg_b200::DdsgFunction>(ddsg_b200::ddsg_from_json(ddsg_b200::load_json(p_ref)));
+    auto vec_loaded = std::make_shared<const ddsg_b200::VectorizedDdsg>(ddsg_b200::VectorizedDdsg::compile(loaded));
+    auto frozen = [vec_loaded](std::span<const double> x, std::span<double> out) {  // tools/ddsg.cpp:263-266
+      thread_local ddsg_b200::EvalWorkspace ws;
+      vec_loaded->evaluate(x, out, ws);
+    };
+    std::vector<double> a(m), b(m);
+    int diff = 0;
+    for (const auto& x : pts) {
+      vec_ref->evaluate(x, a);
+      frozen(x, b);
+      diff += !same_bits(a, b);
+    }
+    CHECK(diff == 0);
+    std::printf("reference-written policy.json on the GPU: %d of %zu points differ\n", diff, pts.size());
+    CHECK(loaded->k_max() == dd->k_max());
+    CHECK(loaded->rejected().size() == dd->rejected().size());
+    CHECK(same_bits(loaded->anchor().coords, dd->anchor().coords));
+
+    ddsg_b200::save_json(ddsg_b200::to_json(*loaded), p_b200);
+    auto back = std::make_shared<const ddsg::DdsgFunction>(ddsg::ddsg_from_json(ddsg::load_json(p_b200)));
+    auto vec_back = ddsg::VectorizedDdsg::compile(back);
+    diff = 0;
+    for (std::size_t i = 0; i < 500; ++i) {
+      vec_ref->evaluate(pts[i], a);
+      vec_back.evaluate(pts[i], b);
+      diff += !same_bits(a, b);
+    }
+    CHECK(diff == 0);
+    // the two documents hold the same values: re-serialising the read-back
+    // with the reference gives the reference's own text
+    CHECK(ddsg::to_json(*back) == ddsg::to_json(*dd));
+
+    // one grid document both ways
+    const auto& [u0, g0] = *std::next(dd->accepted().begin(), static_cast<std::ptrdiff_t>(dd->accepted().size() - 1));
+    const std::string gdoc = ddsg::to_json(g0).dump(2);
+    auto g_b200 = ddsg_b200::sparse_grid_from_json(ddsg_b200::JsonDocument{gdoc});
+    CHECK(g_b200.size() == g0.size());
+    auto g_back = ddsg::sparse_grid_from_json(nlohmann::json::parse(ddsg_b200::to_json(g_b200).text));
+    bool nodes_same = g_back.size() == g0.size();
+    for (std::size_t i = 0; nodes_same && i < g0.size(); ++i)
+      nodes_same = g_back.nodes()[i].key == g0.nodes()[i].key && same_bits(g_back.nodes()[i].surplus, g0.nodes()[i].surplus);
+    CHECK(nodes_same);
+    CHECK(throws<std::invalid_argument>([] { (void)ddsg_b200::sparse_grid_from_json(ddsg_b200::JsonDocument{"{\"schema_version\": 2}"}); }));
+    CHECK(throws<std::invalid_argument>([] { (void)ddsg_b200::ddsg_from_json(ddsg_b200::JsonDocument{"[1, 2"}); }));
+    fs::remove_all(dir);
+  }
+
+  std::printf("%d passed, %d failed\n", g_pass, g_fail);
+  return g_fail;
+}

@@ -104,6 +104,28 @@ def hdmr_case(name, fn, d, m, k_max, L, eps_gamma=0.0, eps_eta=0.0, ctx_dim=None
     print(name, len(slots), "slots")
 
 
+def policy_case(name, fn, d, m, k_max, L, eps_gamma=0.0, eps_eta=0.0, ctx_dim=None, n=256, seed=0):
+    """A policy document written by the reference (to_json + dump, as
+    save_json, serialize.hpp:84-110,147-152) and the reference's evaluation of
+    that document after its own ddsg_from_json + compile."""
+    ctx = None
+    keep = None
+    if ctx_dim is not None:
+        keep = C.c_int(ctx_dim)
+        ctx = C.cast(C.pointer(keep), C.c_void_p)
+    _, _, text = O.ref_decompose(d, m, k_max, L, N.wl_fn(fn), ctx, eps_eta=eps_eta, eps_gamma=eps_gamma,
+                                 want_json=True)
+    (HERE / f"{name}.json").write_text(text)
+    h = C.c_void_p()
+    assert O.ref().ref_hdmr_from_json(text.encode(), C.byref(h)) == 0
+    x = edge_points(d, n, seed)
+    y = np.empty((x.shape[0], m))
+    assert O.ref().ref_hdmr_eval(h, x.ctypes.data, x.shape[0], y.ctypes.data, 1) == 0
+    O.ref().ref_hdmr_free(h)
+    np.savez_compressed(HERE / f"{name}.npz", x=x, y=y)
+    print(name, len(text), "bytes")
+
+
 def main():
     if O.ref() is None:
         raise SystemExit("oracle/_ref/libddsg_ref.so missing: make -C oracle ref")
@@ -117,6 +139,9 @@ def main():
     hdmr_case("hdmr_coupled_d4_k2_L4_adaptive", "wl_coupled", 4, 1, 2, 4, eps_gamma=1e-5, ctx_dim=4, seed=8443)
     hdmr_case("hdmr_pruned_d3_k2_L3", "wl_pruned3", 3, 1, 2, 3, eps_eta=1e-4, seed=77)
     hdmr_case("hdmr_vector3_d2_k2_L4", "wl_vector3", 2, 3, 2, 4, seed=61)
+    policy_case("policy_vector3_d2_k2_L5", "wl_vector3", 2, 3, 2, 5, eps_gamma=1e-6, seed=62)
+    policy_case("policy_coupled_d6_k2_L4_pruned", "wl_coupled", 6, 1, 2, 4, eps_gamma=1e-5, eps_eta=1e-3,
+                ctx_dim=6, seed=63)
 
 
 if __name__ == "__main__":
