@@ -64,6 +64,16 @@ class DeviceProgram {
   const HostProgram& host() const { return hp_; }
   const FastHdmr* fast() const { return fast_; }
   const PlainGrid* plain() const { return plain_; }
+  // Small-batch path of an HDMR program (see launch_eval): the reference's
+  // pairwise tree as internal nodes grouped by height.
+  struct SlotTree {
+    int nodes = 0;    // internal nodes (n_active - 1)
+    int heights = 0;  // tree height
+    const int32_t* left = nullptr;   // [nodes] child ids (< n_active: leaf / slot row)
+    const int32_t* right = nullptr;
+    const int32_t* height_off = nullptr;  // [heights + 1] node ranges per height
+  };
+  const SlotTree& slot_tree() const { return tree_; }
 
  private:
   HostProgram hp_;
@@ -72,6 +82,7 @@ class DeviceProgram {
   bool ready_ = false;
   FastHdmr* fast_ = nullptr;    // slot-staged kernel program, when the program qualifies
   PlainGrid* plain_ = nullptr;  // prefix-walk plain-grid kernel program, when it qualifies
+  SlotTree tree_;
   template <typename T>
   const T* put(const std::vector<T>& v);
 };

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <thread>
@@ -132,6 +133,51 @@ void DeviceProgram::upload(const HostProgram& hp) {
   p.slot_runs = put(hp.slot_runs);
   p.f_anchor = put(hp.f_anchor);
   p_ = p;
+  tree_ = SlotTree{};
+  if (!hp.plain && p.n_active > 1) {
+    // pairwise_sum (ddsg_eval.hpp:154-158) as a node list: leaves are the
+    // active slots 0..na-1, internal node = left + right, left = the first
+    // half (n/2 leaves); internal nodes renumbered by height so one CTA
+    // can fold a height at a time.
+    const int na = p.n_active;
+    struct Node {
+      int l, r, h;
+    };
+    std::vector<Node> nodes;
+    struct Rec {
+      static std::pair<int, int> go(int lo, int cnt, int na, std::vector<Node>& nodes) {  // (id, height)
+        if (cnt == 1) return {lo, 0};
+        const int half = cnt / 2;
+        const auto L = go(lo, half, na, nodes);
+        const auto R = go(lo + half, cnt - half, na, nodes);
+        nodes.push_back({L.first, R.first, 1 + std::max(L.second, R.second)});
+        return {na + static_cast<int>(nodes.size()) - 1, nodes.back().h};
+      }
+    };
+    Rec::go(0, na, na, nodes);
+    const int nn = static_cast<int>(nodes.size());
+    int H = 0;
+    for (const Node& q : nodes) H = std::max(H, q.h);
+    std::vector<int> order(nn);
+    for (int i = 0; i < nn; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nodes[a].h < nodes[b].h; });
+    std::vector<int> rank(nn);
+    for (int i = 0; i < nn; ++i) rank[order[i]] = i;
+    auto remap = [&](int id) { return id < na ? id : na + rank[id - na]; };
+    std::vector<int32_t> left(nn), right(nn), off(H + 1, 0);
+    for (int i = 0; i < nn; ++i) {
+      const Node& q = nodes[order[i]];
+      left[i] = remap(q.l);
+      right[i] = remap(q.r);
+      off[q.h] = i + 1;  // end of height q.h (heights are contiguous after the sort)
+    }
+    for (int h = 1; h <= H; ++h) off[h] = std::max(off[h], off[h - 1]);
+    tree_.nodes = nn;
+    tree_.heights = H;
+    tree_.left = put(left);
+    tree_.right = put(right);
+    tree_.height_off = put(off);
+  }
   delete fast_;
   fast_ = new FastHdmr();
   if (!fast_->build(hp)) {
@@ -247,6 +293,102 @@ __global__ void __launch_bounds__(128) eval_generic_kernel(EvalParams P, const d
   } else {
     for (int c = 0; c < nc; ++c) yp[c] = stack[0][c];
   }
+}
+
+// ------------------------------------------------------- small batches
+//
+// A few points evaluated by the slot kernel are latency-bound (every CTA
+// walks all active slots through its shared-memory ring: ~1 ms for config 5
+// at any n below a few thousand).  For small n the work is spread over slots
+// instead: one thread per (point, active slot, column chunk) computes that
+// slot's row exactly as the generic walk does (canonical order, mul then
+// add, x b), then one CTA per (point, column chunk) folds the rows with the
+// reference's pairwise tree, one tree height at a time.  Same operations on
+// the same operands: bit-identical to every other path.
+template <int kCols>
+__global__ void __launch_bounds__(128) slot_rows_kernel(EvalParams P, const double* __restrict__ x, int64_t n,
+                                                        int64_t base, double* __restrict__ rows,
+                                                        unsigned long long* bad) {
+  const int chunks = (P.m + kCols - 1) / kCols;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int ch = static_cast<int>(tid % chunks);
+  const int64_t pa = tid / chunks;
+  const int a = static_cast<int>(pa % P.n_active);
+  const int64_t p = pa / P.n_active;
+  if (p >= n) return;
+  const double* xp = x + p * P.d;
+  const int k = P.slot_k[a];
+  const int32_t* dims = P.slot_dims + P.slot_dims_off[a];
+  if (a == 0 && ch == 0 && !point_ok(xp, P.d)) atomicMin(bad, static_cast<unsigned long long>(base + p));
+  const int c0 = ch * kCols;
+  const int nc = min(kCols, P.m - c0);
+  const double b = P.slot_b[a];
+  double acc[kCols];
+  if (k == 0) {
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) acc[c] = c < nc ? __dmul_rn(b, P.f_anchor[c0 + c]) : 0.0;
+  } else {
+    bool ok = true;  // the slot's own coordinates (a bad point's rows are never used)
+    for (int j = 0; j < k; ++j) ok &= (xp[dims[j]] >= 0.0 && xp[dims[j]] <= 1.0);
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+    const int mode = P.slot_mode[a];
+    const int s_end = P.slot_sub_end[a];
+    const int runs = P.slot_runs[a];
+    for (int run = 0; ok && run < runs; ++run)
+      for (int s = P.slot_sub_begin[a]; s < s_end; ++s) {
+        const uint8_t* lv = P.levels + P.sub_lv_off[s];
+        double w = 1.0;
+        int64_t lin = 0;
+        for (int j = 0; j < k; ++j) {
+          const int l = lv[j];
+          const double xv = xp[dims[j]];
+          const uint32_t kk = cell_at(xv, l);
+          w = __dmul_rn(w, basis_at(mode, l, kk, xv));
+          lin = (lin << (l - 1)) | kk;
+          if (w == 0.0) break;
+        }
+        if (w == 0.0) continue;
+        const int32_t row = P.slab[P.sub_slab_off[s] + lin];
+        if (row < 0) continue;
+        if (runs > 1 && P.row_run[row] != run) continue;
+        const double* sr = P.surplus + static_cast<int64_t>(row) * P.m + c0;
+#pragma unroll
+        for (int c = 0; c < kCols; ++c)
+          if (c < nc) acc[c] = accum(acc[c], w, sr[c], P.exact);
+      }
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) acc[c] = __dmul_rn(acc[c], b);
+  }
+  double* out = rows + (p * P.n_active + a) * P.m + c0;
+  for (int c = 0; c < nc; ++c) out[c] = acc[c];
+}
+
+template <int kCols>
+__global__ void __launch_bounds__(256) slot_tree_kernel(int na, DeviceProgram::SlotTree T,
+                                                        const double* __restrict__ rows, int m,
+                                                        double* __restrict__ y) {
+  extern __shared__ double vals[];  // [na + T.nodes][kCols]
+  const int chunks = (m + kCols - 1) / kCols;
+  const int64_t p = blockIdx.x / chunks;
+  const int c0 = static_cast<int>(blockIdx.x % chunks) * kCols;
+  const int nc = min(kCols, m - c0);
+  const double* src = rows + p * na * m + c0;
+  for (int i = threadIdx.x; i < na * kCols; i += blockDim.x) {
+    const int a = i / kCols, c = i % kCols;
+    vals[i] = c < nc ? src[static_cast<int64_t>(a) * m + c] : 0.0;
+  }
+  __syncthreads();
+  for (int h = 1; h <= T.heights; ++h) {
+    const int lo = h == 1 ? 0 : T.height_off[h - 1], hi = T.height_off[h];
+    for (int i = lo * kCols + threadIdx.x; i < hi * kCols; i += blockDim.x) {
+      const int q = i / kCols, c = i % kCols;
+      vals[(na + q) * kCols + c] = __dadd_rn(vals[T.left[q] * kCols + c], vals[T.right[q] * kCols + c]);
+    }
+    __syncthreads();
+  }
+  const int root = T.nodes > 0 ? na + T.nodes - 1 : 0;
+  if (threadIdx.x < nc) y[p * m + c0 + threadIdx.x] = vals[root * kCols + threadIdx.x];
 }
 
 // Support statistics: nnz and an order-sensitive FNV-1a hash over
@@ -389,6 +531,16 @@ EventPair& events() {
 
 }  // namespace
 
+// Largest batch that takes the small-batch (slot-parallel) path of an HDMR
+// program; DDSG_SMALL_BATCH overrides (0 disables).
+static int64_t small_batch_points() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DDSG_SMALL_BATCH");
+    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{256};
+  }();
+  return v;
+}
+
 // Launches the evaluation of n device-resident points; returns kernel launches.
 static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* dx, int64_t n,
                            int64_t base, double* dy, unsigned long long* dbad, cudaStream_t st,
@@ -398,6 +550,23 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
   if (const PlainGrid* pg = prog.plain()) {
     const size_t wb = pg->workspace_bytes(n);
     return pg->launch(exact, dx, n, base, dy, dbad, wb ? xt_scratch.get(wb) : nullptr, st);
+  }
+  if (!P.plain && P.n_active > 1 && n <= small_batch_points() &&
+      static_cast<size_t>(2 * P.n_active) * 8 * 8 <= size_t{200} * 1024) {
+    // few points: slot-parallel rows, then the pairwise tree per (point, chunk)
+    constexpr int kCols = 8;
+    const int chunks = (P.m + kCols - 1) / kCols;
+    double* rows = static_cast<double*>(xt_scratch.get(static_cast<size_t>(n) * P.n_active * P.m * 8));
+    const int64_t threads = n * P.n_active * chunks;
+    kernel_timer().begin(st);
+    slot_rows_kernel<kCols><<<static_cast<unsigned>((threads + 127) / 128), 128, 0, st>>>(P, dx, n, base, rows, dbad);
+    const DeviceProgram::SlotTree& T = prog.slot_tree();
+    const size_t smem = static_cast<size_t>(P.n_active + T.nodes) * kCols * 8;
+    ensure_dynamic_smem(reinterpret_cast<const void*>(slot_tree_kernel<kCols>), smem);
+    slot_tree_kernel<kCols><<<static_cast<unsigned>(n * chunks), 256, smem, st>>>(P.n_active, T, rows, P.m, dy);
+    kernel_timer().end(st);
+    DDSG_CUDA(cudaGetLastError());
+    return 2;
   }
   if (const FastHdmr* f = prog.fast()) {
     // chunk so the dim-major scratch stays <= ~1 GiB

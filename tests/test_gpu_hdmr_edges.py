@@ -214,3 +214,49 @@ def test_concurrent_programs_on_host_threads():
     for t in ts:
         t.join()
     assert not errors, errors[:3]
+
+
+# ------------------------------------------------ small batches (n <= 256)
+# Few points take the slot-parallel path (one thread per point x slot x
+# column chunk, then the pairwise tree per point, height by height): the
+# per-point evaluate(x, out, ws) of the reference's callers.
+
+@pytest.mark.parametrize("n", [1, 2, 7, 256, 257])
+@pytest.mark.parametrize("case", ["modes", "b_kinds", "nonfinite", "deep_tree", "order3"])
+def test_small_batches_bit_exact(case, n):
+    if case == "modes":
+        d, m = 6, 23
+        vec, fa, so = make(d, m, family_1d_2d(d, [(0, 1), (1, 2), (2, 5), (3, 4)]), {1: 6, 2: 4},
+                           mode=ZERO_BOUNDARY, seed=n)
+    elif case == "b_kinds":
+        d, m = 4, 7
+        vec, fa, so = make(d, m, family_1d_2d(d, [(0, 1), (2, 3)]), {1: 5, 2: 3}, b=[5, 1, -1, 2, -3, 1, 0])
+    elif case == "nonfinite":
+        d, m = 4, 3
+        vec, fa, so = make(d, m, family_1d_2d(d, [(0, 1)]), {1: 5, 2: 3}, poison=((0, 1), 7, 1, np.inf))
+    elif case == "deep_tree":
+        d, m = 60, 3
+        rng = np.random.default_rng(1)
+        pairs = set()
+        while len(pairs) < 200:
+            a, b = sorted(rng.choice(d, 2, replace=False).tolist())
+            pairs.add((a, b))
+        vec, fa, so = make(d, m, family_1d_2d(d, pairs), {1: 3, 2: 2})
+    else:
+        d, m = 4, 5
+        fam = [()] + [(j,) for j in range(d)] + [(0, 1), (0, 2), (1, 2)] + [(0, 1, 2)]
+        vec, fa, so = make(d, m, fam, {1: 4, 2: 3, 3: 3})
+    check(vec, d, m, fa, so, pts(d, max(n, 9))[:n], nan_ok=case == "nonfinite")
+
+
+def test_small_batch_domain_error_lowest_index():
+    from paper_2202_06555_b200.ddsg import DomainError
+
+    d, m = 4, 5
+    vec, fa, so = make(d, m, family_1d_2d(d, [(0, 1)]), {1: 4, 2: 3})
+    x = pts(d, 9)
+    x[5, 2] = np.nan
+    x[7, 0] = 1.5
+    with pytest.raises(DomainError) as e:
+        vec.evaluate_batch(x)
+    assert e.value.task_id == 5
