@@ -28,6 +28,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "interpolant evals/sec (points x outputs)"
+BLOCK_POINTS = 1 << 14  # seeded point blocks (ddsg_uniform_point_blocks; oracle/ref_workload.py)
 UNIT = "evals/s"
 
 
@@ -125,41 +126,13 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-def build_reference_hdmr(cfg, parts, use_reference_build: bool):
-    """The reference's VectorizedDdsg over the config's component grids.
+def ref_workload():
+    """oracle/ref_workload.py: the configs built and evaluated by the
+    reference alone (oracle/_ref), without loading the product library."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ref_workload as RW
 
-    use_reference_build: build every cut grid with the reference's own
-    SparseGridFunction::build (sparse_grid.hpp:84) from the same C target;
-    otherwise inject our grids through from_nodes (same bits)."""
-    import ctypes as C
-
-    import numpy as np
-
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib as O
-    from paper_2202_06555_b200 import _native as N
-
-    grids = []
-    wl = N.workloads()
-    anchor = np.full(cfg.d, 0.5)
-    for u, b, g in parts.slots:
-        if g is None:
-            grids.append(None)
-            continue
-        if use_reference_build:
-            dims = np.array(u, dtype=np.int32)
-            cut = wl.wl_cut_new(N.wl_fn(cfg.target), None, cfg.d, cfg.m, len(u), dims.ctypes.data, anchor.ctypes.data)
-            lvl = cfg.level_1d if len(u) == 1 else cfg.level_2d
-            eps = cfg.eps_1d if len(u) == 1 else cfg.eps_2d
-            rc, rg = O.ref_build(len(u), cfg.m, cfg.mode, lvl, eps, N.wl_fn("wl_cut_eval"), C.c_void_p(cut))
-            wl.wl_cut_free(C.c_void_p(cut))
-            if rc != 0:
-                raise RuntimeError(f"reference build failed: {rg}")
-            grids.append(rg)
-        else:
-            keys, sur = g.nodes()
-            grids.append(O.ref_from_nodes(len(u), cfg.m, g.boundary_mode, g.max_level, g.eps_gamma, keys, sur))
-    return O.RefHdmr(cfg.d, cfg.m, parts.f_anchor, [(u, b) for u, b, _ in parts.slots], grids)
+    return RW
 
 
 def time_reference(ref_hdmr, cfg, x_sample, target_s: float, workers: int):
@@ -190,30 +163,52 @@ def reference_variants():
     return [p for p in out if p.exists()]
 
 
-def cpu_baseline(cfg, parts, target_s: float, use_reference_build: bool):
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib as O
-    from paper_2202_06555_b200.ddsg import uniform_points
-
+def cpu_baseline(cfg, target_s: float):
+    """The reference's CPU path on this host's cores: every cut grid built by
+    the reference's own SparseGridFunction::build, the first points of the
+    bench's seeded stream through VectorizedDdsg::evaluate_batch(workers =
+    all cores); the faster of the generic and x86-64-v3 builds of oracle/_ref.
+    Returns (baseline dict, the faster build's (RefHdmr, lib))."""
+    RW = ref_workload()
     workers = cpu_cores()
-    x = uniform_points(cfg.seed, 1 << 18, cfg.d)
     best = None
-    for lib in reference_variants():
-        O._ref = None
-        O.REF_PATH = lib
-        ref = build_reference_hdmr(cfg, parts, use_reference_build)
+    for path in reference_variants():
+        lib = RW.use_library(path)
+        ref = RW.build_hdmr(cfg, lib)[0]
+        x = RW.points(lib, cfg, 0, 1 << 18)
         time_reference(ref, cfg, x, 0.5, workers)  # warm
         n, dt = time_reference(ref, cfg, x, target_s, workers)
         rate = n * cfg.m / dt
         if best is None or rate > best[0]:
-            best = (rate, n, dt, lib.name)
-        del ref
+            best = (rate, n, dt, path, ref, lib)
     if best is None:
-        return None
-    rate, n, dt, name = best
-    return {"value": rate, "unit": UNIT, "cores": workers, "kind": "reference",
-            "sample": f"first {n} seeded points of {cfg.name} through the reference's "
-                      f"VectorizedDdsg::evaluate_batch(workers={workers}) ({name}, {dt:.1f} s)"}
+        return None, None
+    rate, n, dt, path, ref, lib = best
+    return ({"value": rate, "unit": UNIT, "cores": workers, "kind": "reference",
+             "sample": f"first {n} points of the seeded stream of {cfg.name} through the reference's "
+                       f"VectorizedDdsg::evaluate_batch(workers={workers}) over grids built by its own "
+                       f"SparseGridFunction::build ({path.name}, {dt:.1f} s)"}, (ref, lib))
+
+
+def parity_check(ref_lib, cfg, y_dev, n_check: int):
+    """Bit-exact check of the first n_check timed outputs against the
+    reference (oracle/_ref, its own grid build) on the same points."""
+    import numpy as np
+
+    ref, lib = ref_lib
+    RW = ref_workload()
+    x = RW.points(lib, cfg, 0, n_check)
+    rc, want = ref.eval(x, workers=cpu_cores(), flat=False)
+    if rc != 0:
+        return {"error": "reference evaluation failed"}
+    got = y_dev[:n_check].cpu().numpy()
+    same = np.all(got.view(np.uint64) == want.view(np.uint64), axis=1)
+    tol = 1e-14 + 1e-12 * np.abs(want)
+    return {"points": int(n_check), "outputs": int(n_check * cfg.m), "bit_identical_points": int(same.sum()),
+            "outputs_outside_tolerance": int((np.abs(got - want) > tol).sum()),
+            "max_abs_diff": float(np.max(np.abs(got - want))),
+            "against": "oracle/_ref VectorizedDdsg::evaluate_batch over the reference's own SparseGridFunction::build "
+                       "of every cut, first points of rank 0's timed inputs"}
 
 
 # -------------------------------------------------------------- our arm
@@ -266,9 +261,15 @@ def run_ours(args, rank, world, local_rank, dist):
     obj.set_eval_mode(EXACT if args.mode == "exact" else FAST)
     build_s = time.time() - t0
 
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(cfg.seed * 1000 + rank)
-    x = torch.rand((n_local, cfg.d), dtype=torch.float64, device="cuda", generator=gen)
+    # the seeded blocked stream (block b: mt19937_64(seed + b), the reference
+    # oracle's generator): rank r evaluates the contiguous shard
+    # [first, first + n_local) of ONE point set, whatever the rank count
+    from paper_2202_06555_b200.ddsg import uniform_point_blocks
+
+    first = rank * (n_total // world) + min(rank, n_total % world)
+    xh = torch.empty((n_local, cfg.d), dtype=torch.float64, pin_memory=True)
+    uniform_point_blocks(cfg.seed, BLOCK_POINTS, first, n_local, cfg.d, out=xh.numpy())
+    x = xh.cuda()
     y = torch.empty((n_local, cfg.m), dtype=torch.float64, device="cuda")
 
     # exact algorithmic work: NNZ_total = sum over points of (slot, node) pairs with w != 0
@@ -357,8 +358,6 @@ def run_ours(args, rank, world, local_rank, dist):
     e2e = None
     if not args.no_e2e:
         try:
-            xh = torch.empty((n_local, cfg.d), dtype=torch.float64, pin_memory=True)
-            xh.copy_(x)
             yh = torch.empty((n_local, cfg.m), dtype=torch.float64, pin_memory=True)
             evaluate(xh, out=yh)
             barrier()
@@ -375,14 +374,18 @@ def run_ours(args, rank, world, local_rank, dist):
             e2e = {"value": n_total * cfg.m / e2e_s, "unit": UNIT,
                    "h2d_bytes_per_step": n_total * cfg.d * 8, "d2h_bytes_per_step": n_total * cfg.m * 8,
                    "s_per_step": e2e_s, "timing": "wall clock around the synchronous C-ABI call"}
-            del xh, yh
+            del yh
         except RuntimeError as e:  # e.g. pinned allocation failure
             e2e = {"value": None, "unit": UNIT, "error": str(e)[:200]}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.kind == "hdmr":
+    cpu, parity = None, None
+    if rank == 0 and not args.no_cpu_baseline and cfg.kind == "hdmr":
         try:
-            cpu = cpu_baseline(cfg, parts, args.cpu_seconds, use_reference_build=False)
+            cpu, ref_lib = cpu_baseline(cfg, args.cpu_seconds)
+            if ref_lib is not None:
+                parity = parity_check(ref_lib, cfg, y, min(n_local, 4096))
+            if world > 1:
+                cpu = None  # reported at N=1 only; the parity check still runs on rank 0
         except Exception as e:
             cpu = {"value": None, "error": str(e)[:200]}
 
@@ -397,7 +400,7 @@ def run_ours(args, rank, world, local_rank, dist):
                        "eval_mode": args.mode, "parallelism": f"points sharded over {world} GPU(s), grids replicated",
                        "l2": f"inputs {n_local * cfg.d * 8 / 1e9:.1f} GB per GPU, larger than L2 (no flush needed)",
                        "build_s": round(build_s, 1)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "gpu_launches": launches,
             "refinement": refine_info,
             "clocks": clk,
         }
@@ -407,28 +410,26 @@ def run_ours(args, rank, world, local_rank, dist):
 # ------------------------------------------------------- reference arm
 
 def run_reference(args, rank, world):
+    """The reference's own CPU path: oracle/_ref only (its build, its
+    evaluate_batch, its point generator, the targets linked into it); the
+    product library is never loaded in this process."""
     if rank != 0:
         return
-    from paper_2202_06555_b200 import workloads as W
-    from paper_2202_06555_b200.ddsg import uniform_points
-
-    cfg = W.CONFIGS[args.config]
+    RW = ref_workload()
+    cfg = RW.configs()[args.config]
     if cfg.kind != "hdmr":
         print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for the HDMR configs"}))
         return
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib as O
-
     if not reference_variants():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libddsg_ref.so was not built"}))
         return
-    parts = W.build_hdmr_parts(cfg)
     workers = cpu_cores()
-    lib = reference_variants()[-1]
-    O._ref = None
-    O.REF_PATH = lib
-    ref = build_reference_hdmr(cfg, parts, use_reference_build=True)
-    x = uniform_points(cfg.seed, 1 << 14, cfg.d)
+    path = reference_variants()[-1]
+    lib = RW.use_library(path)
+    t0 = time.time()
+    ref = RW.build_hdmr(cfg, lib)[0]
+    build_s = time.time() - t0
+    x = RW.points(lib, cfg, 0, 1 << 14)
     # size one step to ~ (a few minutes / steps) of CPU work
     n, dt = time_reference(ref, cfg, x, 2.0, workers)
     for _ in range(args.warmup):
@@ -438,8 +439,11 @@ def run_reference(args, rank, world):
         ref.eval(x[:n], workers=workers, flat=False)
     dt = (time.perf_counter() - t0) / args.steps
     v = n * cfg.m / dt
-    sample = (f"{n} seeded points of {cfg.name} per step through VectorizedDdsg::evaluate_batch"
-              f"(workers={workers}); grids built by the reference's SparseGridFunction::build ({lib.name})")
+    sample = (f"first {n} points of the seeded stream of {cfg.name} per step through "
+              f"VectorizedDdsg::evaluate_batch(workers={workers}); every cut grid built by the reference's "
+              f"SparseGridFunction::build ({path.name}; build {build_s:.1f} s)")
+    loaded = sorted({p.split()[-1] for p in open("/proc/self/maps") if p.strip().endswith(".so")
+                     and str(ROOT) in p})
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -447,6 +451,7 @@ def run_reference(args, rank, world):
         "config": {"workload": cfg.name, "d": cfg.d, "m": cfg.m, "points_per_step": n},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "repo_libraries_loaded": [str(Path(p).relative_to(ROOT)) for p in loaded],
     }), flush=True)
 
 

@@ -292,6 +292,16 @@ ddsg_status ddsg_grid_support(const ddsg_grid_t* g, const double* x, int64_t n, 
  * the reference's test oracle generates them (proj/tests/oracles.hpp:45-53). */
 void ddsg_uniform_points(uint64_t seed, int64_t n, int dim, double* out);
 
+/* Blocked form of the same generator for sharded benchmarks: block b holds
+ * block_points points drawn from std::mt19937_64(seed + b) +
+ * uniform_real_distribution(0,1), point-major.  Writes points
+ * [first, first + n) of that stream into out[n][dim] (host memory), blocks
+ * generated on several host threads; any contiguous range -- a rank's shard
+ * -- is therefore generated independently of how the set is split, and the
+ * oracle reproduces block b with a plain seeded draw. */
+void ddsg_uniform_point_blocks(uint64_t seed, int64_t block_points, int64_t first, int64_t n, int dim,
+                               double* out);
+
 /* ------------------------------------------------ batched policy callers
  *
  * the time iteration's consumers of the policy

@@ -361,6 +361,27 @@ uint64_t ref_sg_node_count_bruteforce(int n, int L) { return oracle::sg_node_cou
 
 unsigned ref_default_workers() { return default_worker_count(); }
 
+// oracle::b_coefficients_bruteforce (oracles.hpp:72-81): the telescopic
+// coefficient of every family member (family incl. the empty index, each
+// member given as order[s] dims concatenated in dims).
+int ref_b_coefficients(int n_family, const int32_t* order, const int32_t* dims, int32_t* b_out) {
+  return guarded([&] {
+    std::vector<ComponentIndex> fam;
+    int64_t off = 0;
+    for (int s = 0; s < n_family; ++s) {
+      ComponentIndex u;
+      u.dims.assign(dims + off, dims + off + order[s]);
+      off += order[s];
+      fam.push_back(std::move(u));
+    }
+    const auto b = oracle::b_coefficients_bruteforce(fam);
+    for (int s = 0; s < n_family; ++s) {
+      auto it = b.find(fam[s]);
+      b_out[s] = it == b.end() ? 0 : it->second;
+    }
+  });
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------- IRBC callers

@@ -63,6 +63,7 @@ SIGNATURES = {
     "ddsg_hdmr_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
     "ddsg_grid_support": (_i, [_p, _pd, _i64, _pd, _pd, _p]),
     "ddsg_uniform_points": (None, [C.c_uint64, _i64, _i, _p]),
+    "ddsg_uniform_point_blocks": (None, [C.c_uint64, _i64, _i64, _i64, _i, _p]),
     "ddsg_hdmr_slot": (_i, [_p, _i, C.POINTER(_i), _p, C.POINTER(C.c_int32), C.POINTER(_p)]),
     "ddsg_grid_from_json": (_i, [C.c_char_p, _i64, C.POINTER(_p)]),
     "ddsg_grid_to_json": (_i, [_p, _p, _i64, C.POINTER(_i64)]),

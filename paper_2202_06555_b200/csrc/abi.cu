@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -447,6 +449,29 @@ void ddsg_uniform_points(uint64_t seed, int64_t n, int dim, double* out) {
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> unif(0.0, 1.0);
   for (int64_t i = 0; i < n * dim; ++i) out[i] = unif(rng);
+}
+
+void ddsg_uniform_point_blocks(uint64_t seed, int64_t block_points, int64_t first, int64_t n, int dim, double* out) {
+  if (n <= 0 || dim <= 0 || block_points <= 0 || first < 0 || !out) return;
+  const int64_t b0 = first / block_points, b1 = (first + n - 1) / block_points;
+  auto work = [&](int64_t b) {
+    const int64_t lo = std::max(first, b * block_points), hi = std::min(first + n, (b + 1) * block_points);
+    std::mt19937_64 rng(seed + static_cast<uint64_t>(b));
+    rng.discard(static_cast<unsigned long long>((lo - b * block_points) * dim));
+    std::uniform_real_distribution<double> unif(0.0, 1.0);
+    double* o = out + (lo - first) * dim;
+    for (int64_t i = 0; i < (hi - lo) * dim; ++i) o[i] = unif(rng);
+  };
+  const int64_t nb = b1 - b0 + 1;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t nt = std::min<int64_t>(nb, std::min<unsigned>(hw, 32u));
+  std::vector<std::thread> pool;
+  std::atomic<int64_t> next{b0};
+  for (int64_t t = 0; t < nt; ++t)
+    pool.emplace_back([&] {
+      for (int64_t b = next++; b <= b1; b = next++) work(b);
+    });
+  for (auto& th : pool) th.join();
 }
 
 }  // extern "C"

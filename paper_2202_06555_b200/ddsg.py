@@ -474,6 +474,17 @@ def measure_fp64_peak():
     return a.value, b.value
 
 
+def uniform_point_blocks(seed: int, block_points: int, first: int, n: int, dim: int, out=None) -> np.ndarray:
+    """Points [first, first + n) of the blocked seeded stream: block b is
+    std::mt19937_64(seed + b) + uniform_real_distribution(0,1), point-major
+    (include/ddsg_b200.h).  out: optional C-contiguous float64 [n][dim] host
+    array (e.g. a pinned torch tensor's numpy view)."""
+    if out is None:
+        out = np.empty((n, dim), dtype=np.float64)
+    N.lib.ddsg_uniform_point_blocks(C.c_uint64(seed), block_points, first, n, dim, _ptr(out))
+    return out
+
+
 def uniform_points(seed: int, n: int, dim: int) -> np.ndarray:
     """std::mt19937_64 + uniform_real_distribution(0,1), point-major (oracles.hpp:45-53)."""
     out = np.empty((n, dim), dtype=np.float64)

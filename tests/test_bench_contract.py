@@ -40,6 +40,48 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    # the reference arm maps only oracle/_ref: no product library in its process
+    assert d["repo_libraries_loaded"] and all(p.startswith("oracle/_ref/") for p in d["repo_libraries_loaded"])
+
+
+def test_reference_arm_builds_the_same_program():
+    """oracle/ref_workload.py (reference build, reference b lattice, targets
+    linked into oracle/_ref, reference point generator) reproduces the
+    product's config-4 program: same family and b, same anchor values, same
+    node bits per cut, and the same blocked point stream."""
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built")
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ref_workload as RW
+    from helpers import bits
+    from paper_2202_06555_b200 import workloads as W
+    from paper_2202_06555_b200.ddsg import uniform_point_blocks
+
+    cfg = RW.configs()[4]
+    lib = RW.use_library(O.REF_PATH)
+    ref, fa, fam, b = RW.build_hdmr(cfg, lib)
+    parts = W.build_hdmr_parts(W.CONFIGS[4])
+    assert [u for u, _, _ in parts.slots] == fam
+    assert [bu for _, bu, _ in parts.slots] == b
+    assert np.array_equal(bits(parts.f_anchor), bits(fa))
+    for (u, bu, g), rg in zip(parts.slots, ref._keep):
+        if g is None:
+            assert rg is None
+            continue
+        k1, s1 = g.nodes()
+        k2, s2 = rg.nodes(len(u), cfg.m)
+        assert np.array_equal(k1, k2) and np.array_equal(bits(s1), bits(s2))
+    first, n = RW.BLOCK_POINTS - 5, 2 * RW.BLOCK_POINTS + 9
+    x_ref = RW.points(lib, cfg, first, n)
+    x_ours = uniform_point_blocks(cfg.seed, RW.BLOCK_POINTS, first, n, cfg.d)
+    assert np.array_equal(bits(x_ref), bits(x_ours))
+    # a shard is the same points whatever the split
+    a = uniform_point_blocks(cfg.seed, RW.BLOCK_POINTS, 0, 3000, cfg.d)
+    b2 = np.concatenate([uniform_point_blocks(cfg.seed, RW.BLOCK_POINTS, 0, 1234, cfg.d),
+                         uniform_point_blocks(cfg.seed, RW.BLOCK_POINTS, 1234, 3000 - 1234, cfg.d)])
+    assert np.array_equal(bits(a), bits(b2))
 
 
 def test_reference_arm_non_zero_rank_is_silent():
