@@ -238,7 +238,10 @@ def run_ours(args, rank, world, local_rank, dist):
         from paper_2202_06555_b200.refine import refine_step
 
         coarse = dataclasses.replace(cfg, level_1d=cfg.level_1d - 1)
-        parts = W.build_hdmr_parts(coarse)
+        if dist is not None:  # build once on rank 0, broadcast the nodes (NCCL)
+            parts = W.broadcast_hdmr_parts(cfg, dist, f"cuda:{local_rank}", level_1d=cfg.level_1d - 1)
+        else:
+            parts = W.build_hdmr_parts(coarse)
         idx = [i for i, (u, b, g) in enumerate(parts.slots) if len(u) == 1]
         grids = [parts.slots[i][2] for i in idx]
         cuts = [W.CutTarget(cfg, parts.slots[i][0]) for i in idx]
@@ -249,7 +252,8 @@ def run_ours(args, rank, world, local_rank, dist):
                        "hierarchize_s": round(st.hierarchize_s, 3), "target_eval_s": round(st.target_s, 3),
                        "allgather_s": round(st.allgather_s, 4),
                        "total_s": round(time.time() - t_ref, 2),
-                       "collective": "all_gather_into_tensor (NCCL)" if dist is not None else "none (1 rank)"}
+                       "collective": st.collective,
+                       "build": "rank 0 builds, nodes broadcast (NCCL)" if dist is not None else "local build"}
         obj = VectorizedDdsg.compile(parts.d, parts.m, parts.f_anchor, parts.slots)
         evaluate = obj.evaluate_batch
     elif cfg.kind == "hdmr":

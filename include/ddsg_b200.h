@@ -236,6 +236,44 @@ ddsg_status ddsg_hdmr_document(const ddsg_hdmr_t* h, int* k_max, double* anchor_
                                int* n_rejected, int64_t* n_rejected_dims, int32_t* rejected_order,
                                int32_t* rejected_dims, int* has_quadratures, double* cut_quadratures);
 
+/* ------------------------------------------- distributed refinement step
+ *
+ * One adaptive refinement step of replicated grids (the
+ * path's only collective), orchestrated natively.  For grid g the new batch
+ * is the reference's next build batch from level sum level_sums[g]
+ * (next_candidates, sparse_grid.hpp:215-254), processed in level-sum groups;
+ * per group round the new nodes of all grids are split into equal, padded,
+ * contiguous shares over the ranks; each rank evaluates the target at its
+ * share (callback), hierarchizes it (surplus = f - interpolate, EXACT, on
+ * the GPU when on_device != 0, else on the host), the surplus rows
+ * [world][share][m] are all-gathered and every rank appends the whole group
+ * in batch order (insert_batch, sparse_grid.hpp:256-298).  The grids stay
+ * bit-identical on every rank and equal to the reference's build at the
+ * next level.  Mutates the grids (external synchronisation, like
+ * ddsg_grid_append). */
+typedef int (*ddsg_node_evaluator)(int grid, const double* xs, int64_t count, double* out, void* ctx);
+/* All-gather of bytes_per_rank bytes from every rank into recv
+ * [world][bytes_per_rank] (device buffers when on_device).  Returns 0 on success. */
+typedef int (*ddsg_allgather_fn)(const void* send, void* recv, int64_t bytes_per_rank, void* ctx);
+typedef struct {
+  int64_t new_nodes, rounds, gathered_bytes;
+  double target_s, hierarchize_s, allgather_s;
+} ddsg_refine_stats;
+/* allgather may be NULL for a single process (world == 1).  Errors:
+ * INVALID_ARGUMENT, BUILD_ERROR (non-finite target value; the node through
+ * ddsg_last_build_point), NCCL_ERROR (the all-gather returned non-zero). */
+ddsg_status ddsg_refine_step(ddsg_grid_t* const* grids, int n_grids, const int* level_sums, ddsg_node_evaluator f,
+                             void* f_ctx, int rank, int world, ddsg_allgather_fn allgather, void* ag_ctx,
+                             int on_device, ddsg_refine_stats* stats);
+/* The same step over a caller's NCCL communicator (an ncclComm_t, e.g. the
+ * C++ host's, or torch's ProcessGroupNCCL._comm_ptr()): device buffers,
+ * ncclAllGather(ncclFloat64) on `stream` (a cudaStream_t) over NVLink.
+ * libnccl.so.2 is resolved at the first call (the library does not link
+ * it).  nccl_comm may be NULL only for world == 1. */
+ddsg_status ddsg_refine_step_nccl(ddsg_grid_t* const* grids, int n_grids, const int* level_sums,
+                                  ddsg_node_evaluator f, void* f_ctx, void* nccl_comm, int rank, int world,
+                                  void* stream, ddsg_refine_stats* stats);
+
 /* ---------------------------------------------------- evaluation workspace
  *
  * EvalWorkspace (ddsg_eval.hpp:21-24): reusable buffers for allocation-free

@@ -27,6 +27,15 @@ NORM_INF, NORM_L2 = 0, 1
 EVAL_EXACT, EVAL_FAST = 0, 1
 
 BATCH_EVALUATOR = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)
+NODE_EVALUATOR = C.CFUNCTYPE(C.c_int, C.c_int, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+class RefineStatsC(C.Structure):
+    """ddsg_refine_stats (include/ddsg_b200.h)."""
+
+    _fields_ = [("new_nodes", C.c_int64), ("rounds", C.c_int64), ("gathered_bytes", C.c_int64),
+                ("target_s", C.c_double), ("hierarchize_s", C.c_double), ("allgather_s", C.c_double)]
 
 _p = C.c_void_p
 _i = C.c_int
@@ -71,6 +80,8 @@ SIGNATURES = {
     "ddsg_hdmr_to_json": (_i, [_p, _p, _i64, C.POINTER(_i64)]),
     "ddsg_hdmr_set_document": (_i, [_p, _i, _p, _i, _p, _p, _p]),
     "ddsg_hdmr_document": (_i, [_p, C.POINTER(_i), _p, _p, C.POINTER(_i), C.POINTER(_i64), _p, _p, C.POINTER(_i), _p]),
+    "ddsg_refine_step": (_i, [_p, _i, _p, _p, _p, _i, _i, _p, _p, _i, _p]),
+    "ddsg_refine_step_nccl": (_i, [_p, _i, _p, _p, _p, _p, _i, _i, _p, _p]),
     "ddsg_workspace_create": (_i, [C.POINTER(_p)]),
     "ddsg_workspace_destroy": (_i, [_p]),
     "ddsg_eval_hdmr_ws": (_i, [_p, _p, _pd, _i64, _pd, C.POINTER(_i64), C.POINTER(C.c_uint64)]),

@@ -11,12 +11,13 @@ rank evaluates the target and hierarchizes its share on its own GPU
 (`ddsg_hierarchize`, exact), the surplus rows are all-gathered (NCCL over
 NVLink on GPU ranks, gloo in the CPU tests) and every rank appends the whole
 group in batch order — grids stay replicated and bit-identical on every rank,
-and equal to the reference's `build` at the next level.
+and equal to the reference's `build` at the next level.  The orchestration
+is native (C-ABI ddsg_refine_step, csrc/refine.cu); this module only adapts
+the caller's target and torch.distributed to it.
 """
 from __future__ import annotations
 
-import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence
 
 import numpy as np
@@ -32,7 +33,7 @@ class RefineStats:
     hierarchize_s: float = 0.0  # GPU (or host) hierarchization of this rank's share
     target_s: float = 0.0       # the caller's target evaluations (host model code)
     allgather_s: float = 0.0
-    per_round: List[int] = field(default_factory=list)
+    collective: str = "none"
 
 
 def coords_of(keys: np.ndarray) -> np.ndarray:
@@ -43,92 +44,114 @@ def coords_of(keys: np.ndarray) -> np.ndarray:
     return index.astype(np.float64) * np.ldexp(1.0, -(lm1 + 1))
 
 
-def _level_sums(keys: np.ndarray) -> np.ndarray:
-    lv = np.floor(np.log2(keys.astype(np.float64))).astype(np.int64) + 1
-    return lv.sum(axis=1)
+class _DeviceArray:
+    """A raw device allocation as a __cuda_array_interface__ object (so torch
+    can wrap the library's device buffers without copying)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False), "version": 3}
 
 
-def _all_gather_rows(local: np.ndarray, rows_per_rank: int, m: int, dist, device: str):
-    """All-gather [rows_per_rank][m] float64 blocks; returns [world*rows_per_rank][m]."""
-    import torch
+def _nccl_comm(dist):
+    """torch's ncclComm_t of the default group, or None (gloo, no NCCL)."""
+    try:
+        import torch
 
-    world = dist.get_world_size()
-    t = torch.from_numpy(np.ascontiguousarray(local)).to(device)
-    if device.startswith("cuda"):
-        out = torch.empty((world * rows_per_rank, m), dtype=torch.float64, device=device)
-        dist.all_gather_into_tensor(out, t)  # ncclAllGather over NVLink
-        return out.cpu().numpy()
-    parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t)
-    return torch.cat(parts).numpy()
+        if dist.get_backend() != "nccl":
+            return None
+        pg = dist.distributed_c10d._get_default_group()
+        return int(pg._get_backend(torch.device("cuda"))._comm_ptr())
+    except Exception:
+        return None
 
 
 def refine_step(grids: Sequence[SparseGridFunction], level_sums: Sequence[int],
                 f_eval: Callable[[int, np.ndarray], np.ndarray], dist=None, device: bool = True,
                 comm_device: Optional[str] = None) -> RefineStats:
-    """Refines every grid by one level-sum step.
+    """Refines every grid by one level-sum step (C-ABI ddsg_refine_step /
+    ddsg_refine_step_nccl: the orchestration is native).
 
     grids:      component grids (same out_dim), replicated on every rank
     level_sums: per grid, the level sum s whose significant nodes get children
     f_eval:     f_eval(grid_index, xs[count][dim]) -> values[count][m]; called
                 only for this rank's share of the new nodes
-    dist:       torch.distributed (initialised) or None for a single process
+    dist:       torch.distributed (initialised) or None for a single process.
+                With the NCCL backend the library all-gathers the device rows
+                itself over torch's communicator (ncclAllGather, no host
+                bounce); otherwise through a torch.distributed all-gather
+                (device tensors wrapping the library's buffers, or host
+                arrays for gloo with device=False).
     device:     hierarchize on the GPU (True) or on the host (False)
     """
-    stats = RefineStats()
+    import ctypes as C
+
+    from . import _native as N
+    from .ddsg import _check
+
     m = grids[0].out_dim
+    dims = [g.dim for g in grids]
     rank = dist.get_rank() if dist is not None else 0
     world = dist.get_world_size() if dist is not None else 1
-    if comm_device is None:
-        comm_device = "cuda" if device else "cpu"
-    batches = [g.refine_candidates(s) for g, s in zip(grids, level_sums)]
-    groups = []
-    for keys in batches:
-        if len(keys) == 0:
-            groups.append([])
-            continue
-        ls = _level_sums(keys)
-        # the batch is sorted by (level sum, key): groups are contiguous
-        groups.append([keys[ls == v] for v in np.unique(ls)])
-    n_rounds = max((len(g) for g in groups), default=0)
-    for r in range(n_rounds):
-        items = []  # (grid index, keys) of this round, in grid order
-        for gi, gr in enumerate(groups):
-            if r < len(gr):
-                items.append((gi, gr[r]))
-        total = sum(len(k) for _, k in items)
-        if total == 0:
-            continue
-        q = (total + world - 1) // world
-        lo, hi = rank * q, min(total, (rank + 1) * q)
-        local = np.zeros((q, m), dtype=np.float64)
-        off = 0
-        for gi, keys in items:
-            a, b = max(lo, off), min(hi, off + len(keys))
-            if a < b:
-                sub = keys[a - off:b - off]
-                xs = coords_of(sub)
-                t0 = time.perf_counter()
-                fv = np.asarray(f_eval(gi, xs), dtype=np.float64).reshape(len(sub), m)
-                stats.target_s += time.perf_counter() - t0
-                if not np.all(np.isfinite(fv)):
-                    raise FloatingPointError(f"refine_step: non-finite target value on grid {gi}")
-                t0 = time.perf_counter()
-                local[a - lo:b - lo] = grids[gi].hierarchize(sub, fv, device=device)
-                stats.hierarchize_s += time.perf_counter() - t0
-            off += len(keys)
-        t0 = time.perf_counter()
-        if dist is not None:
-            allrows = _all_gather_rows(local, q, m, dist, comm_device)[:total]
-            stats.gathered_bytes += world * q * m * 8
-        else:
-            allrows = local[:total]
-        stats.allgather_s += time.perf_counter() - t0
-        off = 0
-        for gi, keys in items:
-            grids[gi].append(keys, allrows[off:off + len(keys)])
-            off += len(keys)
-        stats.new_nodes += total
-        stats.rounds += 1
-        stats.per_round.append(total)
-    return stats
+    errors: List[BaseException] = []
+
+    def node_eval(gi, xs, count, out, ctx):
+        try:
+            x = np.ctypeslib.as_array(xs, shape=(count, dims[gi])).copy()
+            y = np.asarray(f_eval(gi, x), dtype=np.float64).reshape(count, m)
+            np.ctypeslib.as_array(out, shape=(count, m))[:] = y
+            return 0
+        except BaseException as e:  # surfaced after the C call
+            errors.append(e)
+            return 1
+
+    def allgather(send, recv, nbytes, ctx):
+        try:
+            import torch
+
+            n = nbytes // 8
+            if device:
+                ts = torch.as_tensor(_DeviceArray(send, n), device="cuda")
+                tr = torch.as_tensor(_DeviceArray(recv, n * world), device="cuda")
+                dist.all_gather_into_tensor(tr, ts)
+                torch.cuda.synchronize()
+            else:
+                ts = torch.from_numpy(np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_double)), shape=(n,)).copy())
+                parts = [torch.empty_like(ts) for _ in range(world)]
+                dist.all_gather(parts, ts)
+                np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_double)), shape=(n * world,))[:] = \
+                    torch.cat(parts).numpy()
+            return 0
+        except BaseException as e:
+            errors.append(e)
+            return 1
+
+    f_c = N.NODE_EVALUATOR(node_eval)
+    handles = (C.c_void_p * len(grids))(*[g.handle.value for g in grids])
+    ls = np.ascontiguousarray(level_sums, dtype=np.int32)
+    st = N.RefineStatsC()
+    comm = _nccl_comm(dist) if (dist is not None and device) else None
+    if comm is not None:
+        import torch
+
+        stream = torch.cuda.current_stream().cuda_stream
+        status = N.lib.ddsg_refine_step_nccl(C.cast(handles, C.c_void_p), len(grids), ls.ctypes.data,
+                                             C.cast(f_c, C.c_void_p), None, C.c_void_p(comm), rank, world,
+                                             C.c_void_p(stream), C.byref(st))
+        collective = "ncclAllGather over torch's communicator (native, device buffers)"
+    else:
+        ag_c = N.ALLGATHER_FN(allgather) if dist is not None else None
+        status = N.lib.ddsg_refine_step(C.cast(handles, C.c_void_p), len(grids), ls.ctypes.data,
+                                        C.cast(f_c, C.c_void_p), None, rank, world,
+                                        C.cast(ag_c, C.c_void_p) if ag_c is not None else None, None,
+                                        1 if device else 0, C.byref(st))
+        collective = ("torch.distributed all-gather (%s)" % dist.get_backend()) if dist is not None else "none"
+    if errors:
+        raise errors[0]
+    _check(status)
+    for g in grids:  # max_level follows the appended level sums (ddsg_grid_append)
+        lvl = C.c_int()
+        _check(N.lib.ddsg_grid_info(g.handle, None, None, None, C.byref(lvl), None, None))
+        g.max_level = lvl.value
+    return RefineStats(new_nodes=st.new_nodes, rounds=st.rounds, gathered_bytes=st.gathered_bytes,
+                       hierarchize_s=st.hierarchize_s, target_s=st.target_s, allgather_s=st.allgather_s,
+                       collective=collective)

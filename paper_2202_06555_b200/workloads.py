@@ -60,7 +60,10 @@ class HdmrParts:
     slots: list = field(default_factory=list)  # (dims, b, SparseGridFunction or None)
 
 
-def build_hdmr_parts(cfg: Config) -> HdmrParts:
+def build_hdmr_parts(cfg: Config, build_grids: bool = True) -> HdmrParts:
+    """The config's family, b, anchor values and (build_grids) cut grids;
+    build_grids=False leaves every grid None (the receivers of a broadcast,
+    see broadcast_hdmr_parts)."""
     wl = N.workloads()
     fam = hdmr_family(cfg)
     b = telescoping_b(fam)
@@ -88,9 +91,64 @@ def build_hdmr_parts(cfg: Config) -> HdmrParts:
     # the target's tables were initialised by the anchor evaluation above)
     import concurrent.futures as cf
 
+    if not build_grids:
+        parts.slots.extend((u, bu, None) for u, bu in zip(fam, b))
+        return parts
     with cf.ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
         grids = list(ex.map(lambda u: build_cut(u) if u else None, fam))
     parts.slots.extend((u, bu, g) for u, bu, g in zip(fam, b, grids))
+    return parts
+
+
+def broadcast_hdmr_parts(cfg: Config, dist, device: str, level_1d: Optional[int] = None) -> HdmrParts:
+    """Build once, broadcast: rank 0 builds every cut grid; the node keys and
+    surplus rows go to the other ranks in three broadcasts (counts, keys,
+    surpluses; NCCL over NVLink for CUDA tensors) and every rank assembles the
+    same grids with from_nodes (identical stored order and bits).
+    level_1d overrides the 1-d cut level (the bench builds one level short
+    and refines)."""
+    import dataclasses
+
+    import torch
+
+    rank = dist.get_rank()
+    c = dataclasses.replace(cfg, level_1d=level_1d) if level_1d is not None else cfg
+    parts = build_hdmr_parts(c, build_grids=(rank == 0))
+    idx = [i for i, (u, _, _) in enumerate(parts.slots) if u]
+    counts = torch.zeros(len(idx), dtype=torch.int64, device=device)
+    if rank == 0:
+        counts.copy_(torch.tensor([parts.slots[i][2].size() for i in idx], dtype=torch.int64))
+    dist.broadcast(counts, 0)
+    cnt = counts.cpu().numpy()
+    k_tot = int(sum(int(n) * len(parts.slots[i][0]) for n, i in zip(cnt, idx)))
+    s_tot = int(cnt.sum()) * c.m
+    keys = torch.empty(k_tot, dtype=torch.int32, device=device)
+    sur = torch.empty(s_tot, dtype=torch.float64, device=device)
+    if rank == 0:
+        ks, ss = [], []
+        for i in idx:
+            k, s = parts.slots[i][2].nodes()
+            ks.append(k.reshape(-1).view(np.int32))
+            ss.append(s.reshape(-1))
+        keys.copy_(torch.from_numpy(np.concatenate(ks)))
+        sur.copy_(torch.from_numpy(np.concatenate(ss)))
+    dist.broadcast(keys, 0)
+    dist.broadcast(sur, 0)
+    if rank != 0:
+        kh = keys.cpu().numpy().view(np.uint32)
+        sh = sur.cpu().numpy()
+        ko = so = 0
+        slots = list(parts.slots)
+        for n, i in zip(cnt, idx):
+            u, bu, _ = slots[i]
+            k = len(u)
+            lvl, eps = (c.level_1d, c.eps_1d) if k == 1 else (c.level_2d, c.eps_2d)
+            g = SparseGridFunction.from_nodes(k, c.m, lvl, eps, c.mode, kh[ko:ko + n * k].reshape(n, k),
+                                              sh[so:so + n * c.m].reshape(n, c.m))
+            ko += int(n) * k
+            so += int(n) * c.m
+            slots[i] = (u, bu, g)
+        parts.slots = slots
     return parts
 
 

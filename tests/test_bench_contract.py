@@ -118,6 +118,17 @@ def test_bench_default_line_on_gpu():
 
 
 @pytest.mark.gpu
+def test_bench_parity_field_on_gpu():
+    """The bench line carries a bit-exact check of its own timed inputs
+    against the reference (oracle/_ref, the reference's own grid build)."""
+    d = run_bench("--config", "4", "--steps", "2", "--warmup", "3", "--points", "65536", "--cpu-seconds", "1",
+                  timeout=900)
+    p = d["parity"]
+    assert p["points"] == 4096 and p["bit_identical_points"] == 4096 and p["outputs_outside_tolerance"] == 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["value"] > 0
+
+
+@pytest.mark.gpu
 def test_bench_under_torchrun_nccl_one_rank():
     """The multi-GPU launch path on one GPU: torchrun, a one-rank NCCL group
     (DDSG_BENCH_FORCE_DIST=1), the refinement's surplus all-gather over NCCL,
@@ -137,5 +148,9 @@ def test_bench_under_torchrun_nccl_one_rank():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 1 and d["value"] > 0
-    assert d["refinement"]["collective"] == "all_gather_into_tensor (NCCL)"
-    assert d["refinement"]["allgather_bytes"] == d["refinement"]["new_nodes"] * d["config"]["m"] * 8
+    rf = d["refinement"]
+    # the native step all-gathered over torch's NCCL communicator, and it had work to do
+    assert "ncclAllGather" in rf["collective"] and rf["build"].startswith("rank 0 builds")
+    assert rf["new_nodes"] > 0 and rf["rounds"] > 0
+    assert rf["allgather_bytes"] == rf["new_nodes"] * d["config"]["m"] * 8
+    assert d["parity"] is None or d["parity"]["bit_identical_points"] == d["parity"]["points"]
