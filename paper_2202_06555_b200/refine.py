@@ -60,7 +60,13 @@ def _nccl_comm(dist):
         if dist.get_backend() != "nccl":
             return None
         pg = dist.distributed_c10d._get_default_group()
-        return int(pg._get_backend(torch.device("cuda"))._comm_ptr())
+        backend = pg._get_backend(torch.device("cuda"))
+        ptr = int(backend._comm_ptr())
+        if ptr == 0:  # NCCL communicators are created lazily by the first collective
+            dist.all_reduce(torch.zeros(1, device="cuda"))
+            torch.cuda.synchronize()
+            ptr = int(backend._comm_ptr())
+        return ptr or None
     except Exception:
         return None
 
