@@ -9,6 +9,10 @@ Grids are fed to both sides with the SAME bits in canonical node order
 """
 from __future__ import annotations
 
+import os
+import sys
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -219,7 +223,10 @@ def test_hdmr_fast_mode_config5_tolerance(config5):
     finally:
         vec.set_eval_mode(EXACT)
     ok = within_tol(y, want)
-    assert ok.mean() > 0.999  # FAST is a throughput mode; EXACT is the parity mode
+    # FAST carries no guarantee (include/ddsg_b200.h; DESIGN.md §3.1 measures
+    # its violation rates and why an a-posteriori bound cannot certify it);
+    # on this sample every output is within the north-star tolerance
+    assert ok.all(), f"{(~ok).sum()} of {ok.size} outputs outside 1e-14 + 1e-12|ref|"
 
 
 def test_hdmr_domain_error(config4):
@@ -334,3 +341,51 @@ def test_grid_large_sample_vs_reference_interpolate(cid, n):
     rc, want = ref.eval(x, cfg.m, workers=os.cpu_count() or 1)
     assert rc == 0
     assert np.array_equal(bits(g.interpolate(x)), bits(want))
+
+
+# ------------------------------------------------------------ full n (slow)
+
+@pytest.mark.slow
+def test_config1_full_n_vs_reference_interpolate():
+    """Config 1 at its full n = 65,536 points (BASELINE.json) straight against
+    the reference's SparseGridFunction::interpolate on all host cores."""
+    import os
+
+    cfg = W.CONFIGS[1]
+    g = W.build_grid(cfg)
+    keys, sur = g.nodes()
+    ref = O.ref_from_nodes(cfg.d, cfg.m, cfg.mode, g.max_level, g.eps_gamma, keys, sur)
+    x = W.points(cfg)
+    assert x.shape[0] == 65536
+    rc, want = ref.eval(x, cfg.m, workers=os.cpu_count() or 1)
+    assert rc == 0
+    assert np.array_equal(bits(g.interpolate(x)), bits(want))
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("DDSG_FULL_N") != "1",
+                    reason="minutes of reference CPU time: set DDSG_FULL_N=1 (log in profiles/r2_full_n_config5.txt)")
+def test_config5_full_n_vs_reference_evaluate_batch():
+    """Config 5 at its full n = 2^22 points (the bench's seeded stream, the
+    bench's refined program) against the reference's own build and
+    evaluate_batch on all host cores, bit for bit, chunk by chunk."""
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    import ref_workload as RW
+    import torch
+
+    from paper_2202_06555_b200.ddsg import uniform_point_blocks
+
+    cfg = W.CONFIGS[5]
+    vec = W.build_hdmr(cfg)[0]  # stored node order, as the bench's program
+    lib = RW.use_library(O.REF_PATH)
+    ref = RW.build_hdmr(RW.configs()[5], lib)[0]
+    n, chunk = cfg.n_points, 1 << 18
+    bad = 0
+    for first in range(0, n, chunk):
+        x = uniform_point_blocks(cfg.seed, RW.BLOCK_POINTS, first, chunk, cfg.d)
+        y = vec.evaluate_batch(torch.from_numpy(x).cuda()).cpu().numpy()
+        rc, want = ref.eval(x, workers=os.cpu_count() or 1, flat=False)
+        assert rc == 0
+        bad += int((~np.all(y.view(np.uint64) == want.view(np.uint64), axis=1)).sum())
+        print(f"config5 full n: {first + chunk} / {n} points, {bad} differ", flush=True)
+    assert bad == 0
