@@ -262,6 +262,11 @@ bool FastHdmr::build(const HostProgram& hp) {
         P.rows.push_back(-1);
       }
       P.stride = H.fast_full == 2 ? kRotStride : kStride;
+      if (H.tree_t >= (1 << 13) || H.tree_s > 15 || H.nlev > 15) {
+        why_ = "slot tree position beyond the packed header";
+        return false;
+      }
+      H.pack_core();
       const int64_t table_bytes = static_cast<int64_t>(P.rows.size()) * P.stride * 8;
       H.slab_off = static_cast<int32_t>(kTableOff + table_bytes);
       P.bytes = (kTableOff + table_bytes + P.slab.size() * 2 + 15) / 16 * 16;

@@ -59,7 +59,15 @@ constexpr int kBCont = 4;   // b_kind flag: continue the previous block's accumu
 constexpr int kBMore = 8;   // b_kind flag: another run of the same slot follows
 
 // Per-slot header at the front of every staged block (16-B aligned, 160 B).
+// The first 16 bytes are the core every slot needs, read with ONE broadcast
+// LDS.128: `packed` = k (2 bits) | mode << 2 | nlev << 3 (4 bits) |
+// fast_full << 7 (2 bits) | b_kind << 9 (4 bits) | tree_s << 13 (4 bits) |
+// tree_t << 17 (13 bits); then the row table offset and b.  The rest serves
+// the general (partial-grid) path.
 struct SlotHeader {
+  uint32_t packed;    // core (see above); written by pack_core()
+  int32_t table_off;  // core: byte offset of the row table within the block
+  double b;           // core
   int32_t k;          // slot order 0..2
   int32_t mode;       // boundary mode
   int32_t nlev;       // order 1: max level; order 2: max level per dim
@@ -67,15 +75,18 @@ struct SlotHeader {
   int32_t tree_t;     // leaf position in the perfect-tree embedding
   int32_t tree_s;     // leaf span exponent
   int32_t b_kind;     // bits 0-1: 0 multiply by b, 1 b == 1, 2 b == -1; | kBCont | kBMore
-  double b;
   uint32_t present;   // bit i: canonical subspace i has nodes
   uint32_t full;      // bit i: canonical subspace i has all its cells
-  int32_t table_off;  // byte offset of the row table within the block
   int32_t slab_off;   // byte offset of the int16 slab within the block
   int32_t zero_row;   // index of the all-zero row (target of skipped terms)
   int32_t fast_full;  // 1: full grid of level nlev with finite surpluses (static row layout); 2: same, rotated rows
   int16_t sub_base[kMaxSub];  // first row (full) or slab index (partial) per subspace
-  int16_t pad_[(160 - 64 - 2 * kMaxSub) / 2];
+  int16_t pad_[(160 - 68 - 2 * kMaxSub) / 2];
+  void pack_core() {
+    packed = static_cast<uint32_t>(k) | (static_cast<uint32_t>(mode) << 2) | (static_cast<uint32_t>(nlev) << 3) |
+             (static_cast<uint32_t>(fast_full) << 7) | (static_cast<uint32_t>(b_kind) << 9) |
+             (static_cast<uint32_t>(tree_s) << 13) | (static_cast<uint32_t>(tree_t) << 17);
+  }
 };
 static_assert(sizeof(SlotHeader) == 160, "header layout");
 

@@ -506,20 +506,24 @@ __device__ __forceinline__ void leaf_full2_rot(uint32_t q0, double x0, double x1
   unrotate(q0, acc);
 }
 
-// The header fields every slot needs, fetched with four 16-byte loads.
+// The header fields every slot needs: one broadcast 16-byte load, decoded.
 struct HeaderCore {
-  int32_t k, mode, nlev, d0, d1, tree_t, tree_s, b_kind;
+  int k, mode, nlev, fast_full, b_kind, tree_s, tree_t, table_off;
   double b;
-  uint32_t present, full;
-  int32_t table_off, slab_off, zero_row, fast_full;
 };
-static_assert(sizeof(HeaderCore) == 64, "header core");
 __device__ __forceinline__ HeaderCore load_core(const unsigned char* blk) {
+  const uint4 raw = *reinterpret_cast<const uint4*>(blk);
   HeaderCore h;
-  const uint4* src = reinterpret_cast<const uint4*>(blk);
-  uint4* dst = reinterpret_cast<uint4*>(&h);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) dst[i] = src[i];
+  const uint32_t p = raw.x;
+  h.k = static_cast<int>(p & 3u);
+  h.mode = static_cast<int>((p >> 2) & 1u);
+  h.nlev = static_cast<int>((p >> 3) & 15u);
+  h.fast_full = static_cast<int>((p >> 7) & 3u);
+  h.b_kind = static_cast<int>((p >> 9) & 15u);
+  h.tree_s = static_cast<int>((p >> 13) & 15u);
+  h.tree_t = static_cast<int>(p >> 17);
+  h.table_off = static_cast<int>(raw.y);
+  h.b = __hiloint2double(static_cast<int>(raw.w), static_cast<int>(raw.z));
   return h;
 }
 
@@ -637,7 +641,12 @@ __global__ void __launch_bounds__(kPoints, 1)
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [kMaxStages] full, [kMaxStages] empty
   uint64_t* empty = bars + kMaxStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
+  // [kMaxStages] release counters: the warp whose release completes a
+  // stage's round (count % kWarps == 0) refills it -- right when the slowest
+  // warp is done with the stage, by that warp, instead of a producer thread
+  // spinning on the empty barrier
+  unsigned int* released = reinterpret_cast<unsigned int*>(smem + 16 * kMaxStages);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages + 4 * kMaxStages);
   unsigned char* stages = smem + kHeaderBytes;
   double2* deep = reinterpret_cast<double2*>(stages + n_stages * stage_bytes);
   const int smem_levels = min(max(levels - kTmemLevels, 0), kSmemLevels);
@@ -673,6 +682,7 @@ __global__ void __launch_bounds__(kPoints, 1)
     for (int s = 0; s < n_stages; ++s) {
       mbar_init(&bars[s], 1);
       mbar_init(&empty[s], kWarps);
+      released[s] = 0u;
     }
     fence_mbar_init();
     for (int s = 0; s < n_stages && s < n_active; ++s) {
@@ -693,10 +703,8 @@ __global__ void __launch_bounds__(kPoints, 1)
   double xc1 = xt[static_cast<int64_t>(sdims[1]) * n + pc];
   const int c0 = cb * kCols;
 
-  // ring position of slot a (st) and of slot a-1 (pst), with their phase
-  // parities, advanced incrementally (no runtime division per slot)
-  // ring position of block a (st) and of block a-1 (pst), with their phase
-  // parities, advanced incrementally (no runtime division per block)
+  // ring position of block a (st) with its phase parity, advanced
+  // incrementally (no runtime division per block)
   int st = 0, pst = n_stages - 1;
   uint32_t ph = 0, pph = 1;
   for (int a = 0; a < n_active; ++a) {
@@ -773,7 +781,7 @@ __global__ void __launch_bounds__(kPoints, 1)
           if (c0 + c < m) yp[c] = acc[c];
       }
     }
-    __syncwarp();
+    __syncwarp();  // every lane of this warp is done reading stage st
     if ((tid & 31) == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
     pst = st;
     pph = ph;
