@@ -385,11 +385,15 @@ def run_ours(args, rank, world, local_rank, dist):
     cpu, parity = None, None
     if rank == 0 and not args.no_cpu_baseline and cfg.kind == "hdmr":
         try:
-            cpu, ref_lib = cpu_baseline(cfg, args.cpu_seconds)
+            if world == 1:  # the CPU baseline is reported at N=1 only
+                cpu, ref_lib = cpu_baseline(cfg, args.cpu_seconds)
+            else:  # N > 1: only the parity check's reference program
+                RW = ref_workload()
+                variants = reference_variants()
+                lib = RW.use_library(variants[-1]) if variants else None
+                ref_lib = (RW.build_hdmr(cfg, lib)[0], lib) if lib is not None else None
             if ref_lib is not None:
                 parity = parity_check(ref_lib, cfg, y, min(n_local, 4096))
-            if world > 1:
-                cpu = None  # reported at N=1 only; the parity check still runs on rank 0
         except Exception as e:
             cpu = {"value": None, "error": str(e)[:200]}
 
