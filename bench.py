@@ -320,7 +320,9 @@ def run_ours(args, rank, world, local_rank, dist):
     flops = 2.0 * cfg.m * nnz_total
     achieved = flops / (kernel_ms / 1e3) / 1e12
     traffic = None
-    prof = ROOT / "profiles" / "r1_ncu_fast_hdmr_config5.json"
+    profs = sorted((ROOT / "profiles").glob("r*_ncu_fast_hdmr_config5.json"),
+                   key=lambda p: int(p.name[1:].split("_")[0]))  # the latest round's capture
+    prof = profs[-1] if profs else ROOT / "profiles" / "r1_ncu_fast_hdmr_config5.json"
     if cfg.name == "config5_hdmr_d300" and prof.exists():
         # DRAM bytes of the slot kernel from the committed ncu capture of this
         # config, scaled from its launch (447,392 points) to this step
@@ -328,7 +330,7 @@ def run_ours(args, rank, world, local_rank, dist):
     alg_bytes = 8.0 * n_local * (cfg.d + cfg.m) + 8.0 * obj.info()["n_nodes"] * cfg.m if parts else None
     roofline = {"bound": "fp64", "achieved": achieved, "peak": dfma, "unit": "TFLOP/s",
                 "frac": achieved / dfma, "traffic": traffic, "algorithmic_bytes": alg_bytes,
-                "traffic_source": "profiles/r1_ncu_fast_hdmr_config5.json (dram__bytes_read+write per point x points)",
+                "traffic_source": f"profiles/{prof.name} (dram__bytes_read+write per point x points)",
                 "peak_source": "DFMA issue-rate microbenchmark measured live on this GPU "
                                "(MEASURED_PEAKS.json has no FP64 entry); DMMA peak %.1f TFLOP/s" % dmma,
                 "kernel_ms": kernel_ms, "kernel_share": kernel_ms / ms_per_step,
