@@ -292,6 +292,13 @@ ddsg_status ddsg_workspace_destroy(ddsg_workspace_t* ws);
  * per-point count of cut interpolations.  Errors as ddsg_eval_hdmr. */
 ddsg_status ddsg_eval_hdmr_ws(const ddsg_hdmr_t* h, ddsg_workspace_t* ws, const double* x, int64_t n, double* y,
                               int64_t* bad_index, uint64_t* interp_calls);
+/* VectorizedDdsg::evaluate_batch in the reference's vector<vector<double>>
+ * convention (ddsg_eval.hpp:130-139): point i is read from xrows[i] (dim
+ * doubles) and its outputs written to yrows[i] (m doubles); the rows are
+ * gathered / scattered straight into / out of the pinned staging buffers
+ * (no flattened copy).  Errors as ddsg_eval_hdmr. */
+ddsg_status ddsg_eval_hdmr_rows(const ddsg_hdmr_t* h, ddsg_workspace_t* ws, const double* const* xrows, int64_t n,
+                                double* const* yrows, int64_t* bad_index);
 /* SparseGridFunction::interpolate over n host points through a workspace. */
 ddsg_status ddsg_eval_grid_ws(const ddsg_grid_t* g, ddsg_workspace_t* ws, const double* x, int64_t n, double* y,
                               int64_t* bad_index);

@@ -471,24 +471,33 @@ class VectorizedDdsg {  // ddsg_eval.hpp:28-165
   }
 
   // ddsg_eval.hpp:130-139: elementwise equal to evaluate, independent of
-  // `workers`; a bad point raises task_error with the lowest index.
+  // `workers`; a failing point raises task_error with the lowest failing
+  // index (a wrong query length or a point outside the unit cube, whichever
+  // comes first, like for_each_index).  The rows are staged straight from
+  // and into the vectors (ddsg_eval_hdmr_rows, no flattened copy).
   std::vector<std::vector<double>> evaluate_batch(const std::vector<std::vector<double>>& xs,
                                                   unsigned workers = 1) const {
     (void)workers;
     const std::size_t n = xs.size();
-    std::vector<double> flat(n * static_cast<std::size_t>(dim_));
-    for (std::size_t i = 0; i < n; ++i) {
-      if (xs[i].size() != static_cast<std::size_t>(dim_))
-        throw task_error(i, std::make_exception_ptr(std::invalid_argument("ddsg: query dimension mismatch")),
-                         "task " + std::to_string(i) + " failed: ddsg: query dimension mismatch");
-      std::copy(xs[i].begin(), xs[i].end(), flat.begin() + static_cast<std::ptrdiff_t>(i * dim_));
+    std::size_t first_bad_dim = n;
+    for (std::size_t i = 0; i < n && first_bad_dim == n; ++i)
+      if (xs[i].size() != static_cast<std::size_t>(dim_)) first_bad_dim = i;
+    std::vector<std::vector<double>> out(n, std::vector<double>(static_cast<std::size_t>(out_dim_)));
+    std::vector<const double*> xr(first_bad_dim);
+    std::vector<double*> yr(first_bad_dim);
+    for (std::size_t i = 0; i < first_bad_dim; ++i) {
+      xr[i] = xs[i].data();
+      yr[i] = out[i].data();
     }
-    std::vector<double> y(n * static_cast<std::size_t>(out_dim_));
-    evaluate_batch(flat.data(), static_cast<int64_t>(n), y.data());
-    std::vector<std::vector<double>> out(n);
-    for (std::size_t i = 0; i < n; ++i)
-      out[i].assign(y.begin() + static_cast<std::ptrdiff_t>(i * out_dim_),
-                    y.begin() + static_cast<std::ptrdiff_t>((i + 1) * out_dim_));
+    thread_local EvalWorkspace ws;
+    int64_t bad = -1;
+    const ddsg_status s = ddsg_eval_hdmr_rows(h_.get(), ws.handle(), xr.data(), static_cast<int64_t>(first_bad_dim),
+                                              yr.data(), &bad);
+    if (s != DDSG_OK) detail::raise(s, true, bad);
+    if (first_bad_dim < n)
+      throw task_error(first_bad_dim,
+                       std::make_exception_ptr(std::invalid_argument("ddsg: query dimension mismatch")),
+                       "task " + std::to_string(first_bad_dim) + " failed: ddsg: query dimension mismatch");
     return out;
   }
   // Flat form: x [n][dim] -> y [n][m], host or device pointers.

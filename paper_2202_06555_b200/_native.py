@@ -86,6 +86,7 @@ SIGNATURES = {
     "ddsg_workspace_destroy": (_i, [_p]),
     "ddsg_eval_hdmr_ws": (_i, [_p, _p, _pd, _i64, _pd, C.POINTER(_i64), C.POINTER(C.c_uint64)]),
     "ddsg_eval_grid_ws": (_i, [_p, _p, _pd, _i64, _pd, C.POINTER(_i64)]),
+    "ddsg_eval_hdmr_rows": (_i, [_p, _p, _p, _i64, _p, C.POINTER(_i64)]),
     "ddsg_irbc_refresh_derived": (_i, [_p, _i]),
     "ddsg_irbc_steady_state_lambda": (_i, [_p, C.POINTER(_d)]),
     "ddsg_irbc_foc_residuals": (_i, [_p, _p, _p, _i64, _pd, _pd, _pd, _pd, _pd, C.POINTER(_i64), _p]),

@@ -375,6 +375,24 @@ ddsg_status ddsg_eval_hdmr_ws(const ddsg_hdmr_t* h, ddsg_workspace_t* ws, const 
   });
 }
 
+ddsg_status ddsg_eval_hdmr_rows(const ddsg_hdmr_t* h, ddsg_workspace_t* ws, const double* const* xrows, int64_t n,
+                                double* const* yrows, int64_t* bad_index) {
+  if (bad_index) *bad_index = -1;
+  return guarded([&] {
+    if (!h || !ws) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr_rows: null handle");
+    if (n < 0) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr_rows: negative point count");
+    if (n > 0 && (!xrows || !yrows)) fail(DDSG_INVALID_ARGUMENT, "eval_hdmr_rows: null row arrays");
+    auto* self = const_cast<ddsg_hdmr_t*>(h);
+    const auto prog = self->dev.get(h->prog);
+    const int64_t bad =
+        evaluate_staged(*prog, h->eval_mode == DDSG_EVAL_EXACT, nullptr, n, nullptr, ws->ws, xrows, yrows);
+    if (bad >= 0) {
+      if (bad_index) *bad_index = bad;
+      fail(DDSG_DOMAIN_ERROR, "task " + std::to_string(bad) + " failed: ddsg: query outside unit cube");
+    }
+  });
+}
+
 ddsg_status ddsg_eval_grid_ws(const ddsg_grid_t* g, ddsg_workspace_t* ws, const double* x, int64_t n, double* y,
                               int64_t* bad_index) {
   if (bad_index) *bad_index = -1;

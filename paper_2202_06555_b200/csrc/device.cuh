@@ -134,8 +134,10 @@ class StagedWorkspace {
 
 // Evaluates n points held in pageable host memory through `ws`.  Returns the
 // lowest out-of-domain point index or -1.
+// With xrows / yrows non-null, point i is read from xrows[i] and written to
+// yrows[i] (row pointers) instead of x / y.
 int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,
-                        StagedWorkspace& ws);
+                        StagedWorkspace& ws, const double* const* xrows = nullptr, double* const* yrows = nullptr);
 
 // Support statistics (nnz and order-sensitive hash per point).
 int64_t support(const DeviceProgram& prog, const double* x, int64_t n, int64_t* nnz,

@@ -734,8 +734,36 @@ struct StagedWorkspace::Impl {
 StagedWorkspace::StagedWorkspace() : impl_(new Impl()) {}
 StagedWorkspace::~StagedWorkspace() { delete impl_; }
 
+// Row-pointer copies (the reference's vector<vector<double>> calling
+// convention) on several threads for large chunks.
+static void rows_copy(bool gather, double* flat, const double* const* in_rows, double* const* out_rows, int64_t first,
+                      int64_t cnt, int width) {
+  auto work = [=](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      if (gather)
+        std::memcpy(flat + i * width, in_rows[first + i], static_cast<size_t>(width) * 8);
+      else
+        std::memcpy(out_rows[first + i], flat + i * width, static_cast<size_t>(width) * 8);
+    }
+  };
+  const size_t bytes = static_cast<size_t>(cnt) * width * 8;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t nt = std::min<int64_t>({static_cast<int64_t>(bytes >> 23), 8, static_cast<int64_t>(hw)});
+  if (nt <= 1) {
+    work(0, cnt);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const int64_t part = (cnt + nt - 1) / nt;
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t lo = t * part, hi = std::min(cnt, lo + part);
+    if (lo < hi) pool.emplace_back(work, lo, hi);
+  }
+  for (auto& th : pool) th.join();
+}
+
 int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,
-                        StagedWorkspace& wso) {
+                        StagedWorkspace& wso, const double* const* xrows, double* const* yrows) {
   EvalStats& stats = last_stats();
   stats = EvalStats{};
   kernel_timer().collect();
@@ -762,13 +790,19 @@ int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, i
     const int b = static_cast<int>(i & 1);
     const int64_t off = i * chunk, cnt = std::min(chunk, n - off);
     DDSG_CUDA(cudaEventSynchronize(ws.done[b]));
-    host_copy(y + off * m, ws.hy[b].ptr, static_cast<size_t>(cnt) * m * 8);
+    if (yrows)
+      rows_copy(false, static_cast<double*>(ws.hy[b].ptr), nullptr, yrows, off, cnt, m);
+    else
+      host_copy(y + off * m, ws.hy[b].ptr, static_cast<size_t>(cnt) * m * 8);
   };
   for (int64_t i = 0; i < nchunks; ++i) {
     const int b = static_cast<int>(i & 1);
     const int64_t off = i * chunk, cnt = std::min(chunk, n - off);
     if (i >= 2) drain(i - 2);  // frees slot b
-    host_copy(ws.hx[b].ptr, x + off * d, static_cast<size_t>(cnt) * d * 8);
+    if (xrows)
+      rows_copy(true, static_cast<double*>(ws.hx[b].ptr), xrows, nullptr, off, cnt, d);
+    else
+      host_copy(ws.hx[b].ptr, x + off * d, static_cast<size_t>(cnt) * d * 8);
     cudaStream_t st = ws.st[b];
     DDSG_CUDA(cudaMemcpyAsync(ws.dx[b].ptr, ws.hx[b].ptr, cnt * d * 8, cudaMemcpyHostToDevice, st));
     stats.launches += launch_eval(prog, exact, static_cast<const double*>(ws.dx[b].ptr), cnt, off,

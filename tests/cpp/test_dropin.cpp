@@ -343,6 +343,28 @@ static void gpu_cases() {
       CHECK(throws<std::domain_error>([&] { te.rethrow_cause(); }));
     }
     CHECK(caught);
+    // the lowest failing task wins whatever the failure: a short query at
+    // 200 beats the domain error at 300, a domain error at 50 beats both
+    auto mixed = pts;
+    mixed[300][0] = 2.0;
+    mixed[200].pop_back();
+    int which = -1;
+    try {
+      vec.evaluate_batch(mixed);
+    } catch (const task_error& te) {
+      which = static_cast<int>(te.task_id());
+      CHECK(throws<std::invalid_argument>([&] { te.rethrow_cause(); }));
+    }
+    CHECK(which == 200);
+    mixed[50][1] = -1.0;
+    which = -1;
+    try {
+      vec.evaluate_batch(mixed);
+    } catch (const task_error& te) {
+      which = static_cast<int>(te.task_id());
+      CHECK(throws<std::domain_error>([&] { te.rethrow_cause(); }));
+    }
+    CHECK(which == 50);
   }
   // vector-valued outputs (test_ddsg_eval.cpp:224-242) and vectorized == naive
   // (test_ddsg_eval.cpp:106-120): naive telescoping from per-cut batched calls

@@ -1,0 +1,111 @@
+// What a reference-style C++ caller sees through include/ddsg_b200.hpp
+// (VERDICT r1 next #8): the program of a BASELINE config assembled with the
+// shim's from_nodes / from_parts / compile, then
+//   * evaluate_batch(const vector<vector<double>>&) on pageable std::vector
+//     points -- the reference's calling convention (ddsg_eval.hpp:130-139),
+//     host memory in and out, everything inside the timing;
+//   * the same points as one flat pageable buffer through the C-ABI;
+//   * evaluate(x, out, EvalWorkspace&) per point (n = 1 latency, the
+//     compiled_evaluator shape, time_iteration.hpp:86-91).
+// Prints one JSON object.  Build: make -C tools/shim (links libddsg_b200.so).
+// Usage: bench_shim <program.bin> <n_points> [reps]
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ddsg_b200.hpp"
+
+using namespace ddsg_b200;
+
+template <typename T>
+static T rd(std::ifstream& f) {
+  T v;
+  f.read(reinterpret_cast<char*>(&v), sizeof(T));
+  if (!f) throw std::runtime_error("truncated program file");
+  return v;
+}
+
+static double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int main(int argc, char** argv) {
+  if (argc < 3) {
+    std::fprintf(stderr, "usage: %s program.bin n_points [reps]\n", argv[0]);
+    return 2;
+  }
+  const long long n = std::atoll(argv[2]);
+  const int reps = argc > 3 ? std::atoi(argv[3]) : 3;
+  std::ifstream f(argv[1], std::ios::binary);
+  const int d = rd<int32_t>(f), m = rd<int32_t>(f), ns = rd<int32_t>(f);
+  AnchorPoint anchor;
+  anchor.coords.assign(d, 0.5);
+  anchor.f_anchor.resize(m);
+  f.read(reinterpret_cast<char*>(anchor.f_anchor.data()), m * 8);
+  std::map<ComponentIndex, SparseGridFunction> acc;
+  std::map<ComponentIndex, int> coeff;
+  for (int s = 0; s < ns; ++s) {
+    const int k = rd<int32_t>(f);
+    ComponentIndex u;
+    for (int j = 0; j < k; ++j) u.dims.push_back(rd<int32_t>(f));
+    const int b = rd<int32_t>(f), mode = rd<int32_t>(f), lvl = rd<int32_t>(f);
+    const double eps = rd<double>(f);
+    const long long nn = rd<int64_t>(f);
+    coeff[u] = b;
+    if (k == 0) continue;
+    std::vector<uint32_t> keys(nn * k);
+    std::vector<double> sur(nn * m);
+    f.read(reinterpret_cast<char*>(keys.data()), keys.size() * 4);
+    f.read(reinterpret_cast<char*>(sur.data()), sur.size() * 8);
+    std::vector<GridNode> nodes(nn);
+    for (long long i = 0; i < nn; ++i) {
+      nodes[i].key.assign(keys.begin() + i * k, keys.begin() + (i + 1) * k);
+      nodes[i].surplus.assign(sur.begin() + i * m, sur.begin() + (i + 1) * m);
+    }
+    acc.emplace(u, SparseGridFunction::from_nodes(k, m, lvl, eps, static_cast<BoundaryMode>(mode), nodes));
+  }
+  auto dd = std::make_shared<const DdsgFunction>(
+      DdsgFunction::from_parts(d, m, DdsgOptions{}, anchor, std::move(acc), {}, std::move(coeff), {}));
+  const VectorizedDdsg vec = VectorizedDdsg::compile(dd);
+
+  std::mt19937_64 rng(1005);
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  std::vector<std::vector<double>> xs(n, std::vector<double>(d));
+  std::vector<double> flat(n * d), yflat(n * m);
+  for (long long i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j) flat[i * d + j] = xs[i][j] = unif(rng);
+
+  auto batch = vec.evaluate_batch(xs);  // warm (uploads the program)
+  double t_rows = 1e30, t_flat = 1e30;
+  for (int r = 0; r < reps; ++r) {
+    double t0 = now();
+    batch = vec.evaluate_batch(xs);
+    t_rows = std::min(t_rows, now() - t0);
+    t0 = now();
+    vec.evaluate_batch(flat.data(), n, yflat.data());
+    t_flat = std::min(t_flat, now() - t0);
+  }
+  bool same = true;
+  for (long long i = 0; i < n && same; ++i) same = std::memcmp(batch[i].data(), &yflat[i * m], m * 8) == 0;
+
+  EvalWorkspace ws;
+  std::vector<double> out(m);
+  for (int i = 0; i < 50; ++i) vec.evaluate(xs[i % n], out, ws);
+  const int calls = 2000;
+  const double t0 = now();
+  for (int i = 0; i < calls; ++i) vec.evaluate(xs[i % n], out, ws);
+  const double lat = (now() - t0) / calls;
+  same = same && std::memcmp(out.data(), batch[(calls - 1) % n].data(), m * 8) == 0;
+
+  const double evals = static_cast<double>(n) * m;
+  std::printf("{\"points\": %lld, \"d\": %d, \"m\": %d, \"evaluate_batch_vector_of_vectors_s\": %.4f, "
+              "\"evals_per_s_vector_of_vectors\": %.4e, \"flat_pageable_s\": %.4f, \"evals_per_s_flat_pageable\": %.4e, "
+              "\"n1_evaluate_ws_us\": %.1f, \"outputs_identical\": %s}\n",
+              n, d, m, t_rows, evals / t_rows, t_flat, evals / t_flat, lat * 1e6, same ? "true" : "false");
+  return same ? 0 : 1;
+}
