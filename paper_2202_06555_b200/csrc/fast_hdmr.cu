@@ -66,6 +66,10 @@ static int canon_index(int k, int l1, int l2) {
 
 bool FastHdmr::build(const HostProgram& hp) {
   usable_ = false;
+  if (const char* e = std::getenv("DDSG_SLOT_KERNEL"); e && std::atoi(e) == 0) {  // A/B switch
+    why_ = "disabled by DDSG_SLOT_KERNEL=0";
+    return false;
+  }
   if (hp.plain) {
     why_ = "plain grid";
     return false;
