@@ -641,12 +641,7 @@ __global__ void __launch_bounds__(kPoints, 1)
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [kMaxStages] full, [kMaxStages] empty
   uint64_t* empty = bars + kMaxStages;
-  // [kMaxStages] release counters: the warp whose release completes a
-  // stage's round (count % kWarps == 0) refills it -- right when the slowest
-  // warp is done with the stage, by that warp, instead of a producer thread
-  // spinning on the empty barrier
-  unsigned int* released = reinterpret_cast<unsigned int*>(smem + 16 * kMaxStages);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages + 4 * kMaxStages);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 16 * kMaxStages);
   unsigned char* stages = smem + kHeaderBytes;
   double2* deep = reinterpret_cast<double2*>(stages + n_stages * stage_bytes);
   const int smem_levels = min(max(levels - kTmemLevels, 0), kSmemLevels);
@@ -682,7 +677,6 @@ __global__ void __launch_bounds__(kPoints, 1)
     for (int s = 0; s < n_stages; ++s) {
       mbar_init(&bars[s], 1);
       mbar_init(&empty[s], kWarps);
-      released[s] = 0u;
     }
     fence_mbar_init();
     for (int s = 0; s < n_stages && s < n_active; ++s) {
