@@ -51,6 +51,18 @@ __global__ void transpose_check_kernel(const double* __restrict__ x, int64_t n, 
 
 using namespace fast;
 
+// The kernel instance of this program: arithmetic mode x multi-run carry x order-3 slots.
+LaunchFn FastHdmr::instance_launch(int exact) const {
+  static const LaunchFn tab[8] = {fast_launch_000, fast_launch_001, fast_launch_010, fast_launch_011,
+                                  fast_launch_100, fast_launch_101, fast_launch_110, fast_launch_111};
+  return tab[(exact ? 4 : 0) + (has_carry_ ? 2 : 0) + (has_order3_ ? 1 : 0)];
+}
+AttrFn FastHdmr::instance_attr(int exact) const {
+  static const AttrFn tab[8] = {fast_attr_000, fast_attr_001, fast_attr_010, fast_attr_011,
+                                fast_attr_100, fast_attr_101, fast_attr_110, fast_attr_111};
+  return tab[(exact ? 4 : 0) + (has_carry_ ? 2 : 0) + (has_order3_ ? 1 : 0)];
+}
+
 FastHdmr::~FastHdmr() {
   if (blocks_) cudaFree(blocks_);
   if (block_off_) cudaFree(block_off_);
@@ -58,10 +70,18 @@ FastHdmr::~FastHdmr() {
   if (slot_dims_) cudaFree(slot_dims_);
 }
 
-static int canon_index(int k, int l1, int l2) {
+// Position of subspace l in the canonical (|l|_1, l lex) order of a k-d grid.
+static int canon_index(int k, int l1, int l2, int l3 = 0) {
   if (k == 1) return l1 - 1;
-  const int s = l1 + l2;
-  return (s - 2) * (s - 1) / 2 + (l1 - 1);
+  if (k == 2) {
+    const int s = l1 + l2;
+    return (s - 2) * (s - 1) / 2 + (l1 - 1);
+  }
+  int idx = 0;  // order 3: subspaces of lower level sum, then lex within the sum
+  const int s = l1 + l2 + l3;
+  for (int t = 3; t < s; ++t) idx += (t - 1) * (t - 2) / 2;
+  for (int a = 1; a < l1; ++a) idx += s - a - 1;  // (a, b, c) with b + c = s - a, b, c >= 1
+  return idx + (l2 - 1);
 }
 
 bool FastHdmr::build(const HostProgram& hp) {
@@ -88,6 +108,7 @@ bool FastHdmr::build(const HostProgram& hp) {
   d_ = hp.d;
   m_ = hp.m;
   n_active_ = na;
+  has_order3_ = 0;
   levels_ = levels;
   n_cb_ = (hp.m + kCols - 1) / kCols;
 
@@ -136,8 +157,8 @@ bool FastHdmr::build(const HostProgram& hp) {
   int64_t max_bytes = 0;
   for (int a = 0; a < na; ++a) {
     const int k = hp.slot_k[a];
-    if (k > 2) {
-      why_ = "slot order > 2";
+    if (k > 3) {
+      why_ = "slot order > 3";
       return false;
     }
     const int runs = k == 0 ? 1 : hp.slot_runs[a];
@@ -158,7 +179,8 @@ bool FastHdmr::build(const HostProgram& hp) {
       const int flags = (r > 0 ? kBCont : 0) | (r + 1 < runs ? kBMore : 0);
       dims16.push_back(0);
       dims16.push_back(0);
-      const size_t di = dims16.size() - 2;
+      dims16.push_back(-1);
+      const size_t di = dims16.size() - kSlotDims;
       if (k == 0) {
         H.b_kind = 1;  // b * f_anchor is folded into the staged row
         P.rows.push_back(-1);
@@ -167,13 +189,16 @@ bool FastHdmr::build(const HostProgram& hp) {
         H.b = b;
         H.b_kind = (b == 1.0 ? 1 : (b == -1.0 ? 2 : 0)) | flags;
         H.d0 = hp.slot_dims[hp.slot_dims_off[a]];
-        H.d1 = k == 2 ? hp.slot_dims[hp.slot_dims_off[a] + 1] : 0;
-        if (H.d0 > 32767 || H.d1 > 32767) {
+        H.d1 = k >= 2 ? hp.slot_dims[hp.slot_dims_off[a] + 1] : 0;
+        H.d2 = k == 3 ? hp.slot_dims[hp.slot_dims_off[a] + 2] : 0;
+        if (H.d0 > 32767 || H.d1 > 32767 || H.d2 > 32767) {
           why_ = "point dimension above 32767";
           return false;
         }
         dims16[di] = static_cast<int16_t>(H.d0);
-        dims16[di + 1] = static_cast<int16_t>(H.d1);
+        dims16[di + 1] = static_cast<int16_t>(k >= 2 ? H.d1 : 0);  // unused second dim reads dim 0
+        dims16[di + 2] = static_cast<int16_t>(k == 3 ? H.d2 : -1);  // -1: not an order-3 block
+        has_order3_ = has_order3_ || k == 3;
         std::fill(local.begin(), local.end(), -1);
         for (int64_t q = 0; q < row_count; ++q)
           if (runs == 1 || hp.row_run[row_begin + q] == r) {
@@ -187,15 +212,15 @@ bool FastHdmr::build(const HostProgram& hp) {
         int nlev = 0;
         for (int sb = hp.slot_sub_begin[a]; sb < hp.slot_sub_end[a]; ++sb) {
           const uint8_t* lv = &hp.levels[hp.sub_lv_off[sb]];
-          const int l1 = lv[0], l2 = k == 2 ? lv[1] : 0;
-          // the order-2 leaf walks every (l1, l2) with l1 + l2 <= nlev + 1
-          const int reach = k == 2 ? l1 + l2 - 1 : l1;
-          if ((k == 1 && l1 > kL1) || (k == 2 && reach > kL2)) {
+          const int l1 = lv[0], l2 = k >= 2 ? lv[1] : 0, l3 = k == 3 ? lv[2] : 0;
+          // the order-k leaf walks every subspace with level sum <= nlev + k - 1
+          const int reach = k == 1 ? l1 : (k == 2 ? l1 + l2 - 1 : l1 + l2 + l3 - 2);
+          if ((k == 1 && l1 > kL1) || (k == 2 && reach > kL2) || (k == 3 && reach > kL3)) {
             why_ = "slot level above the kernel's static maximum";
             return false;
           }
-          const int idx = canon_index(k, l1, l2);
-          const int64_t cells = int64_t{1} << (l1 - 1 + (k == 2 ? l2 - 1 : 0));
+          const int idx = canon_index(k, l1, l2, l3);
+          const int64_t cells = int64_t{1} << (l1 - 1 + (k >= 2 ? l2 - 1 : 0) + (k == 3 ? l3 - 1 : 0));
           const int32_t* slab = &hp.slab[hp.sub_slab_off[sb]];
           int64_t n_in = 0;
           for (int64_t c = 0; c < cells; ++c) n_in += slab[c] >= 0 && local[slab[c] - row_begin] >= 0;
@@ -219,7 +244,7 @@ bool FastHdmr::build(const HostProgram& hp) {
         {
           // fast_full: the block is the full grid of its max level (every
           // canonical subspace present and complete) with finite surpluses
-          const int nsub = k == 1 ? nlev : nlev * (nlev + 1) / 2;
+          const int nsub = k == 1 ? nlev : (k == 2 ? nlev * (nlev + 1) / 2 : nlev * (nlev + 1) * (nlev + 2) / 6);
           const uint32_t all = nsub >= 32 ? 0xffffffffu : ((1u << nsub) - 1u);
           bool finite = true;
           for (size_t q = 0; q < P.rows.size() && finite; ++q)
@@ -234,14 +259,14 @@ bool FastHdmr::build(const HostProgram& hp) {
           // adds w * 0 for every absent canonical node (term_row's zero row),
           // so the padded block adds the same terms in the same order, but
           // through the static-row path (no slab lookups, loads one term ahead).
-          const int64_t full_rows = k == 1 ? base1(nlev + 1) : base2(1, nlev + 1);
+          const int64_t full_rows = k == 1 ? base1(nlev + 1) : (k == 2 ? base2(1, nlev + 1) : base3(1, 1, nlev + 1));
           if (!H.fast_full && finite && nlev > 0 && (full_rows + 1) * kStride * 8 <= kMaxPaddedBytes) {
             std::vector<int64_t> padded(static_cast<size_t>(full_rows), -1);
             for (int sb = hp.slot_sub_begin[a]; sb < hp.slot_sub_end[a]; ++sb) {
               const uint8_t* lv = &hp.levels[hp.sub_lv_off[sb]];
-              const int l1 = lv[0], l2 = k == 2 ? lv[1] : 0;
-              const int64_t base = k == 1 ? base1(l1) : base2(l1, l2);
-              const int64_t cells = int64_t{1} << (l1 - 1 + (k == 2 ? l2 - 1 : 0));
+              const int l1 = lv[0], l2 = k >= 2 ? lv[1] : 0, l3 = k == 3 ? lv[2] : 0;
+              const int64_t base = k == 1 ? base1(l1) : (k == 2 ? base2(l1, l2) : base3(l1, l2, l3));
+              const int64_t cells = int64_t{1} << (l1 - 1 + (k >= 2 ? l2 - 1 : 0) + (k == 3 ? l3 - 1 : 0));
               const int32_t* slab = &hp.slab[hp.sub_slab_off[sb]];
               for (int64_t c = 0; c < cells; ++c)
                 if (slab[c] >= 0 && local[slab[c] - row_begin] >= 0) padded[base + c] = slab[c];
@@ -258,7 +283,7 @@ bool FastHdmr::build(const HostProgram& hp) {
           // leaf_full2_rot).  Shallower blocks keep stride 9, conflict-free
           // up to 16 rows and a 1-wavefront broadcast for level 1, which the
           // rotation would turn into 2.  DDSG_SLOT_ROT=0 disables it.
-          if (H.fast_full == 1 && nlev >= rot_min_level && runs == 1 && rot_enabled &&
+          if (H.fast_full == 1 && k <= 2 && nlev >= rot_min_level && runs == 1 && rot_enabled &&
               static_cast<int64_t>(P.rows.size() + 1) * kRotStride * 8 <= kMaxRotBytes)
             H.fast_full = 2;
         }
@@ -289,7 +314,7 @@ bool FastHdmr::build(const HostProgram& hp) {
   }
   const int64_t deep_bytes = std::min(std::max(0, levels - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
   has_carry_ = nb > na ? 1 : 0;
-  const int64_t fixed = kHeaderBytes + deep_bytes + has_carry_ * int64_t{kCols} * kPoints * 8 + (4 * int64_t{nb} + 15) / 16 * 16;
+  const int64_t fixed = kHeaderBytes + deep_bytes + has_carry_ * int64_t{kCols} * kPoints * 8 + (2 * kSlotDims * int64_t{nb} + 15) / 16 * 16;
   n_stages_ = static_cast<int>(std::min<int64_t>(kMaxStages, (227 * 1024 - fixed) / block_bytes_));
   const int64_t smem = fixed + int64_t{n_stages_} * block_bytes_;
   if (n_stages_ < 2 || smem > 227 * 1024) {
@@ -339,12 +364,7 @@ bool FastHdmr::build(const HostProgram& hp) {
   DDSG_CUDA(cudaMemcpy(slot_dims_, dims16.data(), dims16.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
   DDSG_CUDA(cudaMalloc(&block_len_, len.size() * sizeof(int32_t)));
   DDSG_CUDA(cudaMemcpy(block_len_, len.data(), len.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  DDSG_CUDA(fast_attr_00(static_cast<int>(smem)));
-  DDSG_CUDA(fast_attr_10(static_cast<int>(smem)));
-  if (has_carry_) {
-    DDSG_CUDA(fast_attr_01(static_cast<int>(smem)));
-    DDSG_CUDA(fast_attr_11(static_cast<int>(smem)));
-  }
+  for (int e = 0; e < 2; ++e) DDSG_CUDA(instance_attr(e)(static_cast<int>(smem)));
   usable_ = true;
   why_.clear();
   return true;
@@ -359,7 +379,7 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   const int64_t tiles = (n + kPoints - 1) / kPoints;
   const int64_t deep_bytes = std::min(std::max(0, levels_ - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
   const size_t smem = kHeaderBytes + n_stages_ * block_bytes_ + deep_bytes + has_carry_ * size_t{kCols} * kPoints * 8 +
-                      (4 * static_cast<size_t>(n_blocks_) + 15) / 16 * 16;
+                      (2 * kSlotDims * static_cast<size_t>(n_blocks_) + 15) / 16 * 16;
   const dim3 grid(static_cast<unsigned>(tiles * n_cb_));
   kernel_timer().begin(st);
   const KernelArgs args{static_cast<const unsigned char*>(blocks_), block_off_, block_len_, slot_dims_, n_blocks_,
@@ -367,13 +387,8 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   // The dynamic shared-memory limit is a property of the kernel function,
   // shared by every program: set this program's own size before launching
   // (a program built later with smaller stages would otherwise have lowered it).
-  if (exact) {
-    DDSG_CUDA((has_carry_ ? fast_attr_11 : fast_attr_10)(static_cast<int>(smem)));
-    (has_carry_ ? fast_launch_11 : fast_launch_10)(grid, smem, st, args);
-  } else {
-    DDSG_CUDA((has_carry_ ? fast_attr_01 : fast_attr_00)(static_cast<int>(smem)));
-    (has_carry_ ? fast_launch_01 : fast_launch_00)(grid, smem, st, args);
-  }
+  DDSG_CUDA(instance_attr(exact)(static_cast<int>(smem)));
+  instance_launch(exact)(grid, smem, st, args);
   kernel_timer().end(st);
   DDSG_CUDA(cudaGetLastError());
   return 2;

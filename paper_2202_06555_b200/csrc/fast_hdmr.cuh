@@ -9,7 +9,8 @@
 //    kMaxStages stages by one TMA bulk copy (cp.async.bulk + mbarrier
 //    expect-tx; per-stage "empty" mbarriers let warps run ahead).
 //  * Each thread walks the block's subspaces in canonical order (statically
-//    unrolled for order-1 levels <= kL1 and order-2 level sums <= kL2 + 1),
+//    unrolled for order-1 levels <= kL1, order-2 level sums <= kL2 + 1 and
+//    order-3 level sums <= kL3 + 2),
 //    computes the candidate cell and the bit-exact weight, and gathers its
 //    row with LDS.64: rows of kStride (9) doubles, or for full 1-d blocks the
 //    rotated dual-copy rows of kRotStride doubles that keep every half-warp
@@ -45,7 +46,10 @@ constexpr int kPoints = kWarps * 32;     // points per CTA
 constexpr int kL1 = 10;                  // max level of order-1 slots
 constexpr int kL2 = 6;                   // max level (per dim) of order-2 slots
 constexpr int kSub2 = kL2 * (kL2 + 1) / 2;  // canonical subspaces of a full order-2 grid
-constexpr int kMaxSub = kSub2 > kL1 ? kSub2 : kL1;
+constexpr int kL3 = 4;                   // max level (per dim) of order-3 slots: level sums <= kL3 + 2
+constexpr int kSub3 = kL3 * (kL3 + 1) * (kL3 + 2) / 6;  // 20 canonical subspaces (<= 32: bit masks)
+constexpr int kMaxSub = (kSub2 > kL1 ? kSub2 : kL1) > kSub3 ? (kSub2 > kL1 ? kSub2 : kL1) : kSub3;
+constexpr int kSlotDims = 3;             // point dims per slot in the dims table (order <= 3)
 constexpr int kTmemLevels = 8;           // tree levels 1..8 in tensor memory (128 columns per warp)
 constexpr int kSmemLevels = 4;           // levels 9..12 in shared memory (level 0 in registers)
 constexpr int kMaxLevels = kTmemLevels + kSmemLevels;  // 2^12 active slots
@@ -57,6 +61,10 @@ constexpr int kMaxPaddedBytes = 96 * 1024;  // largest row table an adaptive blo
 constexpr int kMaxRotBytes = 48 * 1024;     // largest rotated table (1-d levels <= 8: 32 KB; 2-d level 6: 41 KB)
 constexpr int kBCont = 4;   // b_kind flag: continue the previous block's accumulation (later run)
 constexpr int kBMore = 8;   // b_kind flag: another run of the same slot follows
+
+struct KernelArgs;
+using LaunchFn = void (*)(dim3, size_t, cudaStream_t, const KernelArgs&);
+using AttrFn = cudaError_t (*)(int);
 
 // Per-slot header at the front of every staged block (16-B aligned, 160 B).
 // The first 16 bytes are the core every slot needs, read with ONE broadcast
@@ -71,7 +79,7 @@ struct SlotHeader {
   int32_t k;          // slot order 0..2
   int32_t mode;       // boundary mode
   int32_t nlev;       // order 1: max level; order 2: max level per dim
-  int32_t d0, d1;     // point dims of the slot
+  int32_t d0, d1;     // point dims of the slot (the third of an order-3 slot: d2 below)
   int32_t tree_t;     // leaf position in the perfect-tree embedding
   int32_t tree_s;     // leaf span exponent
   int32_t b_kind;     // bits 0-1: 0 multiply by b, 1 b == 1, 2 b == -1; | kBCont | kBMore
@@ -80,8 +88,9 @@ struct SlotHeader {
   int32_t slab_off;   // byte offset of the int16 slab within the block
   int32_t zero_row;   // index of the all-zero row (target of skipped terms)
   int32_t fast_full;  // 1: full grid of level nlev with finite surpluses (static row layout); 2: same, rotated rows
+  int32_t d2;
   int16_t sub_base[kMaxSub];  // first row (full) or slab index (partial) per subspace
-  int16_t pad_[(160 - 68 - 2 * kMaxSub) / 2];
+  int16_t pad_[(160 - 72 - 2 * kMaxSub) / 2];
   void pack_core() {
     packed = static_cast<uint32_t>(k) | (static_cast<uint32_t>(mode) << 2) | (static_cast<uint32_t>(nlev) << 3) |
              (static_cast<uint32_t>(fast_full) << 7) | (static_cast<uint32_t>(b_kind) << 9) |
@@ -114,13 +123,15 @@ class FastHdmr {
  private:
   bool usable_ = false;
   std::string why_;
-  int d_ = 0, m_ = 0, n_cb_ = 0, cb_group_ = 1, n_active_ = 0, n_blocks_ = 0, has_carry_ = 0, levels_ = 0,
+  fast::LaunchFn instance_launch(int exact) const;
+  fast::AttrFn instance_attr(int exact) const;
+  int d_ = 0, m_ = 0, n_cb_ = 0, cb_group_ = 1, n_active_ = 0, n_blocks_ = 0, has_carry_ = 0, has_order3_ = 0, levels_ = 0,
       n_stages_ = fast::kMaxStages;
   int64_t block_bytes_ = 0;  // stage size (max block), multiple of 128
   void* blocks_ = nullptr;   // [n_cb][n_active] blocks of block_bytes_ each (offsets below)
   int64_t* block_off_ = nullptr;  // device: [n_cb * n_active] byte offsets
   int32_t* block_len_ = nullptr;  // device: [n_cb * n_active] byte lengths
-  int16_t* slot_dims_ = nullptr;  // device: [n_active][2] point dims per slot
+  int16_t* slot_dims_ = nullptr;  // device: [n_blocks][kSlotDims] point dims per block
 };
 
 }  // namespace ddsg_b200

@@ -227,6 +227,52 @@ __device__ __forceinline__ void leaf_order2(const SlotHeader& H, const unsigned 
   for (int i = 0; i < kN; ++i) accum_row<kExact>(acc, w[i], table, row[i]);
 }
 
+template <int kExact, int L>
+__device__ __forceinline__ void leaf_order3(const SlotHeader& H, const unsigned char* blk, double x0,
+                                            double x1, double x2, double (&acc)[kCols], bool all_full) {
+  const unsigned char* table = blk + H.table_off;
+  const int mode = H.mode;
+  double v0[L], v1[L], v2[L];
+  uint32_t k0[L], k1[L], k2[L];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    switch (l) {
+#define DDSG_F(LV)                                  \
+  case LV:                                          \
+    factor<LV>(mode, x0, k0[l - 1], v0[l - 1]);     \
+    factor<LV>(mode, x1, k1[l - 1], v1[l - 1]);     \
+    factor<LV>(mode, x2, k2[l - 1], v2[l - 1]);     \
+    break;
+      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4)
+#undef DDSG_F
+      default:
+        break;
+    }
+  }
+  constexpr int kN = L * (L + 1) * (L + 2) / 6;
+  double w[kN];
+  int row[kN];
+  int idx = 0;
+#pragma unroll
+  for (int s = 3; s <= L + 2; ++s) {
+#pragma unroll
+    for (int l1 = 1; l1 < s - 1; ++l1) {
+#pragma unroll
+      for (int l2 = 1; l1 + l2 < s; ++l2) {
+        const int l3 = s - l1 - l2;
+        // reference: w = 1 * v0, * v1, * v2 in dim order (0 stays 0)
+        const double ww = __dmul_rn(__dmul_rn(v0[l1 - 1], v1[l2 - 1]), v2[l3 - 1]);
+        const int cell = static_cast<int>((k0[l1 - 1] << (l2 + l3 - 2)) | (k1[l2 - 1] << (l3 - 1)) | k2[l3 - 1]);
+        row[idx] = term_row(H, blk, idx, cell, ww, all_full);
+        w[idx] = ww;
+        ++idx;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kN; ++i) accum_row<kExact>(acc, w[i], table, row[i]);
+}
+
 // ------------------------------------------------------------------ full grids
 // A full order-1 grid of max level L stores level l's 2^(l-1) cells from row
 // 2^(l-1) - 1; a full order-2 grid stores canonical subspace (l1, l2) from
@@ -236,6 +282,15 @@ __host__ __device__ constexpr int base2(int l1, int l2) {
   int b = 0;
   for (int t = 2; t < l1 + l2; ++t) b += (t - 1) << (t - 2);
   return b + ((l1 - 1) << (l1 + l2 - 2));
+}
+// A full order-3 grid stores canonical subspace (l1, l2, l3) from row
+// base3(l1, l2, l3): every subspace of level sum s holds 2^(s-3) cells.
+__host__ __device__ constexpr int base3(int l1, int l2, int l3) {
+  int b = 0;
+  const int s = l1 + l2 + l3;
+  for (int t = 3; t < s; ++t) b += ((t - 1) * (t - 2) / 2) << (t - 3);
+  for (int a = 1; a < l1; ++a) b += (s - a - 1) << (s - 3);
+  return b + ((l2 - 1) << (s - 3));
 }
 
 // Exact 1-d factor of the candidate node at static level l (basis.hpp:36-54):
@@ -444,6 +499,62 @@ __device__ __forceinline__ void leaf_full2(const unsigned char* table, double x0
   }
 }
 
+// Full order-3 slot with max level L per dim (level sums <= L + 2),
+// canonical order, stride-9 rows; w = ((v0 v1) v2) in dim order (the
+// modified level-1 factor 1 makes its products exact).
+template <int kExact, int kMode, int L>
+__device__ __forceinline__ void leaf_full3(const unsigned char* table, double x0, double x1, double x2,
+                                           double (&acc)[kCols]) {
+  double v0[L], v1[L], v2[L];
+  uint32_t k0[L], k1[L], k2[L];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    switch (l) {
+#define DDSG_F(LV)                                    \
+  case LV:                                            \
+    factor_full<LV, kMode>(x0, k0[l - 1], v0[l - 1]); \
+    factor_full<LV, kMode>(x1, k1[l - 1], v1[l - 1]); \
+    factor_full<LV, kMode>(x2, k2[l - 1], v2[l - 1]); \
+    break;
+      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4)
+#undef DDSG_F
+      default:
+        break;
+    }
+  }
+  constexpr int kN = L * (L + 1) * (L + 2) / 6;
+  auto term = [&](int i, double& w, int& row) {
+    int idx = 0;
+#pragma unroll
+    for (int s = 3; s <= L + 2; ++s)
+#pragma unroll
+      for (int l1 = 1; l1 < s - 1; ++l1)
+#pragma unroll
+        for (int l2 = 1; l1 + l2 < s; ++l2) {
+          const int l3 = s - l1 - l2;
+          if (idx == i) {
+            w = __dmul_rn(__dmul_rn(v0[l1 - 1], v1[l2 - 1]), v2[l3 - 1]);
+            row = base3(l1, l2, l3) +
+                  static_cast<int>((k0[l1 - 1] << (l2 + l3 - 2)) | (k1[l2 - 1] << (l3 - 1)) | k2[l3 - 1]);
+          }
+          ++idx;
+        }
+  };
+  double wb[2];
+  int rb[2];
+  term(0, wb[0], rb[0]);
+  double buf[2][kCols];  // static ping-pong
+  load_row(table, rb[0], buf[0]);
+#pragma unroll
+  for (int i = 0; i < kN; ++i) {
+    if (i + 1 < kN) {
+      term(i + 1, wb[(i + 1) & 1], rb[(i + 1) & 1]);
+      load_row(table, rb[(i + 1) & 1], buf[(i + 1) & 1]);
+    }
+    fma_row<kExact>(acc, wb[i & 1], buf[i & 1]);
+  }
+}
+
 // Full order-2 slot in the rotated layout (fast_full == 2; max level L >= 6,
 // whose level-sum-7 subspaces have 32 candidate rows and conflict in the
 // stride-9 layout): leaf_full2's terms and order, leaf_full1_rot's loads.
@@ -527,9 +638,10 @@ __device__ __forceinline__ HeaderCore load_core(const unsigned char* blk) {
   return h;
 }
 
-template <int kExact>
+template <int kExact, int kOrder3>
 __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHeader& H, const unsigned char* blk,
-                                              double x0, double x1, double (&acc)[kCols], uint32_t lanebits) {
+                                              double x0, double x1, double x2, double (&acc)[kCols],
+                                              uint32_t lanebits) {
   const unsigned char* table = blk + Hc.table_off;
   if (Hc.fast_full == 2) {
     const uint32_t q0 = smem_u32(table) | lanebits;
@@ -576,8 +688,15 @@ __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHe
       DDSG_P1(1, 8) DDSG_P1(1, 9) DDSG_P1(1, 10)
       DDSG_P2(0, 1) DDSG_P2(0, 2) DDSG_P2(0, 3) DDSG_P2(0, 4) DDSG_P2(0, 5) DDSG_P2(0, 6)
       DDSG_P2(1, 1) DDSG_P2(1, 2) DDSG_P2(1, 3) DDSG_P2(1, 4) DDSG_P2(1, 5) DDSG_P2(1, 6)
+#define DDSG_P3(MD, LV) \
+  case MD * 64 + 48 + LV: \
+    if constexpr (kOrder3 != 0) leaf_full3<kExact, MD, LV>(table, x0, x1, x2, acc); \
+    return;
+      DDSG_P3(0, 1) DDSG_P3(0, 2) DDSG_P3(0, 3) DDSG_P3(0, 4)
+      DDSG_P3(1, 1) DDSG_P3(1, 2) DDSG_P3(1, 3) DDSG_P3(1, 4)
 #undef DDSG_P1
 #undef DDSG_P2
+#undef DDSG_P3
       default:
         break;
     }
@@ -593,10 +712,16 @@ __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHe
   case 32 + LV:     \
     leaf_order2<kExact, LV>(H, blk, x0, x1, acc, all_full); \
     break;
+#define DDSG_L3(LV) \
+  case 48 + LV:     \
+    if constexpr (kOrder3 != 0) leaf_order3<kExact, LV>(H, blk, x0, x1, x2, acc, all_full); \
+    break;
     DDSG_L1(1) DDSG_L1(2) DDSG_L1(3) DDSG_L1(4) DDSG_L1(5) DDSG_L1(6) DDSG_L1(7) DDSG_L1(8) DDSG_L1(9) DDSG_L1(10)
     DDSG_L2(1) DDSG_L2(2) DDSG_L2(3) DDSG_L2(4) DDSG_L2(5) DDSG_L2(6)
+    DDSG_L3(1) DDSG_L3(2) DDSG_L3(3) DDSG_L3(4)
 #undef DDSG_L1
 #undef DDSG_L2
+#undef DDSG_L3
     default:
       break;
   }
@@ -631,7 +756,7 @@ struct TreeStore {
   }
 };
 
-template <int kExact, int kCarry>
+template <int kExact, int kCarry, int kOrder3>
 __global__ void __launch_bounds__(kPoints, 1)
     fast_hdmr_kernel(const unsigned char* __restrict__ blocks, const int64_t* __restrict__ block_off,
                      const int32_t* __restrict__ block_len, const int16_t* __restrict__ slot_dims,
@@ -685,7 +810,7 @@ __global__ void __launch_bounds__(kPoints, 1)
     }
   }
   if (use_tmem && warp == 0) tmem_alloc(tmem_slot, 512);
-  for (int i = tid; i < 2 * n_active; i += kPoints) sdims[i] = slot_dims[i];
+  for (int i = tid; i < kSlotDims * n_active; i += kPoints) sdims[i] = slot_dims[i];
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -693,8 +818,11 @@ __global__ void __launch_bounds__(kPoints, 1)
   if (use_tmem)
     store.tbase = *tmem_slot + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(128 * (warp >> 2));
 
-  double xc0 = xt[static_cast<int64_t>(sdims[0]) * n + pc];
-  double xc1 = xt[static_cast<int64_t>(sdims[1]) * n + pc];
+  // coordinates of the slot's dims (dims table [block][3]: an absent second
+  // dim reads dim 0, unused; the third is -1 unless the block is order 3)
+  auto coord = [&](int a, int j) { return xt[static_cast<int64_t>(sdims[kSlotDims * a + j]) * n + pc]; };
+  double xc0 = coord(0, 0), xc1 = coord(0, 1), xc2 = 0.5;
+  if (kOrder3 && sdims[2] >= 0) xc2 = coord(0, 2);
   const int c0 = cb * kCols;
 
   // ring position of block a (st) with its phase parity, advanced
@@ -728,10 +856,11 @@ __global__ void __launch_bounds__(kPoints, 1)
       for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
     }
     const int k = Hc.k;
-    const double x0 = xc0, x1 = xc1;
+    const double x0 = xc0, x1 = xc1, x2 = xc2;
     if (a + 1 < n_active) {  // prefetch the next block's coordinates
-      xc0 = xt[static_cast<int64_t>(sdims[2 * (a + 1)]) * n + pc];
-      xc1 = xt[static_cast<int64_t>(sdims[2 * (a + 1) + 1]) * n + pc];
+      xc0 = coord(a + 1, 0);
+      xc1 = coord(a + 1, 1);
+      if (kOrder3 && sdims[kSlotDims * (a + 1) + 2] >= 0) xc2 = coord(a + 1, 2);  // order-3 blocks (warp-uniform)
     }
     bool leaf_done = true;
     if (k == 0) {
@@ -739,7 +868,7 @@ __global__ void __launch_bounds__(kPoints, 1)
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = r0[c];
     } else {
-      leaf_dispatch<kExact>(Hc, H, blk, x0, x1, acc, lanebits);
+      leaf_dispatch<kExact, kOrder3>(Hc, H, blk, x0, x1, x2, acc, lanebits);
       if (kCarry && (Hc.b_kind & kBMore)) {  // more runs of this slot follow: park the partial sum
         double2* cs = carry + tid;
 #pragma unroll
@@ -807,25 +936,25 @@ struct KernelArgs {
   int n_stages;
 };
 
-#define DDSG_FAST_INSTANCE(E, C)                                                                          \
-  void fast_launch_##E##C(dim3 grid, size_t smem, cudaStream_t st, const KernelArgs& a) {                 \
-    fast_hdmr_kernel<E, C><<<grid, kPoints, smem, st>>>(a.blocks, a.block_off, a.block_len, a.slot_dims, \
-                                                        a.n_blocks, a.n_cb, a.cb_group, a.levels, a.xt,   \
-                                                        a.n, a.m, a.y, a.stage_bytes, a.n_stages);        \
+#define DDSG_FAST_INSTANCE(E, C, O)                                                                       \
+  void fast_launch_##E##C##O(dim3 grid, size_t smem, cudaStream_t st, const KernelArgs& a) {             \
+    fast_hdmr_kernel<E, C, O><<<grid, kPoints, smem, st>>>(a.blocks, a.block_off, a.block_len, a.slot_dims, \
+                                                           a.n_blocks, a.n_cb, a.cb_group, a.levels, a.xt,   \
+                                                           a.n, a.m, a.y, a.stage_bytes, a.n_stages);        \
   }                                                                                                       \
-  cudaError_t fast_attr_##E##C(int smem) {                                                                \
-    ensure_dynamic_smem(reinterpret_cast<const void*>(fast_hdmr_kernel<E, C>), static_cast<size_t>(smem));  \
+  cudaError_t fast_attr_##E##C##O(int smem) {                                                             \
+    ensure_dynamic_smem(reinterpret_cast<const void*>(fast_hdmr_kernel<E, C, O>), static_cast<size_t>(smem)); \
     return cudaSuccess;                                                                                   \
   }
 
-void fast_launch_00(dim3, size_t, cudaStream_t, const KernelArgs&);
-void fast_launch_01(dim3, size_t, cudaStream_t, const KernelArgs&);
-void fast_launch_10(dim3, size_t, cudaStream_t, const KernelArgs&);
-void fast_launch_11(dim3, size_t, cudaStream_t, const KernelArgs&);
-cudaError_t fast_attr_00(int);
-cudaError_t fast_attr_01(int);
-cudaError_t fast_attr_10(int);
-cudaError_t fast_attr_11(int);
+// Instances: EXACT / FAST x with / without the multi-run carry x with /
+// without order-3 slots (programs without them keep the leaner code).
+#define DDSG_FAST_DECL(E, C, O) \
+  void fast_launch_##E##C##O(dim3, size_t, cudaStream_t, const KernelArgs&); \
+  cudaError_t fast_attr_##E##C##O(int);
+DDSG_FAST_DECL(0, 0, 0) DDSG_FAST_DECL(0, 0, 1) DDSG_FAST_DECL(0, 1, 0) DDSG_FAST_DECL(0, 1, 1)
+DDSG_FAST_DECL(1, 0, 0) DDSG_FAST_DECL(1, 0, 1) DDSG_FAST_DECL(1, 1, 0) DDSG_FAST_DECL(1, 1, 1)
+#undef DDSG_FAST_DECL
 
 }  // namespace fast
 }  // namespace ddsg_b200

@@ -1,8 +1,8 @@
-// Explicit instance fast_hdmr_kernel<1, 0> (kExact = 1, kCarry = 0).
+// Explicit instance fast_hdmr_kernel<1, 1, 0> (kExact = 1, kCarry = 1, kOrder3 = 0).
 #include "fast_hdmr_device.cuh"
 
 namespace ddsg_b200 {
 namespace fast {
-DDSG_FAST_INSTANCE(1, 0)
+DDSG_FAST_INSTANCE(1, 1, 0)
 }  // namespace fast
 }  // namespace ddsg_b200

@@ -123,10 +123,68 @@ def test_deep_1d_cuts(L1, expect_slot_kernel):
     check(vec, d, m, fa, so, pts(d, 400))
 
 
-def test_order3_slots_fall_back_exactly():
-    d, m = 4, 5
-    fam = [()] + [(j,) for j in range(d)] + [(0, 1), (0, 2), (1, 2)] + [(0, 1, 2)]
-    vec, fa, so = make(d, m, fam, {1: 4, 2: 3, 3: 3})
+@pytest.mark.parametrize("mode", [ZERO_BOUNDARY, MODIFIED_LINEAR])
+@pytest.mark.parametrize("L3", [1, 2, 3, 4])
+def test_order3_slots_on_the_slot_kernel(mode, L3):
+    """k_max = 3 families (decompose supports them, hdmr.hpp:364): order-3
+    slots with level sums <= 6 run on the slot kernel (leaf_full3), bit-exact."""
+    d, m = 6, 9
+    fam = ([()] + [(j,) for j in range(d)] + [(0, 1), (0, 2), (1, 2), (2, 4), (3, 5)]
+           + [(0, 1, 2)])
+    vec, fa, so = make(d, m, fam, {1: 5, 2: 4, 3: L3}, mode=mode, seed=L3)
+    assert vec.uses_slot_kernel()
+    check(vec, d, m, fa, so, pts(d, 500))
+
+
+def _partial_triple(m, rng, drop, poison=False):
+    keys = full_keys(3, 4)
+    lv = np.floor(np.log2(keys.astype(np.float64))).astype(int) + 1
+    deep = lv.sum(axis=1) >= 5
+    keep = ~(deep & (rng.random(len(keys)) < drop))
+    keys = keys[keep]
+    sur = rng.uniform(-1, 1, (len(keys), m))
+    if poison:
+        sur[len(keys) // 2, 1] = np.inf
+    return keys, sur
+
+
+@pytest.mark.parametrize("poison", [False, True])
+def test_order3_adaptive_slots(poison):
+    """Partial order-3 grids: padded to the full grid (finite surpluses) or
+    walked through the slab (non-finite surpluses), bit-exact."""
+    rng = np.random.default_rng(5)
+    d, m = 4, 7
+    family = [(), (0,), (1,), (2,), (3,), (0, 1), (0, 2), (1, 2), (0, 1, 2)]
+    b = telescoping_b(family)
+    fa = rng.uniform(-1, 1, m)
+    slots_o, slots_g = [], []
+    for u, bu in zip(family, b):
+        if not u:
+            slots_o.append((u, bu, None))
+            slots_g.append((u, bu, None))
+            continue
+        if len(u) == 3:
+            keys, sur = _partial_triple(m, rng, 0.4, poison)
+        else:
+            keys = full_keys(len(u), 4)
+            sur = rng.uniform(-1, 1, (len(keys), m))
+        slots_o.append((u, bu, (MODIFIED_LINEAR, keys, sur)))
+        slots_g.append((u, bu, SparseGridFunction.from_nodes(len(u), m, 4, 0.0, MODIFIED_LINEAR, keys, sur)))
+    vec = VectorizedDdsg.compile(d, m, fa, slots_g)
+    assert vec.uses_slot_kernel()
+    check(vec, d, m, fa, slots_o, pts(d, 600), nan_ok=poison)
+
+
+@pytest.mark.parametrize("levels,k", [({1: 4, 2: 3, 3: 5}, 3), ({1: 3, 2: 3, 3: 2, 4: 2}, 4)])
+def test_beyond_the_slot_kernel_falls_back_exactly(levels, k):
+    """Order-3 slots of level sum > 6 and order-4 slots run on the generic
+    kernel, still bit-exact."""
+    d, m = 5, 5
+    fam = [()] + [(j,) for j in range(d)] + [(0, 1), (0, 2), (1, 2), (0, 3), (1, 3), (2, 3)] + [(0, 1, 2)]
+    if k == 4:
+        fam += [(0, 1, 3), (0, 2, 3), (1, 2, 3), (0, 1, 2, 3)]
+    fam = sorted(fam, key=lambda u: (len(u), u))
+    vec, fa, so = make(d, m, fam, levels)
     assert not vec.uses_slot_kernel()
     check(vec, d, m, fa, so, pts(d, 300))
 
@@ -245,7 +303,7 @@ def test_small_batches_bit_exact(case, n):
     else:
         d, m = 4, 5
         fam = [()] + [(j,) for j in range(d)] + [(0, 1), (0, 2), (1, 2)] + [(0, 1, 2)]
-        vec, fa, so = make(d, m, fam, {1: 4, 2: 3, 3: 3})
+        vec, fa, so = make(d, m, fam, {1: 4, 2: 3, 3: 5})  # order 3 beyond the slot kernel
     check(vec, d, m, fa, so, pts(d, max(n, 9))[:n], nan_ok=case == "nonfinite")
 
 
