@@ -29,6 +29,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -482,12 +483,29 @@ class VectorizedDdsg {  // ddsg_eval.hpp:28-165
     std::size_t first_bad_dim = n;
     for (std::size_t i = 0; i < n && first_bad_dim == n; ++i)
       if (xs[i].size() != static_cast<std::size_t>(dim_)) first_bad_dim = i;
-    std::vector<std::vector<double>> out(n, std::vector<double>(static_cast<std::size_t>(out_dim_)));
+    // the result rows (allocated on several threads for large batches: the
+    // reference allocates them inside its workers too, ddsg_eval.hpp:134-136)
+    std::vector<std::vector<double>> out(n);
     std::vector<const double*> xr(first_bad_dim);
     std::vector<double*> yr(first_bad_dim);
-    for (std::size_t i = 0; i < first_bad_dim; ++i) {
-      xr[i] = xs[i].data();
-      yr[i] = out[i].data();
+    auto alloc = [&](std::size_t lo, std::size_t hi) {
+      for (std::size_t i = lo; i < hi; ++i) {
+        out[i].resize(static_cast<std::size_t>(out_dim_));
+        if (i < first_bad_dim) {
+          xr[i] = xs[i].data();
+          yr[i] = out[i].data();
+        }
+      }
+    };
+    const std::size_t nt = n < (std::size_t{1} << 16) ? 1 : std::min<std::size_t>(8, std::max(1u, std::thread::hardware_concurrency()));
+    if (nt <= 1) {
+      alloc(0, n);
+    } else {
+      std::vector<std::thread> pool;
+      const std::size_t part = (n + nt - 1) / nt;
+      for (std::size_t t = 0; t < nt; ++t)
+        if (t * part < n) pool.emplace_back(alloc, t * part, std::min(n, (t + 1) * part));
+      for (auto& th : pool) th.join();
     }
     thread_local EvalWorkspace ws;
     int64_t bad = -1;
