@@ -227,50 +227,32 @@ __device__ __forceinline__ void leaf_order2(const SlotHeader& H, const unsigned 
   for (int i = 0; i < kN; ++i) accum_row<kExact>(acc, w[i], table, row[i]);
 }
 
-template <int kExact, int L>
-__device__ __forceinline__ void leaf_order3(const SlotHeader& H, const unsigned char* blk, double x0,
-                                            double x1, double x2, double (&acc)[kCols], bool all_full) {
+// General-path order-3 slot (partial grids with non-finite surpluses: rare):
+// a rolled loop over the canonical subspaces with runtime-level factors
+// (basis.cuh), compact code instead of the unrolled static leaves.
+template <int kExact>
+__device__ __forceinline__ void leaf_order3(const SlotHeader& H, const unsigned char* blk, double x0, double x1,
+                                            double x2, double (&acc)[kCols], bool all_full) {
   const unsigned char* table = blk + H.table_off;
   const int mode = H.mode;
-  double v0[L], v1[L], v2[L];
-  uint32_t k0[L], k1[L], k2[L];
-#pragma unroll
-  for (int l = 1; l <= L; ++l) {
-    switch (l) {
-#define DDSG_F(LV)                                  \
-  case LV:                                          \
-    factor<LV>(mode, x0, k0[l - 1], v0[l - 1]);     \
-    factor<LV>(mode, x1, k1[l - 1], v1[l - 1]);     \
-    factor<LV>(mode, x2, k2[l - 1], v2[l - 1]);     \
-    break;
-      DDSG_F(1) DDSG_F(2) DDSG_F(3) DDSG_F(4)
-#undef DDSG_F
-      default:
-        break;
-    }
-  }
-  constexpr int kN = L * (L + 1) * (L + 2) / 6;
-  double w[kN];
-  int row[kN];
+  const int L = H.nlev;
   int idx = 0;
-#pragma unroll
+#pragma unroll 1
   for (int s = 3; s <= L + 2; ++s) {
-#pragma unroll
+#pragma unroll 1
     for (int l1 = 1; l1 < s - 1; ++l1) {
-#pragma unroll
-      for (int l2 = 1; l1 + l2 < s; ++l2) {
+#pragma unroll 1
+      for (int l2 = 1; l1 + l2 < s; ++l2, ++idx) {
         const int l3 = s - l1 - l2;
+        const uint32_t k0 = cell_at(x0, l1), k1 = cell_at(x1, l2), k2 = cell_at(x2, l3);
         // reference: w = 1 * v0, * v1, * v2 in dim order (0 stays 0)
-        const double ww = __dmul_rn(__dmul_rn(v0[l1 - 1], v1[l2 - 1]), v2[l3 - 1]);
-        const int cell = static_cast<int>((k0[l1 - 1] << (l2 + l3 - 2)) | (k1[l2 - 1] << (l3 - 1)) | k2[l3 - 1]);
-        row[idx] = term_row(H, blk, idx, cell, ww, all_full);
-        w[idx] = ww;
-        ++idx;
+        const double w = __dmul_rn(__dmul_rn(basis_at(mode, l1, k0, x0), basis_at(mode, l2, k1, x1)),
+                                   basis_at(mode, l3, k2, x2));
+        const int cell = static_cast<int>((k0 << (l2 + l3 - 2)) | (k1 << (l3 - 1)) | k2);
+        accum_row<kExact>(acc, w, table, term_row(H, blk, idx, cell, w, all_full));
       }
     }
   }
-#pragma unroll
-  for (int i = 0; i < kN; ++i) accum_row<kExact>(acc, w[i], table, row[i]);
 }
 
 // ------------------------------------------------------------------ full grids
@@ -499,6 +481,51 @@ __device__ __forceinline__ void leaf_full2(const unsigned char* table, double x0
   }
 }
 
+// Canonical order-3 subspace i: (l1, l2, l3) with level sums ascending, lex.
+struct Sub3 {
+  int l1, l2, l3;
+};
+__host__ __device__ constexpr Sub3 sub3(int i) {
+  int idx = 0;
+  for (int s = 3; s < 32; ++s)
+    for (int l1 = 1; l1 < s - 1; ++l1)
+      for (int l2 = 1; l1 + l2 < s; ++l2) {
+        if (idx == i) return Sub3{l1, l2, s - l1 - l2};
+        ++idx;
+      }
+  return Sub3{1, 1, 1};
+}
+
+// Term I of a full order-3 leaf: weight and row from compile-time levels.
+template <int kMode, int L, int I>
+__device__ __forceinline__ void term3(const double (&v0)[L], const double (&v1)[L], const double (&v2)[L],
+                                      const uint32_t (&k0)[L], const uint32_t (&k1)[L], const uint32_t (&k2)[L],
+                                      double& w, int& row) {
+  constexpr Sub3 t = sub3(I);
+  w = __dmul_rn(__dmul_rn(v0[t.l1 - 1], v1[t.l2 - 1]), v2[t.l3 - 1]);
+  row = base3(t.l1, t.l2, t.l3) + static_cast<int>((k0[t.l1 - 1] << (t.l2 + t.l3 - 2)) |
+                                                   (k1[t.l2 - 1] << (t.l3 - 1)) | k2[t.l3 - 1]);
+}
+
+// Terms I.. of a full order-3 leaf, one term ahead (static ping-pong).
+template <int kExact, int kMode, int L, int I>
+__device__ __forceinline__ void walk3(const unsigned char* table, const double (&v0)[L], const double (&v1)[L],
+                                      const double (&v2)[L], const uint32_t (&k0)[L], const uint32_t (&k1)[L],
+                                      const uint32_t (&k2)[L], double (&acc)[kCols], double w, double (&cur)[kCols]) {
+  constexpr int kN = L * (L + 1) * (L + 2) / 6;
+  if constexpr (I + 1 < kN) {
+    double wn;
+    int rn;
+    term3<kMode, L, I + 1>(v0, v1, v2, k0, k1, k2, wn, rn);
+    double nxt[kCols];
+    load_row(table, rn, nxt);
+    fma_row<kExact>(acc, w, cur);
+    walk3<kExact, kMode, L, I + 1>(table, v0, v1, v2, k0, k1, k2, acc, wn, nxt);
+  } else {
+    fma_row<kExact>(acc, w, cur);
+  }
+}
+
 // Full order-3 slot with max level L per dim (level sums <= L + 2),
 // canonical order, stride-9 rows; w = ((v0 v1) v2) in dim order (the
 // modified level-1 factor 1 makes its products exact).
@@ -522,37 +549,12 @@ __device__ __forceinline__ void leaf_full3(const unsigned char* table, double x0
         break;
     }
   }
-  constexpr int kN = L * (L + 1) * (L + 2) / 6;
-  auto term = [&](int i, double& w, int& row) {
-    int idx = 0;
-#pragma unroll
-    for (int s = 3; s <= L + 2; ++s)
-#pragma unroll
-      for (int l1 = 1; l1 < s - 1; ++l1)
-#pragma unroll
-        for (int l2 = 1; l1 + l2 < s; ++l2) {
-          const int l3 = s - l1 - l2;
-          if (idx == i) {
-            w = __dmul_rn(__dmul_rn(v0[l1 - 1], v1[l2 - 1]), v2[l3 - 1]);
-            row = base3(l1, l2, l3) +
-                  static_cast<int>((k0[l1 - 1] << (l2 + l3 - 2)) | (k1[l2 - 1] << (l3 - 1)) | k2[l3 - 1]);
-          }
-          ++idx;
-        }
-  };
-  double wb[2];
-  int rb[2];
-  term(0, wb[0], rb[0]);
-  double buf[2][kCols];  // static ping-pong
-  load_row(table, rb[0], buf[0]);
-#pragma unroll
-  for (int i = 0; i < kN; ++i) {
-    if (i + 1 < kN) {
-      term(i + 1, wb[(i + 1) & 1], rb[(i + 1) & 1]);
-      load_row(table, rb[(i + 1) & 1], buf[(i + 1) & 1]);
-    }
-    fma_row<kExact>(acc, wb[i & 1], buf[i & 1]);
-  }
+  double w;
+  int row;
+  term3<kMode, L, 0>(v0, v1, v2, k0, k1, k2, w, row);
+  double cur[kCols];
+  load_row(table, row, cur);
+  walk3<kExact, kMode, L, 0>(table, v0, v1, v2, k0, k1, k2, acc, w, cur);
 }
 
 // Full order-2 slot in the rotated layout (fast_full == 2; max level L >= 6,
@@ -714,7 +716,7 @@ __device__ __forceinline__ void leaf_dispatch(const HeaderCore& Hc, const SlotHe
     break;
 #define DDSG_L3(LV) \
   case 48 + LV:     \
-    if constexpr (kOrder3 != 0) leaf_order3<kExact, LV>(H, blk, x0, x1, x2, acc, all_full); \
+    if constexpr (kOrder3 != 0) leaf_order3<kExact>(H, blk, x0, x1, x2, acc, all_full); \
     break;
     DDSG_L1(1) DDSG_L1(2) DDSG_L1(3) DDSG_L1(4) DDSG_L1(5) DDSG_L1(6) DDSG_L1(7) DDSG_L1(8) DDSG_L1(9) DDSG_L1(10)
     DDSG_L2(1) DDSG_L2(2) DDSG_L2(3) DDSG_L2(4) DDSG_L2(5) DDSG_L2(6)
