@@ -26,12 +26,20 @@ from paper_2202_06555_b200.workloads import telescoping_b
 pytestmark = pytest.mark.gpu
 
 
+def level_vectors(k: int, budget: int):
+    """Level vectors l (l_j >= 1) with sum(l_j - 1) <= budget."""
+    if k == 0:
+        yield ()
+        return
+    for e in range(budget + 1):
+        for rest in level_vectors(k - 1, budget - e):
+            yield (e + 1,) + rest
+
+
 def regular_keys(k: int, L: int) -> np.ndarray:
     """All nodes of the regular k-dim grid of level L (level sum <= L + k - 1)."""
     out = []
-    for lv in itertools.product(range(1, L + 1), repeat=k):
-        if sum(lv) > L + k - 1:
-            continue
+    for lv in level_vectors(k, L - 1):
         for cells in itertools.product(*[range(1 << (l - 1)) for l in lv]):
             out.append([(1 << (l - 1)) + c for l, c in zip(lv, cells)])
     return np.array(out, dtype=np.uint32).reshape(-1, k)
@@ -103,3 +111,45 @@ def test_random_programs_cover_every_path():
     """The seeds above reach both the slot kernel and its fallback."""
     paths = {random_program(s)[4].uses_slot_kernel() for s in range(40)}
     assert paths == {True, False}
+
+
+# ------------------------------------------------------------- plain grids
+
+def random_grid(seed: int):
+    """A random plain grid: d 1..24 (dense walk <= 20 dims, sparse walk for
+    modified-linear grids up to 64, generic beyond), level 1..max for the
+    dimension, random deep-node subsets, several stored-order runs, m 1..30,
+    batches on both sides of the Morton-sort threshold (4096)."""
+    rng = np.random.default_rng(10_000 + seed)
+    d = int(rng.integers(1, 25))
+    L = int(rng.integers(1, {1: 12, 2: 8, 3: 6}.get(d, 5 if d <= 8 else 3) + 1))
+    m = int(rng.choice([1, 2, 5, 11, 21, 30]))
+    mode = int(rng.choice([ZERO_BOUNDARY, MODIFIED_LINEAR]))
+    keys = regular_keys(d, L)
+    if rng.random() < 0.5:
+        lv = np.floor(np.log2(keys.astype(np.float64))).astype(int) + 1
+        keep = (lv.sum(axis=1) <= d + 1) | (rng.random(len(keys)) < rng.uniform(0.3, 0.9))
+        keys = keys[keep]
+    if rng.random() < 0.3 and len(keys) > 2:
+        cut = int(rng.integers(1, len(keys)))
+        keys = np.concatenate([keys[cut:], keys[:cut]])
+    sur = rng.uniform(-1, 1, (len(keys), m)) * 10.0 ** rng.uniform(-3, 3)
+    g = SparseGridFunction.from_nodes(d, m, L, 0.0, mode, keys, sur)
+    n = int(rng.choice([1, 7, 300, 4096, 6000]))
+    x = O.port_uniform_points(20_000 + seed, n, d)
+    special = np.array([0.0, 1.0, 0.5, 0.125, 1 - 2.0 ** -53, 5e-324])
+    mask = rng.random(x.shape) < 0.05
+    x[mask] = rng.choice(special, size=int(mask.sum()))
+    return d, m, mode, keys, sur, g, x
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_random_grid_bit_exact(seed):
+    d, m, mode, keys, sur, g, x = random_grid(seed)
+    rc, want, _ = O.port_grid_eval(d, m, mode, keys, sur, x)
+    assert rc == 0
+    y = g.interpolate(x)
+    assert np.array_equal(bits(y), bits(want)), f"seed {seed}: {int((bits(y) != bits(want)).sum())} outputs differ"
+    nnz_o, h_o = O.port_grid_support(d, mode, keys, x)
+    nnz, h = g.support(x)
+    assert np.array_equal(nnz, nnz_o) and np.array_equal(h, h_o)
