@@ -391,6 +391,113 @@ __global__ void __launch_bounds__(256) slot_tree_kernel(int na, DeviceProgram::S
   if (threadIdx.x < nc) y[p * m + c0 + threadIdx.x] = vals[root * kCols + threadIdx.x];
 }
 
+// -------------------------------------------------- small plain batches
+//
+// A few points on the plain kernels are latency-bound: one thread walks all
+// subspaces of its point (config 2: 0.77 ms, config 3: 6.4 ms at n = 1).
+// Small batches instead split the walk: plain_terms_kernel computes, with
+// one thread per (point, subspace), the term's weight (the reference's
+// dim-ordered product with early exit), the stored-order run of its node
+// (-1 for a term the reference skips: w == 0 or no node) and copies the
+// node's surplus row into a dense [point][subspace][m] block (zeros for a
+// skipped term); plain_sum_kernel then runs one thread per (point, output)
+// through the terms in canonical order per run, acc = acc + w * s (mul then
+// add; FMA in FAST mode).  Every load of the sum is independent of the
+// accumulator (a skipped or other-run term adds 0 * 0 through a select,
+// which leaves the accumulator's bits unchanged: it is never -0), so the
+// serial chain is only the additions.  Same operations, same order:
+// bit-identical.
+__global__ void __launch_bounds__(128) plain_terms_kernel(EvalParams P, const double* __restrict__ x, int64_t n,
+                                                          int64_t base, double* __restrict__ wts,
+                                                          int8_t* __restrict__ runs_out, double* __restrict__ srows,
+                                                          unsigned long long* bad) {
+  const int n_sub = P.slot_sub_end[0] - P.slot_sub_begin[0];
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p = tid / n_sub;
+  const int t = static_cast<int>(tid % n_sub);
+  if (p >= n) return;
+  const int64_t pt = p * n_sub + t;
+  double* so = srows + pt * P.m;
+  const double* xp = x + p * P.d;
+  if (!point_ok(xp, P.d)) {  // the call fails; never index the slab with a bad cell
+    if (t == 0) atomicMin(bad, static_cast<unsigned long long>(base + p));
+    wts[pt] = 0.0;
+    runs_out[pt] = -1;
+    for (int c = 0; c < P.m; ++c) so[c] = 0.0;
+    return;
+  }
+  const int s = P.slot_sub_begin[0] + t;
+  const uint8_t* lv = P.levels + P.sub_lv_off[s];
+  const int mode = P.slot_mode[0];
+  double w = 1.0;
+  int64_t lin = 0;
+  for (int j = 0; j < P.d; ++j) {
+    const int l = lv[j];
+    const double xv = xp[j];
+    const uint32_t kk = cell_at(xv, l);
+    w = __dmul_rn(w, basis_at(mode, l, kk, xv));
+    lin = (lin << (l - 1)) | kk;
+    if (w == 0.0) break;
+  }
+  const int32_t row = w != 0.0 ? P.slab[P.sub_slab_off[s] + lin] : -1;
+  const int run = row < 0 ? -1 : (P.slot_runs[0] > 1 ? static_cast<int>(P.row_run[row]) : 0);
+  wts[pt] = run < 0 ? 0.0 : w;
+  runs_out[pt] = static_cast<int8_t>(run);
+  const double* sr = P.surplus + static_cast<int64_t>(row < 0 ? 0 : row) * P.m;
+  for (int c = 0; c < P.m; ++c) so[c] = run < 0 ? 0.0 : sr[c];
+}
+
+template <int kExact>
+__global__ void __launch_bounds__(128) plain_sum_kernel(EvalParams P, int64_t n, const double* __restrict__ wts,
+                                                        const int8_t* __restrict__ runs_in,
+                                                        const double* __restrict__ srows, double* __restrict__ y) {
+  const int n_sub = P.slot_sub_end[0] - P.slot_sub_begin[0];
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p = tid / P.m;
+  const int c = static_cast<int>(tid % P.m);
+  if (p >= n) return;
+  const double* W = wts + p * n_sub;
+  const int8_t* R = runs_in + p * n_sub;
+  const double* S = srows + p * static_cast<int64_t>(n_sub) * P.m + c;
+  const int runs = P.slot_runs[0];
+  // software pipeline: the loads of block b + 1 are issued before the
+  // additions of block b, so the serial chain is the additions alone
+  constexpr int kAhead = 16;
+  auto fetch = [&](int t0, double (&wv)[kAhead], double (&sv)[kAhead], int (&rv)[kAhead]) {
+#pragma unroll
+    for (int k = 0; k < kAhead; ++k) {
+      const int t = min(t0 + k, n_sub - 1);
+      wv[k] = __ldg(W + t);
+      sv[k] = __ldg(S + static_cast<int64_t>(t) * P.m);
+      rv[k] = t0 + k < n_sub ? static_cast<int>(__ldg(R + t)) : -1;
+    }
+  };
+  double acc = 0.0;
+  for (int run = 0; run < runs; ++run) {  // stored order = runs of canonical order (sparse_grid.hpp:117-127)
+    double wa[kAhead], sa[kAhead], wb[kAhead], sb[kAhead];
+    int ra[kAhead], rb[kAhead];
+    fetch(0, wa, sa, ra);
+    for (int t0 = 0; t0 < n_sub; t0 += 2 * kAhead) {
+      if (t0 + kAhead < n_sub) fetch(t0 + kAhead, wb, sb, rb);
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) {
+        const bool use = ra[k] == run;
+        acc = kExact ? __dadd_rn(acc, __dmul_rn(use ? wa[k] : 0.0, use ? sa[k] : 0.0))
+                     : __fma_rn(use ? wa[k] : 0.0, use ? sa[k] : 0.0, acc);
+      }
+      if (t0 + kAhead >= n_sub) break;
+      if (t0 + 2 * kAhead < n_sub) fetch(t0 + 2 * kAhead, wa, sa, ra);
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) {
+        const bool use = rb[k] == run;
+        acc = kExact ? __dadd_rn(acc, __dmul_rn(use ? wb[k] : 0.0, use ? sb[k] : 0.0))
+                     : __fma_rn(use ? wb[k] : 0.0, use ? sb[k] : 0.0, acc);
+      }
+    }
+  }
+  y[p * P.m + c] = acc;
+}
+
 // Support statistics: nnz and an order-sensitive FNV-1a hash over
 // (slot id, stored node index) of every term with w != 0, in evaluation order.
 __global__ void support_kernel(EvalParams P, const double* __restrict__ x, int64_t n, int64_t base,
@@ -541,12 +648,47 @@ static int64_t small_batch_points() {
   return v;
 }
 
+// Largest plain-grid batch that takes the small-batch path: while the
+// sequential per-(point, output) sums over the subspaces beat the plain
+// kernel's one-thread-per-point walk (DDSG_SMALL_PLAIN overrides, 0 disables).
+static int64_t small_plain_points(const DeviceProgram& prog) {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DDSG_SMALL_PLAIN");
+    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{256};
+  }();
+  const HostProgram& hp = prog.host();
+  const int64_t n_sub = hp.slot_sub_end.empty() ? 0 : hp.slot_sub_end[0] - hp.slot_sub_begin[0];
+  if (n_sub <= 0 || hp.slot_runs.empty() || hp.slot_runs[0] > 127) return 0;
+  // keep the term scratch ([point][subspace] weights, runs and surplus rows) <= 256 MiB
+  return std::min<int64_t>(v, (int64_t{256} << 20) / ((8 * hp.m + 9) * n_sub));
+}
+
 // Launches the evaluation of n device-resident points; returns kernel launches.
 static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* dx, int64_t n,
                            int64_t base, double* dy, unsigned long long* dbad, cudaStream_t st,
                            Scratch& xt_scratch) {
   if (n <= 0) return 0;
   const EvalParams P = prog.params(exact);
+  if (P.plain && n <= small_plain_points(prog)) {
+    // few points: per-term weights and rows in parallel, then the canonical-order sums
+    const int n_sub = prog.host().slot_sub_end[0] - prog.host().slot_sub_begin[0];
+    const size_t terms = static_cast<size_t>(n) * n_sub;
+    char* ws = static_cast<char*>(xt_scratch.get(terms * (8 * static_cast<size_t>(P.m) + 9) + 64));
+    double* srows = reinterpret_cast<double*>(ws);
+    double* wts = srows + terms * P.m;
+    int8_t* runs = reinterpret_cast<int8_t*>(wts + terms);
+    kernel_timer().begin(st);
+    plain_terms_kernel<<<static_cast<unsigned>((terms + 127) / 128), 128, 0, st>>>(P, dx, n, base, wts, runs, srows,
+                                                                                     dbad);
+    const int64_t outs = n * P.m;
+    if (exact)
+      plain_sum_kernel<1><<<static_cast<unsigned>((outs + 127) / 128), 128, 0, st>>>(P, n, wts, runs, srows, dy);
+    else
+      plain_sum_kernel<0><<<static_cast<unsigned>((outs + 127) / 128), 128, 0, st>>>(P, n, wts, runs, srows, dy);
+    kernel_timer().end(st);
+    DDSG_CUDA(cudaGetLastError());
+    return 2;
+  }
   if (const PlainGrid* pg = prog.plain()) {
     const size_t wb = pg->workspace_bytes(n);
     return pg->launch(exact, dx, n, base, dy, dbad, wb ? xt_scratch.get(wb) : nullptr, st);
