@@ -118,7 +118,12 @@ def refine_step(grids: Sequence[SparseGridFunction], level_sums: Sequence[int],
             if device:
                 ts = torch.as_tensor(_DeviceArray(send, n), device="cuda")
                 tr = torch.as_tensor(_DeviceArray(recv, n * world), device="cuda")
-                dist.all_gather_into_tensor(tr, ts)
+                if dist.get_backend() == "nccl":
+                    dist.all_gather_into_tensor(tr, ts)
+                else:  # gloo: host staging of the device rows
+                    parts = [torch.empty(n, dtype=torch.float64) for _ in range(world)]
+                    dist.all_gather(parts, ts.cpu())
+                    tr.copy_(torch.cat(parts))
                 torch.cuda.synchronize()
             else:
                 ts = torch.from_numpy(np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_double)), shape=(n,)).copy())

@@ -148,3 +148,43 @@ def test_native_refinement_over_torch_nccl_communicator(tmp_path):
         h = W.build_cut_grid(cfg, u, lvl + 1, cfg.eps_1d if len(u) == 1 else cfg.eps_2d)
         k, s = h.nodes()
         assert np.array_equal(o[f"k{i}"], k) and np.array_equal(bits(o[f"s{i}"]), bits(s))
+
+
+def _gloo_device_refine_worker(rank, world, port, out_path):
+    import torch
+
+    from paper_2202_06555_b200.refine import refine_step
+
+    torch.cuda.set_device(0)
+    dist = _init(rank, world, port, "gloo")
+    try:
+        cfg = W.CONFIGS[5]
+        slots = [((3,), 5), ((250,), 4), ((3, 17), 3), ((40, 299), 2)]
+        grids = [W.build_cut_grid(cfg, u, lvl, cfg.eps_1d if len(u) == 1 else cfg.eps_2d) for u, lvl in slots]
+        cuts = [W.CutTarget(cfg, u) for u, _ in slots]
+        st = refine_step(grids, [lvl + len(u) - 1 for u, lvl in slots], lambda gi, xs: cuts[gi](xs), dist=dist,
+                         device=True)
+        payload = {"new": np.array([st.new_nodes]), "gathered": np.array([st.gathered_bytes])}
+        for i, g in enumerate(grids):
+            k, s = g.nodes()
+            payload[f"k{i}"], payload[f"s{i}"] = k, s
+        np.savez(f"{out_path}_{rank}.npz", **payload)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_native_refinement_two_ranks_device_rows(tmp_path):
+    """ddsg_refine_step with two ranks on the one GPU: each hierarchizes its
+    share into device rows, the all-gather callback (gloo) exchanges them,
+    both ranks append identically -- the reference-exact next-level build."""
+    world = 2
+    mp.spawn(_gloo_device_refine_worker, args=(world, _free_port(), str(tmp_path / "g")), nprocs=world, join=True)
+    outs = [dict(np.load(tmp_path / f"g_{r}.npz")) for r in range(world)]
+    cfg = W.CONFIGS[5]
+    assert outs[0]["new"][0] > 0 and outs[0]["gathered"][0] > 0
+    for i, (u, lvl) in enumerate([((3,), 5), ((250,), 4), ((3, 17), 3), ((40, 299), 2)]):
+        h = W.build_cut_grid(cfg, u, lvl + 1, cfg.eps_1d if len(u) == 1 else cfg.eps_2d)
+        k, s = h.nodes()
+        for o in outs:
+            assert np.array_equal(o[f"k{i}"], k) and np.array_equal(bits(o[f"s{i}"]), bits(s))
