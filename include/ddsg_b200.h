@@ -135,6 +135,9 @@ ddsg_status ddsg_grid_info(const ddsg_grid_t* g, int* dim, int* m, int* mode, in
                            double* eps_gamma, int64_t* n_nodes);
 /* Copies nodes in stored order: keys [n][dim], surplus [n][m] (either may be NULL). */
 ddsg_status ddsg_grid_nodes(const ddsg_grid_t* g, uint32_t* heap_keys, double* surplus);
+/* SparseGridFunction::contains / node_at (sparse_grid.hpp:151-157): *index =
+ * the stored position of the node with this key ([dim] heap keys), or -1. */
+ddsg_status ddsg_grid_find(const ddsg_grid_t* g, const uint32_t* heap_key, int64_t* index);
 /* SparseGridFunction::quadrature (sparse_grid.hpp:138-149), host, fixed node order. */
 ddsg_status ddsg_grid_quadrature(const ddsg_grid_t* g, double* out);
 

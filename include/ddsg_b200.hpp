@@ -180,20 +180,24 @@ class SparseGridFunction {
     return SparseGridFunction(g);
   }
 
-  // sparse_grid.hpp:81 (stored order)
-  std::vector<GridNode> nodes() const {
-    const std::size_t n = size();
-    std::vector<uint32_t> keys(n * static_cast<std::size_t>(dim_));
-    std::vector<double> sur(n * static_cast<std::size_t>(out_dim_));
-    detail::check(ddsg_grid_nodes(h_.get(), keys.data(), sur.data()));
-    std::vector<GridNode> out(n);
-    for (std::size_t i = 0; i < n; ++i) {
-      out[i].key.assign(keys.begin() + static_cast<std::ptrdiff_t>(i * dim_),
-                        keys.begin() + static_cast<std::ptrdiff_t>((i + 1) * dim_));
-      out[i].surplus.assign(sur.begin() + static_cast<std::ptrdiff_t>(i * out_dim_),
-                            sur.begin() + static_cast<std::ptrdiff_t>((i + 1) * out_dim_));
+  // sparse_grid.hpp:81 (stored order).  Read once from the C-ABI and kept
+  // (the grid is immutable through the shim), so repeated calls are cheap.
+  const std::vector<GridNode>& nodes() const {
+    if (!nodes_) {
+      const std::size_t n = size();
+      std::vector<uint32_t> keys(n * static_cast<std::size_t>(dim_));
+      std::vector<double> sur(n * static_cast<std::size_t>(out_dim_));
+      detail::check(ddsg_grid_nodes(h_.get(), keys.data(), sur.data()));
+      auto out = std::make_shared<std::vector<GridNode>>(n);
+      for (std::size_t i = 0; i < n; ++i) {
+        (*out)[i].key.assign(keys.begin() + static_cast<std::ptrdiff_t>(i * dim_),
+                             keys.begin() + static_cast<std::ptrdiff_t>((i + 1) * dim_));
+        (*out)[i].surplus.assign(sur.begin() + static_cast<std::ptrdiff_t>(i * out_dim_),
+                                 sur.begin() + static_cast<std::ptrdiff_t>((i + 1) * out_dim_));
+      }
+      nodes_ = std::move(out);
     }
-    return out;
+    return *nodes_;
   }
 
   // sparse_grid.hpp:111-128 (one point; std::domain_error outside [0,1]^dim)
@@ -225,10 +229,18 @@ class SparseGridFunction {
     return q;
   }
 
+  // sparse_grid.hpp:151-157: hash lookup of a node key
   bool contains(const NodeKey& key) const {
-    for (const auto& n : nodes())
-      if (n.key == key) return true;
-    return false;
+    if (key.size() != static_cast<std::size_t>(dim_)) return false;
+    int64_t idx = -1;
+    detail::check(ddsg_grid_find(h_.get(), key.data(), &idx));
+    return idx >= 0;
+  }
+  const GridNode& node_at(const NodeKey& key) const {
+    int64_t idx = -1;
+    if (key.size() == static_cast<std::size_t>(dim_)) detail::check(ddsg_grid_find(h_.get(), key.data(), &idx));
+    if (idx < 0) throw std::out_of_range("sparse grid: node not present");
+    return nodes()[static_cast<std::size_t>(idx)];
   }
 
   const ddsg_grid_t* handle() const { return h_.get(); }
@@ -240,6 +252,7 @@ class SparseGridFunction {
     void operator()(ddsg_grid_t* g) const { ddsg_grid_destroy(g); }
   };
   std::shared_ptr<ddsg_grid_t> h_;
+  mutable std::shared_ptr<const std::vector<GridNode>> nodes_;  // nodes() cache
   int dim_ = 0, out_dim_ = 0, max_level_ = 0;
   double eps_gamma_ = 0.0;
   BoundaryMode mode_ = BoundaryMode::zero_boundary;
@@ -322,6 +335,36 @@ class DdsgFunction {  // hdmr.hpp:195-356
     return it->second;
   }
   const std::map<ComponentIndex, std::vector<double>>& cut_quadratures() const { return cut_quadratures_; }
+
+  // hdmr.hpp:222-231: telescopic combination of cut quadratures (f_u's quadrature)
+  std::vector<double> component_quadrature(const ComponentIndex& u) const {
+    std::vector<double> q(static_cast<std::size_t>(out_dim_), 0.0);
+    const std::size_t k = u.order();
+    std::vector<ComponentIndex> subs;  // all_subsets(u) in (order, lex) order (component_index.hpp:75-87)
+    for (std::size_t mask = 0; mask < (std::size_t{1} << k); ++mask) {
+      ComponentIndex v;
+      for (std::size_t j = 0; j < k; ++j)
+        if (mask & (std::size_t{1} << j)) v.dims.push_back(u.dims[j]);
+      subs.push_back(std::move(v));
+    }
+    std::sort(subs.begin(), subs.end());
+    for (const auto& v : subs) {
+      const auto& qc = cut_quadrature(v);
+      const double sign = ((u.order() - v.order()) % 2 == 0) ? 1.0 : -1.0;
+      for (std::size_t c = 0; c < q.size(); ++c) q[c] += sign * qc[c];
+    }
+    return q;
+  }
+  // hdmr.hpp:235-243
+  std::vector<double> cumulative_quadrature(std::size_t k) const {
+    std::vector<double> q = anchor_.f_anchor;
+    for (const auto& [u, grid] : accepted_) {
+      if (u.order() > k) continue;
+      const auto qu = component_quadrature(u);
+      for (std::size_t c = 0; c < q.size(); ++c) q[c] += qu[c];
+    }
+    return q;
+  }
 
   std::size_t total_grid_points() const {  // hdmr.hpp:245-250
     std::size_t n = 1;

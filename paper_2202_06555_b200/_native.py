@@ -58,6 +58,7 @@ SIGNATURES = {
     "ddsg_grid_info": (_i, [_p, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_d), C.POINTER(_i64)]),
     "ddsg_grid_nodes": (_i, [_p, _p, _p]),
     "ddsg_grid_quadrature": (_i, [_p, _p]),
+    "ddsg_grid_find": (_i, [_p, _p, C.POINTER(_i64)]),
     "ddsg_eval_grid": (_i, [_p, _pd, _i64, _pd, C.POINTER(_i64), _p]),
     "ddsg_hdmr_create": (_i, [_i, _i, _p, _i, _p, _p, _p, _p, C.POINTER(_p)]),
     "ddsg_hdmr_destroy": (_i, [_p]),

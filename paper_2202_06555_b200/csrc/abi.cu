@@ -243,6 +243,13 @@ ddsg_status ddsg_grid_nodes(const ddsg_grid_t* g, uint32_t* heap_keys, double* s
   });
 }
 
+ddsg_status ddsg_grid_find(const ddsg_grid_t* g, const uint32_t* heap_key, int64_t* index) {
+  return guarded([&] {
+    if (!g || !heap_key || !index) fail(DDSG_INVALID_ARGUMENT, "grid_find: null argument");
+    *index = g->g.find(heap_key);
+  });
+}
+
 ddsg_status ddsg_grid_quadrature(const ddsg_grid_t* g, double* out) {
   return guarded([&] {
     if (!g || !out) fail(DDSG_INVALID_ARGUMENT, "grid_quadrature: null argument");

@@ -184,6 +184,20 @@ int main() {
     for (const auto& [u, b] : dd->coeff_b())
       CHECK(same_bits(dd->cut_quadrature(u), src.cut_quadrature(ddsg_b200::ComponentIndex{u.dims})));
     CHECK(src.rejected().size() == dd->rejected().size());
+    for (const auto& [u, g] : dd->accepted())
+      CHECK(same_bits(dd->component_quadrature(u), src.component_quadrature(ddsg_b200::ComponentIndex{u.dims})));
+    CHECK(same_bits(dd->cumulative_quadrature(1), src.cumulative_quadrature(1)));
+    CHECK(same_bits(dd->cumulative_quadrature(2), src.cumulative_quadrature(2)));
+    {  // node lookup (sparse_grid.hpp:151-157)
+      const auto& [u0, g0] = *dd->accepted().rbegin();
+      const auto& gb = src.accepted().at(ddsg_b200::ComponentIndex{u0.dims});
+      const auto& nd = g0.nodes()[g0.size() / 2];
+      CHECK(gb.contains(nd.key) && same_bits(gb.node_at(nd.key).surplus, nd.surplus));
+      ddsg_b200::NodeKey absent(nd.key.size(), (1u << 29) + 7u);
+      CHECK(!gb.contains(absent) && !g0.contains(absent));
+      CHECK(throws<std::out_of_range>([&] { (void)gb.node_at(absent); }));
+      CHECK(&gb.nodes() == &gb.nodes());  // cached: a stable reference, like the reference's
+    }
     CHECK(throws<std::out_of_range>([&] { (void)src.cut_quadrature(ddsg_b200::ComponentIndex{{0, 1, 2}}); }));
     std::vector<double> out(m), bad_x(d, 0.5), short_x(d - 1, 0.5);
     bad_x[3] = 1.5;
