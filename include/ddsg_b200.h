@@ -111,7 +111,9 @@ ddsg_status ddsg_grid_append(ddsg_grid_t* g, int64_t n_new, const uint32_t* heap
 
 /* Residual hierarchization of new nodes against the current grid on the GPU
  * (sparse_grid.hpp:264-276,302-315): surplus_out[i] = f_values[i] -
- * interpolate(g, x(keys[i])).  Does not modify g. */
+ * interpolate(g, x(keys[i])).  f_values / surplus_out: both host or both
+ * device memory (device rows stay on the device, e.g. for an all-gather).
+ * Does not modify g. */
 ddsg_status ddsg_hierarchize(const ddsg_grid_t* g, int64_t n_new, const uint32_t* heap_keys,
                              const double* f_values, double* surplus_out);
 

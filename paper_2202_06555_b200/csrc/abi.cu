@@ -181,9 +181,21 @@ ddsg_status ddsg_hierarchize(const ddsg_grid_t* g, int64_t n_new, const uint32_t
       if (!valid_key(heap_keys[i])) fail(DDSG_INVALID_ARGUMENT, "hierarchize: invalid heap key");
       x[i] = coordinate_of(heap_keys[i]);
     }
-    std::vector<double> interp(static_cast<size_t>(n_new) * G.m);
     auto* self = const_cast<ddsg_grid_t*>(g);
     const auto prog = self->device();
+    const bool f_dev = is_device_pointer(f_values), s_dev = is_device_pointer(surplus_out);
+    if (f_dev != s_dev) fail(DDSG_INVALID_ARGUMENT, "hierarchize: f_values and surplus_out must both be host or device");
+    if (f_dev) {  // device-resident rows (e.g. straight into an all-gather buffer)
+      double* di = nullptr;
+      DDSG_CUDA(cudaMalloc(&di, static_cast<size_t>(n_new) * G.m * 8 + 8));
+      std::unique_ptr<double, decltype(&cudaFree)> hold(di, cudaFree);
+      const int64_t bad = evaluate(*prog, 1, x.data(), n_new, di, nullptr);
+      if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "hierarchize: node outside the unit cube");
+      residual_on_device(f_values, di, n_new * G.m, surplus_out, nullptr);
+      DDSG_CUDA(cudaDeviceSynchronize());
+      return;
+    }
+    std::vector<double> interp(static_cast<size_t>(n_new) * G.m);
     const int64_t bad = evaluate(*prog, 1, x.data(), n_new, interp.data(), nullptr);
     if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "hierarchize: node outside the unit cube");
     for (int64_t i = 0; i < n_new * G.m; ++i) surplus_out[i] = f_values[i] - interp[i];

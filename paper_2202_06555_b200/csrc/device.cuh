@@ -139,6 +139,12 @@ class StagedWorkspace {
 int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, int64_t n, double* y,
                         StagedWorkspace& ws, const double* const* xrows = nullptr, double* const* yrows = nullptr);
 
+// Device memory (cudaMalloc / managed) as opposed to host memory.
+bool is_device_pointer(const void* p);
+// out[i] = f[i] - interp[i] (the reference's residual, sparse_grid.hpp:272)
+// on device buffers, on stream st.
+void residual_on_device(const double* f, const double* interp, int64_t count, double* out, cudaStream_t st);
+
 // Support statistics (nnz and order-sensitive hash per point).
 int64_t support(const DeviceProgram& prog, const double* x, int64_t n, int64_t* nnz,
                 uint64_t* hash, cudaStream_t stream);

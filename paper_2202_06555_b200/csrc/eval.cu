@@ -563,6 +563,12 @@ bool is_device_ptr(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+__global__ void residual_kernel(const double* __restrict__ f, const double* __restrict__ interp, int64_t count,
+                                double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = __dsub_rn(f[i], interp[i]);  // sparse_grid.hpp:272 (f - interpolate)
+}
+
 // Ordinary (pageable) host memory: not device memory and not page-locked.
 bool is_pageable(const void* p) {
   if (!p) return false;
@@ -958,6 +964,14 @@ int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, i
   DDSG_CUDA(cudaStreamSynchronize(ws.st[0]));
   stats.main_ms = kernel_timer().collect();
   return *hbad == ULLONG_MAX ? -1 : static_cast<int64_t>(*hbad);
+}
+
+bool is_device_pointer(const void* p) { return is_device_ptr(p); }
+
+void residual_on_device(const double* f, const double* interp, int64_t count, double* out, cudaStream_t st) {
+  if (count <= 0) return;
+  residual_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(f, interp, count, out);
+  DDSG_CUDA(cudaGetLastError());
 }
 
 int64_t support(const DeviceProgram& prog, const double* x, int64_t n, int64_t* nnz, uint64_t* hash,

@@ -35,12 +35,6 @@ using namespace ddsg_b200::abi;
 
 namespace {
 
-__global__ void residual_kernel(const double* __restrict__ f, const double* __restrict__ interp, int64_t count,
-                                double* __restrict__ out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < count) out[i] = __dsub_rn(f[i], interp[i]);  // sparse_grid.hpp:272 (f - interpolate)
-}
-
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -202,9 +196,7 @@ ddsg_status ddsg_refine_step(ddsg_grid_t* const* grids, int n_grids, const int* 
             if (bad >= 0) fail(DDSG_DOMAIN_ERROR, "refine_step: node outside the unit cube");
             double* df = d_f.get(cnt * row_bytes);
             DDSG_CUDA(cudaMemcpy(df, fv.data(), cnt * row_bytes, cudaMemcpyHostToDevice));
-            const int64_t e = cnt * m;
-            residual_kernel<<<static_cast<unsigned>((e + 255) / 256), 256>>>(df, di, e, dl + (a - lo) * m);
-            DDSG_CUDA(cudaGetLastError());
+            residual_on_device(df, di, cnt * m, dl + (a - lo) * m, nullptr);
             DDSG_CUDA(cudaDeviceSynchronize());
           } else {
             // host hierarchization, bit-identical to insert_batch (sparse_grid.hpp:264-276)

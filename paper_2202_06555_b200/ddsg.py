@@ -261,6 +261,17 @@ class SparseGridFunction:
         """surplus = f - interpolate(grid, x(key)) for new nodes (sparse_grid.hpp:264-276);
         device=True evaluates on the GPU, False on the host (both bit-identical)."""
         keys = np.ascontiguousarray(keys, dtype=np.uint32).reshape(-1, self.dim)
+        if hasattr(f_values, "data_ptr") and getattr(f_values, "is_cuda", False):
+            # device rows in, device rows out (ddsg_hierarchize with device buffers)
+            import torch
+
+            fv = f_values.reshape(-1, self.out_dim).contiguous().to(torch.float64)
+            if fv.shape[0] != keys.shape[0]:
+                raise InvalidArgument("hierarchize: f_values rows != keys rows")
+            out = torch.empty_like(fv)
+            with _DeviceScope(fv, None):
+                _check(N.lib.ddsg_hierarchize(self._h, keys.shape[0], _ptr(keys), _ptr(fv), _ptr(out)))
+            return out
         f_values = np.ascontiguousarray(f_values, dtype=np.float64).reshape(-1, self.out_dim)
         if f_values.shape[0] != keys.shape[0]:
             raise InvalidArgument("hierarchize: f_values rows != keys rows")

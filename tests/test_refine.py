@@ -135,3 +135,22 @@ def test_refine_step_plain_grid_d20_host():
 @pytest.mark.gpu
 def test_refine_step_plain_grid_d20_gpu_hierarchize():
     _config3_step(4, device=True)
+
+
+@pytest.mark.gpu
+def test_hierarchize_device_rows_equal_host_rows():
+    """ddsg_hierarchize with device f_values / surplus_out: the same bits as
+    the host form (and as the reference's insert_batch on the host path)."""
+    import torch
+
+    grids = _grids(0)
+    cuts, f = _f_eval()
+    for gi, (g, s) in enumerate(zip(grids, _level_sums())):
+        keys = g.refine_candidates(s)
+        if len(keys) == 0:
+            continue
+        fv = f(gi, coords_of(keys))
+        host = g.hierarchize(keys, fv, device=True)
+        dev = g.hierarchize(keys, torch.from_numpy(fv).cuda()).cpu().numpy()
+        ref = g.hierarchize(keys, fv, device=False)
+        assert np.array_equal(bits(dev), bits(host)) and np.array_equal(bits(dev), bits(ref))
