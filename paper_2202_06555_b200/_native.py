@@ -6,10 +6,13 @@ There is no fallback: if libddsg_b200.so is missing the import fails loudly
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libddsg_b200.so"
+# DDSG_B200_LIB selects another in-tree build of the same library (A/B
+# measurements of build-time variants, e.g. libddsg_b200_c16.so)
+LIB_PATH = _PKG / os.environ.get("DDSG_B200_LIB", "libddsg_b200.so")
 WL_PATH = _PKG / "libddsg_workloads.so"
 
 if not LIB_PATH.exists():

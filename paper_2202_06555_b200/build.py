@@ -15,8 +15,14 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = ROOT / "build" / "ddsg_b200"
-LIB = PKG / "libddsg_b200.so"
+# Experiment builds (A/B measurements of compile-time variants): DDSG_BUILD_TAG=t
+# with DDSG_BUILD_DEFS="-DDDSG_SLOT_COLS=16 ..." compiles libddsg_b200_t.so,
+# loaded with DDSG_B200_LIB=libddsg_b200_t.so (see _native.py).
+BUILD_TAG = os.environ.get("DDSG_BUILD_TAG", "")
+BUILD_DEFS = os.environ.get("DDSG_BUILD_DEFS", "").split()
+_SUFFIX = f"_{BUILD_TAG}" if BUILD_TAG else ""
+BUILD = ROOT / "build" / f"ddsg_b200{_SUFFIX}"
+LIB = PKG / f"libddsg_b200{_SUFFIX}.so"
 WL_SRC = PKG / "csrc_workloads" / "workloads.c"
 WL_LIB = PKG / "libddsg_workloads.so"
 
@@ -32,7 +38,7 @@ COMMON = [
     "-Xptxas",
     "-v",
     f"-I{ROOT / 'include'}",
-]
+] + BUILD_DEFS
 
 
 def _sources() -> list[Path]:
@@ -83,7 +89,7 @@ def build_library(verbose: bool = False) -> Path:
     # C++ drop-in test driver (tests/cpp): include/ddsg_b200.hpp over the C-ABI
     drv_src = ROOT / "tests" / "cpp" / "test_dropin.cpp"
     drv = ROOT / "build" / "test_dropin"
-    if drv_src.exists() and _stale(drv, [drv_src, LIB, ROOT / "include" / "ddsg_b200.hpp"]):
+    if not BUILD_TAG and drv_src.exists() and _stale(drv, [drv_src, LIB, ROOT / "include" / "ddsg_b200.hpp"]):
         cmd = ["g++", "-std=c++20", "-O2", "-Wall", f"-I{ROOT / 'include'}", str(drv_src), f"-L{PKG}", "-lddsg_b200",
                "-Wl,-rpath,$ORIGIN/../paper_2202_06555_b200", "-o", str(drv)]
         res = subprocess.run(cmd, capture_output=True, text=True)

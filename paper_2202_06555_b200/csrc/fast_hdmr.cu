@@ -351,7 +351,7 @@ bool FastHdmr::build(const HostProgram& hp) {
               v = hp.surplus[P.rows[r] * m_ + col];  // (the zero row stays 0)
           }
           table[r * P.stride + c] = v;
-          if (P.stride == kRotStride) table[r * P.stride + kCols + c] = v;  // second copy
+          if (P.stride == kRotStride && kRotCopies == 2) table[r * P.stride + kCols + c] = v;  // second copy
         }
       if (!P.slab.empty())
         std::memcpy(blk + P.h.slab_off, P.slab.data(), P.slab.size() * 2);

@@ -38,11 +38,19 @@ namespace ddsg_b200 {
 
 namespace fast {
 
-constexpr int kCols = 8;                 // output columns per thread / CTA column block
+#ifndef DDSG_SLOT_COLS
+#define DDSG_SLOT_COLS 8                 // 8: 16 warps x 8 columns per CTA; 16: 8 warps x 16 columns
+#endif
+constexpr int kCols = DDSG_SLOT_COLS;    // output columns per thread / CTA column block
+static_assert(kCols == 8 || kCols == 16, "slot kernel column block");
 constexpr int kStride = kCols + 1;       // doubles per staged row: odd, so 16 consecutive rows
                                          // fall on 16 distinct 8-byte bank pairs (LDS.64 conflict-free)
-constexpr int kWarps = 16;
+constexpr int kWarps = kCols == 8 ? 16 : 8;  // 128 or 255 registers per thread
 constexpr int kPoints = kWarps * 32;     // points per CTA
+#ifndef DDSG_SLOT_AHEAD
+#define DDSG_SLOT_AHEAD 1                // terms whose rows are in flight ahead of the accumulating term
+#endif
+constexpr int kAhead = DDSG_SLOT_AHEAD;  // (2 needs the 16-column build's registers)
 constexpr int kL1 = 10;                  // max level of order-1 slots
 constexpr int kL2 = 6;                   // max level (per dim) of order-2 slots
 constexpr int kSub2 = kL2 * (kL2 + 1) / 2;  // canonical subspaces of a full order-2 grid
@@ -56,7 +64,10 @@ constexpr int kMaxLevels = kTmemLevels + kSmemLevels;  // 2^12 active slots
 constexpr int kMaxStages = 4;            // shared-memory ring depth (fewer when slot blocks are large)
 constexpr int kHeaderBytes = 128;      // mbarriers + TMEM address slot
 constexpr int kTableOff = 256;         // byte offset of the row table in a staged block (128-B aligned rows)
-constexpr int kRotStride = 2 * kCols;  // doubles per row of the rotated layout (two copies of the 8 columns)
+constexpr int kRotStride = 16;         // doubles per 128-byte row of the rotated layout
+constexpr int kRotCopies = kRotStride / kCols;  // two copies of 8 columns, or the 16 columns once
+constexpr int kTmemCols = 512 / (kWarps / 4);   // TMEM columns per warp (the warps of a lane quarter split 512)
+static_assert(kTmemCols >= 2 * kCols * 8, "8 tree levels per warp in tensor memory");
 constexpr int kMaxPaddedBytes = 96 * 1024;  // largest row table an adaptive block is padded to
 constexpr int kMaxRotBytes = 48 * 1024;     // largest rotated table (1-d levels <= 8: 32 KB; 2-d level 6: 41 KB)
 constexpr int kBCont = 4;   // b_kind flag: continue the previous block's accumulation (later run)

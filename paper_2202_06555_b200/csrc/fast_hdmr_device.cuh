@@ -45,7 +45,43 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+#ifndef DDSG_SLOT_L2HINT
+#define DDSG_SLOT_L2HINT 0  // bit 0: point coordinates evict_last; bit 1: outputs evict_first; bit 2: tables evict_last
+#endif
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldg_x(const double* p) {
+  if (DDSG_SLOT_L2HINT & 1) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_policy_evict_last()));
+    return v;
+  }
+  return __ldg(p);
+}
+__device__ __forceinline__ void stg_y(double* p, double v) {
+  if (DDSG_SLOT_L2HINT & 2)
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(l2_policy_evict_first()) : "memory");
+  else
+    *p = v;
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  if (DDSG_SLOT_L2HINT & 4) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_policy_evict_last())
+        : "memory");
+    return;
+  }
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
@@ -77,7 +113,8 @@ __device__ __forceinline__ void tmem_fence_before() {
 __device__ __forceinline__ void tmem_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_store8(uint32_t taddr, const double (&v)[kCols]) {
+// 8 doubles of a thread <-> 16 consecutive 32-bit TMEM columns of its lane
+__device__ __forceinline__ void tmem_store16(uint32_t taddr, const double* v) {
   uint32_t r[16];
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -90,19 +127,29 @@ __device__ __forceinline__ void tmem_store8(uint32_t taddr, const double (&v)[kC
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_load8(uint32_t taddr, double (&v)[kCols]) {
-  uint32_t r[16];
+__device__ __forceinline__ void tmem_load16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr)
       : "memory");
+}
+// A thread's kCols doubles of one tree level: 2 * kCols TMEM columns.
+__device__ __forceinline__ void tmem_store8(uint32_t taddr, const double (&v)[kCols]) {
+#pragma unroll
+  for (int h = 0; h < kCols / 8; ++h) tmem_store16(taddr + 16u * h, v + 8 * h);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_load8(uint32_t taddr, double (&v)[kCols]) {
+  uint32_t r[kCols / 8][16];
+#pragma unroll
+  for (int h = 0; h < kCols / 8; ++h) tmem_load16(taddr + 16u * h, r[h]);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int c = 0; c < 8; ++c) v[c] = __hiloint2double(static_cast<int>(r[2 * c + 1]), static_cast<int>(r[2 * c]));
+  for (int c = 0; c < kCols; ++c)
+    v[c] = __hiloint2double(static_cast<int>(r[c / 8][2 * (c % 8) + 1]), static_cast<int>(r[c / 8][2 * (c % 8)]));
 }
 
 template <int kExact>
@@ -341,12 +388,13 @@ __device__ __forceinline__ void leaf_full1(const unsigned char* table, double x,
     }
     row[l - 1] = base1(l) + static_cast<int>(kk);
   }
-  double buf[2][kCols];  // static ping-pong: term i+1 loads while term i accumulates
-  load_row(table, row[0], buf[0]);
+  double buf[kAhead + 1][kCols];  // static ring: terms i+1..i+kAhead load while term i accumulates
+#pragma unroll
+  for (int i = 0; i < kAhead && i < L; ++i) load_row(table, row[i], buf[i]);
 #pragma unroll
   for (int i = 0; i < L; ++i) {
-    if (i + 1 < L) load_row(table, row[i + 1], buf[(i + 1) & 1]);
-    fma_row<kExact>(acc, w[i], buf[i & 1]);
+    if (i + kAhead < L) load_row(table, row[i + kAhead], buf[(i + kAhead) % (kAhead + 1)]);
+    fma_row<kExact>(acc, w[i], buf[i % (kAhead + 1)]);
   }
 }
 
@@ -360,10 +408,16 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   return v;
 }
 
+// One rotated row (address | lane bits): slot pair j <- column pair (lane rotation) ^ j.
+__device__ __forceinline__ void load_row_rot(uint32_t addr, double (&s)[kCols]) {
+#pragma unroll
+  for (int j = 0; j < kCols / 2; ++j) lds_f64x2(addr ^ static_cast<uint32_t>(j << 4), s[2 * j], s[2 * j + 1]);
+}
+
 // Rotated layout: un-rotate an accumulator (see leaf_full1_rot).
 __device__ __forceinline__ void unrotate(uint32_t q0, double (&acc)[kCols]) {
   // slot pair j holds column pair p0 ^ j (p0 = this lane's rotation, bits 4-5 of q0)
-  const uint32_t p0 = (q0 >> 4) & 3u;
+  const uint32_t p0 = (q0 >> 4) & static_cast<uint32_t>(kCols / 2 - 1);
 #pragma unroll
   for (int b = 1; b < kCols / 2; b <<= 1) {
     const bool flip = (p0 & static_cast<uint32_t>(b)) != 0u;
@@ -409,18 +463,13 @@ __device__ __forceinline__ void leaf_full1_rot(uint32_t q0, double x, double (&a
     }
     row[l - 1] = q0 + ((static_cast<uint32_t>(base1(l)) + kk) << 7);
   }
-  double buf[2][kCols];  // static ping-pong: term i+1 loads while term i accumulates
+  double buf[kAhead + 1][kCols];  // static ring: terms i+1..i+kAhead load while term i accumulates
 #pragma unroll
-  for (int j = 0; j < kCols / 2; ++j)
-    lds_f64x2(row[0] ^ static_cast<uint32_t>(j << 4), buf[0][2 * j], buf[0][2 * j + 1]);
+  for (int i = 0; i < kAhead && i < L; ++i) load_row_rot(row[i], buf[i]);
 #pragma unroll
   for (int i = 0; i < L; ++i) {
-    if (i + 1 < L) {
-#pragma unroll
-      for (int j = 0; j < kCols / 2; ++j)
-        lds_f64x2(row[i + 1] ^ static_cast<uint32_t>(j << 4), buf[(i + 1) & 1][2 * j], buf[(i + 1) & 1][2 * j + 1]);
-    }
-    fma_row<kExact>(acc, w[i], buf[i & 1]);
+    if (i + kAhead < L) load_row_rot(row[i + kAhead], buf[(i + kAhead) % (kAhead + 1)]);
+    fma_row<kExact>(acc, w[i], buf[i % (kAhead + 1)]);
   }
   unrotate(q0, acc);
 }
@@ -466,18 +515,22 @@ __device__ __forceinline__ void leaf_full2(const unsigned char* table, double x0
         ++idx;
       }
   };
-  double wb[2];
-  int rb[2];
-  term(0, wb[0], rb[0]);
-  double buf[2][kCols];  // static ping-pong
-  load_row(table, rb[0], buf[0]);
+  constexpr int kR = kAhead + 1;
+  double wb[kR];
+  int rb[kR];
+  double buf[kR][kCols];  // static ring
+#pragma unroll
+  for (int i = 0; i < kAhead && i < kN; ++i) {
+    term(i, wb[i], rb[i]);
+    load_row(table, rb[i], buf[i]);
+  }
 #pragma unroll
   for (int i = 0; i < kN; ++i) {
-    if (i + 1 < kN) {
-      term(i + 1, wb[(i + 1) & 1], rb[(i + 1) & 1]);
-      load_row(table, rb[(i + 1) & 1], buf[(i + 1) & 1]);
+    if (i + kAhead < kN) {
+      term(i + kAhead, wb[(i + kAhead) % kR], rb[(i + kAhead) % kR]);
+      load_row(table, rb[(i + kAhead) % kR], buf[(i + kAhead) % kR]);
     }
-    fma_row<kExact>(acc, wb[i & 1], buf[i & 1]);
+    fma_row<kExact>(acc, wb[i % kR], buf[i % kR]);
   }
 }
 
@@ -598,23 +651,22 @@ __device__ __forceinline__ void leaf_full2_rot(uint32_t q0, double x0, double x1
         ++idx;
       }
   };
-  double wb[2];
-  uint32_t ab[2];
-  term(0, wb[0], ab[0]);
-  double buf[2][kCols];  // static ping-pong
+  constexpr int kR = kAhead + 1;
+  double wb[kR];
+  uint32_t ab[kR];
+  double buf[kR][kCols];  // static ring
 #pragma unroll
-  for (int j = 0; j < kCols / 2; ++j)
-    lds_f64x2(ab[0] ^ static_cast<uint32_t>(j << 4), buf[0][2 * j], buf[0][2 * j + 1]);
+  for (int i = 0; i < kAhead && i < kN; ++i) {
+    term(i, wb[i], ab[i]);
+    load_row_rot(ab[i], buf[i]);
+  }
 #pragma unroll
   for (int i = 0; i < kN; ++i) {
-    if (i + 1 < kN) {
-      term(i + 1, wb[(i + 1) & 1], ab[(i + 1) & 1]);
-#pragma unroll
-      for (int j = 0; j < kCols / 2; ++j)
-        lds_f64x2(ab[(i + 1) & 1] ^ static_cast<uint32_t>(j << 4), buf[(i + 1) & 1][2 * j],
-                  buf[(i + 1) & 1][2 * j + 1]);
+    if (i + kAhead < kN) {
+      term(i + kAhead, wb[(i + kAhead) % kR], ab[(i + kAhead) % kR]);
+      load_row_rot(ab[(i + kAhead) % kR], buf[(i + kAhead) % kR]);
     }
-    fma_row<kExact>(acc, wb[i & 1], buf[i & 1]);
+    fma_row<kExact>(acc, wb[i % kR], buf[i % kR]);
   }
   unrotate(q0, acc);
 }
@@ -736,7 +788,7 @@ struct TreeStore {
   int tid;
   __device__ __forceinline__ void load(int i, double (&v)[kCols]) const {
     if (i < kTmemLevels) {
-      tmem_load8(tbase + 16u * static_cast<uint32_t>(i), v);
+      tmem_load8(tbase + static_cast<uint32_t>(2 * kCols * i), v);
     } else {
       const double2* L = smem + (static_cast<int64_t>(i - kTmemLevels) * (kCols / 2)) * kPoints + tid;
 #pragma unroll
@@ -749,7 +801,7 @@ struct TreeStore {
   }
   __device__ __forceinline__ void store(int i, const double (&v)[kCols]) const {
     if (i < kTmemLevels) {
-      tmem_store8(tbase + 16u * static_cast<uint32_t>(i), v);
+      tmem_store8(tbase + static_cast<uint32_t>(2 * kCols * i), v);
     } else {
       double2* L = smem + (static_cast<int64_t>(i - kTmemLevels) * (kCols / 2)) * kPoints + tid;
 #pragma unroll
@@ -793,7 +845,9 @@ __global__ void __launch_bounds__(kPoints, 1)
   // rotated-layout lane bits: copy (bit 6) = (lane >> 2) & 1, column-pair
   // rotation (bits 4-5) = lane & 3 -- the 8 lanes of a quarter-warp hit the 8
   // distinct 16-byte units of a 128-byte row in every LDS.128
-  const uint32_t lanebits = static_cast<uint32_t>((((tid >> 2) & 1) << 6) | ((tid & 3) << 4));
+  // (16 columns: one copy, rotation (bits 4-6) = lane & 7)
+  const uint32_t lanebits = kRotCopies == 2 ? static_cast<uint32_t>((((tid >> 2) & 1) << 6) | ((tid & 3) << 4))
+                                            : static_cast<uint32_t>((tid & 7) << 4);
   const int64_t p = static_cast<int64_t>(tile) * kPoints + tid;
   const bool valid = p < n;
   const int64_t pc = valid ? p : n - 1;
@@ -818,11 +872,11 @@ __global__ void __launch_bounds__(kPoints, 1)
   tmem_fence_after();
   TreeStore store{deep, 0u, tid};
   if (use_tmem)
-    store.tbase = *tmem_slot + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(128 * (warp >> 2));
+    store.tbase = *tmem_slot + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(kTmemCols * (warp >> 2));
 
   // coordinates of the slot's dims (dims table [block][3]: an absent second
   // dim reads dim 0, unused; the third is -1 unless the block is order 3)
-  auto coord = [&](int a, int j) { return xt[static_cast<int64_t>(sdims[kSlotDims * a + j]) * n + pc]; };
+  auto coord = [&](int a, int j) { return ldg_x(xt + static_cast<int64_t>(sdims[kSlotDims * a + j]) * n + pc); };
   double xc0 = coord(0, 0), xc1 = coord(0, 1), xc2 = 0.5;
   if (kOrder3 && sdims[2] >= 0) xc2 = coord(0, 2);
   const int c0 = cb * kCols;
@@ -903,7 +957,7 @@ __global__ void __launch_bounds__(kPoints, 1)
         double* yp = y + p * m + c0;
 #pragma unroll
         for (int c = 0; c < kCols; ++c)
-          if (c0 + c < m) yp[c] = acc[c];
+          if (c0 + c < m) stg_y(yp + c, acc[c]);
       }
     }
     __syncwarp();  // every lane of this warp is done reading stage st
