@@ -59,18 +59,12 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   return p;
 }
 __device__ __forceinline__ double ldg_x(const double* p) {
-  if (DDSG_SLOT_L2HINT & 1) {
-    double v;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_policy_evict_last()));
-    return v;
-  }
-  return __ldg(p);
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_policy_evict_last()));
+  return v;
 }
 __device__ __forceinline__ void stg_y(double* p, double v) {
-  if (DDSG_SLOT_L2HINT & 2)
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(l2_policy_evict_first()) : "memory");
-  else
-    *p = v;
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(l2_policy_evict_first()) : "memory");
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -876,7 +870,10 @@ __global__ void __launch_bounds__(kPoints, 1)
 
   // coordinates of the slot's dims (dims table [block][3]: an absent second
   // dim reads dim 0, unused; the third is -1 unless the block is order 3)
-  auto coord = [&](int a, int j) { return ldg_x(xt + static_cast<int64_t>(sdims[kSlotDims * a + j]) * n + pc); };
+  auto coord = [&](int a, int j) {
+    if (DDSG_SLOT_L2HINT & 1) return ldg_x(xt + static_cast<int64_t>(sdims[kSlotDims * a + j]) * n + pc);
+    return xt[static_cast<int64_t>(sdims[kSlotDims * a + j]) * n + pc];
+  };
   double xc0 = coord(0, 0), xc1 = coord(0, 1), xc2 = 0.5;
   if (kOrder3 && sdims[2] >= 0) xc2 = coord(0, 2);
   const int c0 = cb * kCols;
@@ -957,7 +954,12 @@ __global__ void __launch_bounds__(kPoints, 1)
         double* yp = y + p * m + c0;
 #pragma unroll
         for (int c = 0; c < kCols; ++c)
-          if (c0 + c < m) stg_y(yp + c, acc[c]);
+          if (c0 + c < m) {
+            if (DDSG_SLOT_L2HINT & 2)
+              stg_y(yp + c, acc[c]);
+            else
+              yp[c] = acc[c];
+          }
       }
     }
     __syncwarp();  // every lane of this warp is done reading stage st
