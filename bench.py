@@ -358,7 +358,10 @@ def run_ours(args, rank, world, local_rank, dist):
         "resource": "shared-memory gather: 16 surplus doubles/clk/SM (LDS pipe, 128 B/clk/SM)",
         "achieved": achieved, "peak": smem_peak, "unit": "TFLOP/s (2 FLOP per gathered double)",
         "frac": achieved / smem_peak,
-        "peak_source": "profiles/r1_lds_gather.json microbenchmark x %d SMs x %.0f MHz (median SM clock in the timed region)" % (sms, mhz)}
+        "peak_source": "shared-memory crossbar 128 B/clk/SM (B300_MICROARCH.md 'LDS/STS' table; reproduced by "
+                       "profiles/r1_lds_gather.json: 0.496 lane-varying LDS.64 warp instructions/clk/SM) x %d SMs x "
+                       "%.0f MHz (median SM clock in the timed region); every multiply-add of the hot path reads "
+                       "its own 8-byte surplus from shared memory" % (sms, mhz)}
 
     # e2e through the same API with pinned host buffers
     e2e = None
