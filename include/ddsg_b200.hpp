@@ -7,7 +7,7 @@
 // runs on the GPU; every batched call is one C-ABI call.
 //
 //   SparseGridFunction   sparse_grid.hpp:72-351
-//   DdsgFunction         hdmr.hpp:195-356   (from_parts only; decompose is out of scope)
+//   DdsgFunction         hdmr.hpp:195-356   (from_parts, evaluate_naive; decompose / select_anchor: hdmr.hpp:45-133,364-483)
 //   EvalWorkspace        ddsg_eval.hpp:21-24
 //   VectorizedDdsg       ddsg_eval.hpp:28-165
 //   JSON documents       serialize.hpp:17-160 (JsonDocument stands in for nlohmann::json)
@@ -22,7 +22,11 @@
 #include <fstream>
 #include <sstream>
 #include <functional>
+#include <atomic>
+#include <limits>
 #include <map>
+#include <mutex>
+#include <random>
 #include <memory>
 #include <new>
 #include <set>
@@ -315,8 +319,128 @@ struct DdsgOptions {  // hdmr.hpp:166-175 (only the fields evaluation uses matte
   unsigned workers = 1;
 };
 
+using Evaluator = std::function<void(std::span<const double>, std::span<double>)>;  // hdmr.hpp:40
+
+// component_index.hpp:57-72: the order-k index sets of {0..d-1}, lexicographic.
+inline std::vector<ComponentIndex> order_k_indices(int d, std::size_t k) {
+  std::vector<ComponentIndex> all;
+  if (k > static_cast<std::size_t>(d)) return all;
+  std::vector<int> c(k);
+  for (std::size_t i = 0; i < k; ++i) c[i] = static_cast<int>(i);
+  for (;;) {
+    all.push_back(ComponentIndex{c});
+    std::size_t i = k;  // rightmost position that can still advance
+    while (i > 0 && c[i - 1] == d - static_cast<int>(k - i) - 1) --i;
+    if (i == 0) return all;
+    ++c[i - 1];
+    for (std::size_t j = i; j < k; ++j) c[j] = c[j - 1] + 1;
+  }
+}
+
+// component_index.hpp:75-87: every subset of u, in (order, lex) order.
+inline std::vector<ComponentIndex> all_subsets(const ComponentIndex& u) {
+  const std::size_t k = u.order();
+  std::vector<ComponentIndex> subs;
+  subs.reserve(std::size_t{1} << k);
+  for (std::size_t mask = 0; mask < (std::size_t{1} << k); ++mask) {
+    ComponentIndex v;
+    for (std::size_t j = 0; j < k; ++j)
+      if (mask & (std::size_t{1} << j)) v.dims.push_back(u.dims[j]);
+    subs.push_back(std::move(v));
+  }
+  std::sort(subs.begin(), subs.end());
+  return subs;
+}
+
+struct ExpansionDiagnostics {  // hdmr.hpp:178-186
+  struct EtaRecord {
+    ComponentIndex index;
+    double eta = 0.0;
+    bool accepted = true;
+  };
+  std::vector<double> rho_by_order;                  // rho after orders 1..K (NaN: zero denominator)
+  std::vector<std::vector<EtaRecord>> eta_by_order;  // order-k records at [k-1] (order 1: none)
+};
+
+class rho_denominator_error : public std::runtime_error {  // hdmr.hpp:100-106
+ public:
+  rho_denominator_error()
+      : std::runtime_error("expansion_rho: order-(k-1) cumulative quadrature is zero; "
+                           "treat rho as above-threshold and continue expanding") {}
+};
+
+// hdmr.hpp:108-119: ||Q_k - Q_{k-1}||_2 / ||Q_{k-1}||_2 over the outputs (sums in output order).
+inline double expansion_rho(const std::vector<double>& cumulative_k, const std::vector<double>& cumulative_km1) {
+  double diff2 = 0.0, base2 = 0.0;
+  for (std::size_t c = 0; c < cumulative_k.size(); ++c) {
+    const double delta = cumulative_k[c] - cumulative_km1[c];
+    diff2 += delta * delta;
+    base2 += cumulative_km1[c] * cumulative_km1[c];
+  }
+  if (base2 == 0.0) throw rho_denominator_error();
+  return std::sqrt(diff2) / std::sqrt(base2);
+}
+
+// hdmr.hpp:124-133: quadrature mass of one component against the lower orders (+inf: accept).
+inline double eta_coefficient(const std::vector<double>& component_quadrature,
+                              const std::vector<double>& lower_order_sum) {
+  double mass2 = 0.0, base2 = 0.0;
+  for (std::size_t c = 0; c < component_quadrature.size(); ++c) {
+    mass2 += component_quadrature[c] * component_quadrature[c];
+    base2 += lower_order_sum[c] * lower_order_sum[c];
+  }
+  if (base2 == 0.0) return std::numeric_limits<double>::infinity();
+  return std::sqrt(mass2) / std::sqrt(base2);
+}
+
+// hdmr.hpp:45-77: the sample closest (l1 over the outputs) to the sample mean
+// of n_samples uniform draws (std::mt19937_64(seed)); lowest index on ties.
+inline AnchorPoint select_anchor(const Evaluator& f, int dim, int out_dim, int n_samples, std::uint64_t seed) {
+  if (n_samples < 1) throw std::invalid_argument("select_anchor: n_samples must be >= 1");
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  const std::size_t m = static_cast<std::size_t>(out_dim), n = static_cast<std::size_t>(n_samples);
+  std::vector<std::vector<double>> pts(n, std::vector<double>(static_cast<std::size_t>(dim)));
+  std::vector<std::vector<double>> vals(n, std::vector<double>(m));
+  std::vector<double> mean(m, 0.0);
+  for (std::size_t i = 0; i < n; ++i) {
+    for (double& c : pts[i]) c = unif(rng);
+    f(pts[i], vals[i]);
+    for (std::size_t c = 0; c < m; ++c) {
+      if (!std::isfinite(vals[i][c]))
+        throw build_error("select_anchor: evaluator returned a non-finite value", pts[i]);
+      mean[c] += vals[i][c];
+    }
+  }
+  for (double& c : mean) c /= static_cast<double>(n_samples);
+  std::size_t best = 0;
+  double best_dist = std::numeric_limits<double>::infinity();
+  for (std::size_t i = 0; i < n; ++i) {
+    double dist = 0.0;
+    for (std::size_t c = 0; c < m; ++c) dist += std::abs(vals[i][c] - mean[c]);
+    if (dist < best_dist) {
+      best_dist = dist;
+      best = i;
+    }
+  }
+  return AnchorPoint{std::move(pts[best]), std::move(vals[best])};
+}
+
+// hdmr.hpp:81-93: f restricted to the cut through the anchor along the dims of u.
+inline Evaluator cut_evaluator(const Evaluator& f, const AnchorPoint& anchor, const ComponentIndex& u) {
+  if (u.empty()) throw std::invalid_argument("cut_evaluator: component index must be non-empty");
+  return [f, base = anchor.coords, dims = u.dims](std::span<const double> y, std::span<double> out) {
+    std::vector<double> x = base;  // per call: safe under concurrent grid builds
+    for (std::size_t j = 0; j < dims.size(); ++j) x[static_cast<std::size_t>(dims[j])] = y[j];
+    f(x, out);
+  };
+}
+
 class DdsgFunction {  // hdmr.hpp:195-356
  public:
+  friend DdsgFunction decompose(const Evaluator&, int, int, const AnchorPoint&, const DdsgOptions&,
+                                ExpansionDiagnostics*);
+
   int dim() const { return dim_; }
   int out_dim() const { return out_dim_; }
   int k_max() const { return opt_.k_max; }
@@ -374,6 +498,38 @@ class DdsgFunction {  // hdmr.hpp:195-356
   }
   std::size_t order_reached() const { return order_reached_; }
 
+  // hdmr.hpp:257-270: the telescopic double sum without deduplication, one
+  // cut interpolation per (u, v subset of u) -- the vectorized form's oracle.
+  void evaluate_naive(std::span<const double> x, std::span<double> out, std::uint64_t* interp_calls = nullptr) const {
+    check_point(x);
+    const std::size_t m = static_cast<std::size_t>(out_dim_);
+    for (std::size_t c = 0; c < m; ++c) out[c] = anchor_.f_anchor[c];
+    std::vector<double> term(m), y;
+    for (const auto& [u, grid] : accepted_)
+      for (const auto& v : all_subsets(u)) {
+        const double sign = ((u.order() - v.order()) % 2 == 0) ? 1.0 : -1.0;
+        evaluate_cut(v, x, y, term, interp_calls);
+        for (std::size_t c = 0; c < m; ++c) out[c] += sign * term[c];
+      }
+  }
+  std::vector<double> evaluate_naive(std::span<const double> x) const {  // hdmr.hpp:272-276
+    std::vector<double> out(static_cast<std::size_t>(out_dim_));
+    evaluate_naive(x, out);
+    return out;
+  }
+  // hdmr.hpp:280-297: the cut interpolant of an accepted index at x restricted to its dims.
+  void evaluate_cut(const ComponentIndex& v, std::span<const double> x, std::vector<double>& restricted_scratch,
+                    std::span<double> out, std::uint64_t* interp_calls = nullptr) const {
+    if (v.empty()) {
+      for (std::size_t c = 0; c < static_cast<std::size_t>(out_dim_); ++c) out[c] = anchor_.f_anchor[c];
+      return;
+    }
+    restricted_scratch.resize(v.order());
+    for (std::size_t j = 0; j < v.order(); ++j) restricted_scratch[j] = x[static_cast<std::size_t>(v.dims[j])];
+    if (interp_calls) ++*interp_calls;
+    accepted_.at(v).interpolate(restricted_scratch, out);
+  }
+
   void check_point(std::span<const double> x) const {  // hdmr.hpp:299-304
     if (x.size() != static_cast<std::size_t>(dim_)) throw std::invalid_argument("ddsg: query dimension mismatch");
     for (double v : x)
@@ -408,7 +564,132 @@ class DdsgFunction {  // hdmr.hpp:195-356
   std::map<ComponentIndex, int> coeff_b_;
   std::map<ComponentIndex, std::vector<double>> cut_quadratures_;
   std::size_t order_reached_ = 0;
+
+  // hdmr.hpp:339-355: b_i = sum over accepted u containing i of (-1)^(|u| - |i|).
+  void finalize_coefficients() {
+    coeff_b_.clear();
+    std::vector<const ComponentIndex*> family;
+    const ComponentIndex none{};
+    family.push_back(&none);
+    for (const auto& kv : accepted_) family.push_back(&kv.first);
+    for (const ComponentIndex* i : family) {
+      int b = 0;
+      for (const ComponentIndex* u : family)
+        if (u->is_superset_of(*i)) b += ((u->order() - i->order()) % 2 == 0) ? 1 : -1;
+      coeff_b_[*i] = b;
+    }
+  }
 };
+
+// hdmr.hpp:364-483: the adaptive decomposition.  Per order k the index set is
+// the order-k indices that contain no rejected index; their cut grids are
+// built (here on opt.workers host threads, one component at a time each --
+// results do not depend on the schedule), eta prunes within the order
+// (order 1 is always kept), rho decides whether order k+1 is built.  Grids,
+// quadratures, eta, rho, the accepted / rejected sets and b are bit-identical
+// to the reference's (tests/cpp/test_ref_dropin.cpp).  exact_cuts is not
+// supported.
+inline DdsgFunction decompose(const Evaluator& f, int dim, int out_dim, const AnchorPoint& anchor,
+                              const DdsgOptions& opt, ExpansionDiagnostics* diag = nullptr) {
+  if (dim < 1) throw std::invalid_argument("decompose: dim must be >= 1");
+  if (opt.k_max < 1 || opt.k_max > dim)
+    throw std::invalid_argument("decompose: k_max must satisfy 1 <= k_max <= dim");
+  if (opt.eps_rho < 0.0 || opt.eps_eta < 0.0) throw std::invalid_argument("decompose: thresholds must be >= 0");
+  if (anchor.coords.size() != static_cast<std::size_t>(dim))
+    throw std::invalid_argument("decompose: anchor dimension mismatch");
+  if (opt.exact_cuts) throw std::invalid_argument("decompose: exact_cuts is not supported by the B200 drop-in");
+
+  DdsgFunction out;
+  out.dim_ = dim;
+  out.out_dim_ = out_dim;
+  out.opt_ = opt;
+  out.anchor_ = anchor;
+  if (out.anchor_.f_anchor.empty()) {
+    out.anchor_.f_anchor.resize(static_cast<std::size_t>(out_dim));
+    f(out.anchor_.coords, out.anchor_.f_anchor);
+  }
+  out.cut_quadratures_[ComponentIndex{}] = out.anchor_.f_anchor;
+
+  for (int k = 1; k <= opt.k_max; ++k) {
+    std::vector<ComponentIndex> current;
+    for (auto& u : order_k_indices(dim, static_cast<std::size_t>(k))) {
+      const bool pruned = std::any_of(out.rejected_.begin(), out.rejected_.end(),
+                                      [&](const ComponentIndex& z) { return u.is_superset_of(z); });
+      if (!pruned) current.push_back(std::move(u));
+    }
+    if (current.empty()) break;
+
+    // cut grids of this order: independent builds, the lowest failing component reports
+    std::vector<SparseGridFunction> grids(current.size());
+    std::vector<std::vector<double>> quads(current.size());
+    std::vector<std::string> failure(current.size());
+    std::vector<char> failed(current.size(), 0);
+    std::atomic<std::size_t> next{0};
+    auto worker = [&] {
+      for (std::size_t id = next.fetch_add(1); id < current.size(); id = next.fetch_add(1)) {
+        try {
+          SgBuildOptions sgo;
+          sgo.max_level = opt.max_level;
+          sgo.eps_gamma = opt.eps_gamma;
+          sgo.mode = opt.mode;
+          grids[id] = SparseGridFunction::build(cut_evaluator(f, out.anchor_, current[id]),
+                                                static_cast<int>(current[id].order()), out_dim, sgo);
+          quads[id] = grids[id].quadrature();
+        } catch (const std::exception& e) {
+          failed[id] = 1;
+          failure[id] = e.what();
+        }
+      }
+    };
+    {
+      const std::size_t nthreads = std::min<std::size_t>(std::max(1u, opt.workers), current.size());
+      std::vector<std::thread> pool;
+      for (std::size_t t = 1; t < nthreads; ++t) pool.emplace_back(worker);
+      worker();
+      for (auto& t : pool) t.join();
+    }
+    for (std::size_t id = 0; id < current.size(); ++id)
+      if (failed[id])
+        throw std::runtime_error("decompose: component " + current[id].to_string() + " failed: " + failure[id]);
+
+    // order boundary: eta within the order, then the bookkeeping
+    const auto lower_sum = out.cumulative_quadrature(static_cast<std::size_t>(k) - 1);
+    if (diag && diag->eta_by_order.size() < static_cast<std::size_t>(k))
+      diag->eta_by_order.resize(static_cast<std::size_t>(k));
+    for (std::size_t id = 0; id < current.size(); ++id) {
+      const ComponentIndex& u = current[id];
+      out.cut_quadratures_[u] = quads[id];
+      bool accept = true;
+      double eta = std::numeric_limits<double>::quiet_NaN();
+      if (u.order() >= 2) {
+        eta = eta_coefficient(out.component_quadrature(u), lower_sum);
+        accept = opt.eps_eta == 0.0 || eta > opt.eps_eta;
+      }
+      if (accept) {
+        out.accepted_[u] = std::move(grids[id]);
+      } else {
+        out.rejected_.insert(u);
+        out.cut_quadratures_.erase(u);
+      }
+      if (diag && u.order() >= 2) diag->eta_by_order[static_cast<std::size_t>(k) - 1].push_back({u, eta, accept});
+    }
+    out.order_reached_ = static_cast<std::size_t>(k);
+
+    const auto cum_k = out.cumulative_quadrature(static_cast<std::size_t>(k));
+    double rho = std::numeric_limits<double>::quiet_NaN();
+    bool stop = false;
+    try {
+      rho = expansion_rho(cum_k, lower_sum);
+      stop = rho < opt.eps_rho;
+    } catch (const rho_denominator_error&) {
+      stop = false;  // no evidence of convergence: keep expanding
+    }
+    if (diag) diag->rho_by_order.push_back(rho);
+    if (stop) break;
+  }
+  out.finalize_coefficients();
+  return out;
+}
 
 // Reusable evaluation buffers (ddsg_eval.hpp:21-24): pinned host staging,
 // device buffers and a stream, created on first use on the current device.

@@ -461,15 +461,179 @@ static void irbc_gpu_cases() {
   CHECK(e1.samples == e2.samples && e1.avg_log10 == e2.avg_log10);
 }
 
+// ------------------------------------------------- decomposition (test_hdmr.cpp)
+
+static AnchorPoint center_anchor(const Evaluator& f, int d, int m) {  // oracles.hpp: center of the cube
+  AnchorPoint a;
+  a.coords.assign(static_cast<std::size_t>(d), 0.5);
+  a.f_anchor.resize(static_cast<std::size_t>(m));
+  f(a.coords, a.f_anchor);
+  return a;
+}
+
+static void decompose_cpu_cases() {
+  auto idx = [](std::vector<int> dims) { return ComponentIndex{std::move(dims)}; };
+  // test_hdmr.cpp:32-50
+  {
+    const auto a = select_anchor(scalar([](std::span<const double> x) { return x[0] + x[1]; }), 2, 1, 4000, 42);
+    CHECK(std::abs(a.f_anchor[0] - 1.0) <= 0.05);
+    const auto ac = select_anchor(scalar([](std::span<const double>) { return 3.25; }), 3, 1, 50, 7);
+    CHECK(ac.f_anchor[0] == 3.25);
+    std::mt19937_64 rng(7);
+    std::uniform_real_distribution<double> unif(0.0, 1.0);
+    const double c0 = unif(rng), c1 = unif(rng), c2 = unif(rng);
+    CHECK((ac.coords == std::vector<double>{c0, c1, c2}));  // ties: the lowest sample index
+    const auto asq = select_anchor(scalar([](std::span<const double> x) { return x[0] * x[0]; }), 1, 1, 10000, 99);
+    CHECK(std::abs(asq.f_anchor[0] - 1.0 / 3.0) < 0.02);
+  }
+  // test_hdmr.cpp:52-80
+  {
+    auto f = scalar([](std::span<const double> x) { return x[0] * 10.0 + x[1] + 100.0 * x[2]; });
+    AnchorPoint a{{0.1, 0.2, 0.7}, {0.0}};
+    std::vector<double> out(1), y{0.2, 0.9};
+    cut_evaluator(f, a, idx({0, 1}))(y, out);
+    CHECK(std::abs(out[0] - (0.2 * 10.0 + 0.9 + 70.0)) <= 1e-15 * 73.0);
+    auto prod = scalar([](std::span<const double> x) { return x[0] * x[1] * x[2]; });
+    AnchorPoint half{{0.5, 0.5, 0.5}, {}};
+    std::vector<double> y1{0.5};
+    cut_evaluator(prod, half, idx({1}))(y1, out);
+    CHECK(std::abs(out[0] - 0.125) <= 1e-15);
+    std::vector<double> y3{0.3, 0.4, 0.5}, want(1);
+    cut_evaluator(f, a, idx({0, 1, 2}))(y3, out);
+    f(y3, want);
+    CHECK(out[0] == want[0]);
+    CHECK(throws<std::invalid_argument>([&] { (void)cut_evaluator(f, a, ComponentIndex{}); }));
+  }
+  // test_hdmr.cpp:82-90
+  CHECK(expansion_rho({2.0, 0.0}, {2.0, 0.0}) == 0.0);
+  CHECK(std::abs(expansion_rho({2.0, 2.0}, {2.0, 0.0}) - 1.0) < 1e-12);
+  CHECK(throws<rho_denominator_error>([] { (void)expansion_rho({1.0}, {0.0}); }));
+  CHECK(eta_coefficient({0.0}, {1.0}) == 0.0);
+  CHECK(std::isinf(eta_coefficient({1.0}, {0.0})));
+  // test_hdmr.cpp:92-106: the centered blind spot of eta
+  {
+    auto f = scalar([](std::span<const double> x) { return x[0] * x[1]; });
+    DdsgOptions opt;
+    opt.k_max = 2;
+    opt.max_level = 5;
+    opt.mode = BoundaryMode::modified_linear;
+    ExpansionDiagnostics diag;
+    (void)decompose(f, 2, 1, center_anchor(f, 2, 1), opt, &diag);
+    CHECK(diag.eta_by_order.size() == 2 && diag.eta_by_order[1].size() == 1);
+    if (diag.eta_by_order.size() == 2 && diag.eta_by_order[1].size() == 1) CHECK(diag.eta_by_order[1][0].eta < 1e-12);
+  }
+  // test_hdmr.cpp:150-173: rho stops a separable function after order 2
+  {
+    auto f = scalar([](std::span<const double> x) { return x[0] + x[1] + x[2]; });
+    AnchorPoint anchor{{0.2, 0.8, 0.3}, {}};
+    DdsgOptions opt;
+    opt.k_max = 3;
+    opt.eps_rho = 1e-4;
+    opt.max_level = 4;
+    opt.mode = BoundaryMode::modified_linear;
+    opt.workers = 2;
+    ExpansionDiagnostics diag;
+    const auto dd = decompose(f, 3, 1, anchor, opt, &diag);
+    CHECK(dd.order_reached() == 2);
+    CHECK(diag.rho_by_order.size() == 2 && std::abs(diag.rho_by_order[1]) <= 1e-13);
+    CHECK(dd.accepted().count(idx({0})) == 1 && dd.accepted().count(idx({1})) == 1 && dd.accepted().count(idx({2})) == 1);
+    CHECK(dd.accepted().count(idx({0, 1})) == 1 && dd.accepted().count(idx({0, 1, 2})) == 0);
+    for (const auto& u : {idx({0, 1}), idx({0, 2}), idx({1, 2})}) CHECK(std::abs(dd.component_quadrature(u)[0]) < 1e-13);
+  }
+  // test_hdmr.cpp:193-220: eta prunes supersets of rejected indices
+  {
+    auto f = scalar([](std::span<const double> x) {
+      return x[0] + x[1] + std::exp(x[0] * x[2]) + std::exp(x[1] * x[2]);
+    });
+    DdsgOptions opt;
+    opt.k_max = 3;
+    opt.eps_eta = 1e-5;
+    opt.max_level = 5;
+    opt.mode = BoundaryMode::modified_linear;
+    opt.workers = 3;
+    const auto dd = decompose(f, 3, 1, center_anchor(f, 3, 1), opt);
+    CHECK(dd.rejected().count(idx({0, 1})) == 1);
+    CHECK(dd.accepted().count(idx({0, 2})) == 1 && dd.accepted().count(idx({1, 2})) == 1);
+    CHECK(dd.accepted().count(idx({0, 1, 2})) == 0 && dd.rejected().count(idx({0, 1, 2})) == 0);
+    bool sound = true;
+    for (const auto& [u, grid] : dd.accepted()) {
+      for (const auto& z : dd.rejected()) sound = sound && !u.is_superset_of(z);
+      for (const auto& v : all_subsets(u))
+        if (!v.empty()) sound = sound && dd.accepted().count(v) == 1;
+    }
+    CHECK(sound);
+  }
+  // test_hdmr.cpp:222-243: with zero thresholds the telescoping collapses
+  {
+    auto f = scalar([](std::span<const double> x) {
+      return std::exp(x[0]) * (1.0 + 0.5 * std::sin(3.0 * x[1])) + x[1] * x[2];
+    });
+    DdsgOptions opt;
+    opt.k_max = 3;
+    opt.max_level = 4;
+    opt.mode = BoundaryMode::modified_linear;
+    const auto dd = decompose(f, 3, 1, center_anchor(f, 3, 1), opt);
+    bool collapsed = dd.coeff_b().size() == 8;
+    for (const auto& [u, b] : dd.coeff_b()) collapsed = collapsed && b == (u.order() == 3 ? 1 : 0);
+    CHECK(collapsed);
+    CHECK(order_k_indices(5, 2).size() == 10 && order_k_indices(3, 4).empty());
+  }
+}
+
+static void decompose_gpu_cases() {
+  // test_hdmr.cpp:175-190 and 245-251: the decomposition against the plain sparse grid
+  {
+    auto f = scalar([](std::span<const double> x) { return x[0] + x[1] + x[2]; });
+    AnchorPoint anchor{{0.2, 0.8, 0.3}, {}};
+    DdsgOptions opt;
+    opt.k_max = 3;
+    opt.eps_rho = 1e-4;
+    opt.max_level = 4;
+    opt.mode = BoundaryMode::modified_linear;
+    const auto dd = decompose(f, 3, 1, anchor, opt);
+    const auto sg = build_scalar([](std::span<const double> x) { return x[0] + x[1] + x[2]; }, 3, 4, 0.0,
+                                 BoundaryMode::modified_linear);
+    double err_dd = 0.0, err_sg = 0.0;
+    for (const auto& p : uniform_points(3, 1000, 5150)) {
+      std::vector<double> want(1);
+      f(p, want);
+      err_dd = std::max(err_dd, std::abs(dd.evaluate_naive(p)[0] - want[0]));
+      err_sg = std::max(err_sg, std::abs(sg.interpolate(p)[0] - want[0]));
+    }
+    CHECK(err_dd <= err_sg + 1e-12);
+  }
+  {
+    auto fn = [](std::span<const double> x) { return std::exp(x[0]) * (1.0 + 0.5 * std::sin(3.0 * x[1])) + x[1] * x[2]; };
+    auto f = scalar(fn);
+    DdsgOptions opt;
+    opt.k_max = 3;
+    opt.max_level = 4;
+    opt.mode = BoundaryMode::modified_linear;
+    const auto dd = decompose(f, 3, 1, center_anchor(f, 3, 1), opt);
+    const auto sg = build_scalar(fn, 3, 4, 0.0, BoundaryMode::modified_linear);
+    const auto vec = VectorizedDdsg::compile(std::make_shared<const DdsgFunction>(dd));
+    double worst = 0.0, worst_vec = 0.0;
+    for (const auto& p : uniform_points(3, 200, 909)) {
+      const double ref = sg.interpolate(p)[0];
+      worst = std::max(worst, std::abs(dd.evaluate_naive(p)[0] - ref));
+      worst_vec = std::max(worst_vec, std::abs(vec.evaluate(p)[0] - ref));
+    }
+    CHECK(worst <= 1e-12);
+    CHECK(worst_vec <= 1e-12);
+  }
+}
+
 int main(int argc, char** argv) {
   const std::string which = argc > 1 ? argv[1] : "cpu";
   if (which == "cpu" || which == "all") {
     cpu_cases();
     irbc_cpu_cases();
+    decompose_cpu_cases();
   }
   if (which == "gpu" || which == "all") {
     gpu_cases();
     irbc_gpu_cases();
+    decompose_gpu_cases();
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;

@@ -17,7 +17,10 @@
 //      it through the C-ABI (tools/ddsg.cpp:261-268 shape) and evaluates it
 //      on the GPU bit-exactly; the shim's writer is read back by the
 //      reference's ddsg_from_json, same bits;
-//   5. slots(), cut quadratures, exception types.
+//   5. slots(), cut quadratures, exception types;
+//   6. ddsg_b200::decompose / select_anchor (the shim's own restatement of
+//      hdmr.hpp:45-133,364-483) against ddsg::decompose: identical accepted /
+//      rejected sets, b, cut grids, quadratures and eta / rho diagnostics.
 // Exit code = number of failed checks.
 #include <cmath>
 #include <cstdio>
@@ -265,6 +268,123 @@ int main() {
     CHECK(throws<std::invalid_argument>([] { (void)ddsg_b200::sparse_grid_from_json(ddsg_b200::JsonDocument{"{\"schema_version\": 2}"}); }));
     CHECK(throws<std::invalid_argument>([] { (void)ddsg_b200::ddsg_from_json(ddsg_b200::JsonDocument{"[1, 2"}); }));
     fs::remove_all(dir);
+  }
+
+  // 6. the decomposition itself (hdmr.hpp:364-483) through the shim: same
+  //    target, anchor and options under both namespaces; accepted / rejected
+  //    sets, b, every cut grid (stored order, keys, surplus bits), cut
+  //    quadratures and the eta / rho diagnostics must be identical.
+  for (int variant = 0; variant < 3; ++variant) {
+    ddsg::DdsgOptions ro = opt;
+    ddsg_b200::DdsgOptions bo;
+    if (variant == 1) {  // order 3, everything kept, rho stops nothing
+      ro.k_max = 3;
+      ro.max_level = 3;
+      ro.eps_eta = 0.0;
+      ro.eps_gamma = 0.0;
+    } else if (variant == 2) {  // zero-boundary cuts, rho stops after order 1
+      ro.mode = ddsg::BoundaryMode::zero_boundary;
+      ro.max_level = 4;
+      ro.eps_rho = 10.0;
+    }
+    bo.k_max = ro.k_max;
+    bo.eps_rho = ro.eps_rho;
+    bo.eps_eta = ro.eps_eta;
+    bo.max_level = ro.max_level;
+    bo.eps_gamma = ro.eps_gamma;
+    bo.mode = ro.mode == ddsg::BoundaryMode::modified_linear ? ddsg_b200::BoundaryMode::modified_linear
+                                                             : ddsg_b200::BoundaryMode::zero_boundary;
+    bo.workers = 3;
+    ddsg::ExpansionDiagnostics dr;
+    ddsg_b200::ExpansionDiagnostics db;
+    const auto ref_anchor = ddsg::select_anchor(target, d, m, 64, 11);
+    const auto b200_anchor = ddsg_b200::select_anchor(target, d, m, 64, 11);
+    CHECK(same_bits(ref_anchor.coords, b200_anchor.coords) && same_bits(ref_anchor.f_anchor, b200_anchor.f_anchor));
+    ddsg::AnchorPoint ar = variant == 0 ? anchor : ref_anchor;
+    ddsg_b200::AnchorPoint ab{ar.coords, ar.f_anchor};
+    const ddsg::DdsgFunction fr = ddsg::decompose(target, d, m, ar, ro, &dr);
+    const ddsg_b200::DdsgFunction fb = ddsg_b200::decompose(target, d, m, ab, bo, &db);
+    bool same = fr.accepted().size() == fb.accepted().size() && fr.rejected().size() == fb.rejected().size() &&
+                fr.order_reached() == fb.order_reached() && fr.total_grid_points() == fb.total_grid_points() &&
+                same_bits(fr.anchor().f_anchor, fb.anchor().f_anchor);
+    for (const auto& z : fr.rejected()) same = same && fb.rejected().count(ddsg_b200::ComponentIndex{z.dims}) == 1;
+    for (const auto& [u, b] : fr.coeff_b()) {
+      const auto it = fb.coeff_b().find(ddsg_b200::ComponentIndex{u.dims});
+      same = same && it != fb.coeff_b().end() && it->second == b;
+      same = same && same_bits(fr.cut_quadrature(u), fb.cut_quadrature(ddsg_b200::ComponentIndex{u.dims}));
+    }
+    std::size_t nodes = 0;
+    for (const auto& [u, g] : fr.accepted()) {
+      const auto it = fb.accepted().find(ddsg_b200::ComponentIndex{u.dims});
+      if (it == fb.accepted().end() || it->second.size() != g.size()) {
+        same = false;
+        continue;
+      }
+      const auto& nb = it->second.nodes();
+      for (std::size_t i = 0; i < g.size(); ++i)
+        same = same && nb[i].key == g.nodes()[i].key && same_bits(nb[i].surplus, g.nodes()[i].surplus);
+      nodes += g.size();
+    }
+    CHECK(same);
+    bool diag_same = dr.rho_by_order.size() == db.rho_by_order.size() && dr.eta_by_order.size() == db.eta_by_order.size();
+    for (std::size_t k = 0; diag_same && k < dr.rho_by_order.size(); ++k)
+      diag_same = std::memcmp(&dr.rho_by_order[k], &db.rho_by_order[k], sizeof(double)) == 0;
+    for (std::size_t k = 0; diag_same && k < dr.eta_by_order.size(); ++k) {
+      diag_same = dr.eta_by_order[k].size() == db.eta_by_order[k].size();
+      for (std::size_t i = 0; diag_same && i < dr.eta_by_order[k].size(); ++i)
+        diag_same = dr.eta_by_order[k][i].index.dims == db.eta_by_order[k][i].index.dims &&
+                    dr.eta_by_order[k][i].accepted == db.eta_by_order[k][i].accepted &&
+                    std::memcmp(&dr.eta_by_order[k][i].eta, &db.eta_by_order[k][i].eta, sizeof(double)) == 0;
+    }
+    CHECK(diag_same);
+    // the native decomposition evaluates like the reference's (vectorized and naive)
+    auto vb = ddsg_b200::VectorizedDdsg::compile(std::make_shared<const ddsg_b200::DdsgFunction>(fb));
+    auto vr = ddsg::VectorizedDdsg::compile(std::make_shared<const ddsg::DdsgFunction>(fr));
+    std::vector<double> a(m), b(m);
+    int diff = 0, diff_naive = 0;
+    for (std::size_t i = 0; i < 200; ++i) {
+      vr.evaluate(pts[i], a);
+      vb.evaluate(pts[i], b);
+      diff += !same_bits(a, b);
+      if (i < 20) {
+        std::uint64_t cr = 0, cb = 0;
+        fr.evaluate_naive(pts[i], a, &cr);
+        fb.evaluate_naive(pts[i], b, &cb);
+        diff_naive += !same_bits(a, b) || cr != cb;
+      }
+    }
+    CHECK(diff == 0);
+    CHECK(diff_naive == 0);
+    std::printf("decompose variant %d through the shim: %zu accepted, %zu rejected, order %zu, %zu nodes: %s\n", variant,
+                fb.accepted().size(), fb.rejected().size(), fb.order_reached(), nodes, same && diag_same ? "identical" : "DIFFERENT");
+  }
+  {  // argument checks and the failing-component report (hdmr.hpp:366-373, 425-429)
+    ddsg_b200::DdsgOptions bo;
+    bo.k_max = 1;
+    bo.max_level = 2;
+    ddsg_b200::AnchorPoint ab{std::vector<double>(d, 0.5), {}};
+    CHECK(throws<std::invalid_argument>([&] { (void)ddsg_b200::decompose(target, 0, m, ab, bo); }));
+    ddsg_b200::DdsgOptions bad = bo;
+    bad.k_max = d + 1;
+    CHECK(throws<std::invalid_argument>([&] { (void)ddsg_b200::decompose(target, d, m, ab, bad); }));
+    bad = bo;
+    bad.eps_eta = -1.0;
+    CHECK(throws<std::invalid_argument>([&] { (void)ddsg_b200::decompose(target, d, m, ab, bad); }));
+    ddsg_b200::AnchorPoint short_anchor{std::vector<double>(d - 1, 0.5), {}};
+    CHECK(throws<std::invalid_argument>([&] { (void)ddsg_b200::decompose(target, d, m, short_anchor, bo); }));
+    auto nan_target = [](std::span<const double> x, std::span<double> out) {
+      target(x, out);
+      if (x[2] != 0.5) out[1] = std::nan("");
+    };
+    bool reported = false;
+    try {
+      (void)ddsg_b200::decompose(nan_target, d, m, ab, bo);
+    } catch (const std::runtime_error& e) {
+      reported = std::string(e.what()).rfind("decompose: component {2} failed: ", 0) == 0;
+    }
+    CHECK(reported);
+    CHECK(throws<std::invalid_argument>([&] { (void)ddsg_b200::select_anchor(target, d, m, 0, 1); }));
+    CHECK(throws<std::invalid_argument>([&] { (void)ddsg_b200::cut_evaluator(target, ab, ddsg_b200::ComponentIndex{}); }));
   }
 
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
