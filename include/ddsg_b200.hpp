@@ -23,6 +23,7 @@
 #include <sstream>
 #include <functional>
 #include <atomic>
+#include <bit>
 #include <limits>
 #include <map>
 #include <mutex>
@@ -46,6 +47,108 @@ using NodeKey = std::vector<HeapKey>;     // grid_index.hpp:22
 
 enum class BoundaryMode { zero_boundary, modified_linear };  // basis.hpp:22
 enum class SurplusNorm { inf, l2 };                          // sparse_grid.hpp:53
+
+// ---- 1-d node bookkeeping (grid_index.hpp:24-55): node (l, i), i odd, as the
+// heap key 2^(l-1) + (i-1)/2 (root (1,1) = 1, parent = key >> 1).
+inline int level_of(HeapKey hk) { return static_cast<int>(std::bit_width(hk)); }
+inline std::uint32_t index_of(HeapKey hk) { return ((hk << 1) | 1u) - (std::uint32_t{1} << level_of(hk)); }
+inline HeapKey heap_key(int level, std::uint32_t index) {
+  if (level < 1 || level > 30) throw std::invalid_argument("heap_key: level out of range [1,30]");
+  const std::uint32_t last = (std::uint32_t{1} << level) - 1u;
+  if ((index & 1u) == 0u || index > last)
+    throw std::invalid_argument("heap_key: index must be odd in [1, 2^l - 1], got l=" + std::to_string(level) +
+                                " i=" + std::to_string(index));
+  return (index + last) >> 1;  // 2^(l-1) + (i-1)/2
+}
+inline double coordinate_of(HeapKey hk) { return std::ldexp(static_cast<double>(index_of(hk)), -level_of(hk)); }
+inline bool has_parent(HeapKey hk) { return hk > 1u; }
+inline HeapKey parent_key(HeapKey hk) { return hk >> 1; }
+inline int level_sum(const NodeKey& key) {
+  int total = 0;
+  for (HeapKey hk : key) total += level_of(hk);
+  return total;
+}
+inline void coordinates_of(const NodeKey& key, std::vector<double>& out) {
+  out.resize(key.size());
+  std::transform(key.begin(), key.end(), out.begin(), [](HeapKey hk) { return coordinate_of(hk); });
+}
+
+// ---- 1-d basis (basis.hpp:25-84): same expressions, so host values carry the
+// reference's bits (the device kernels restate them exactly).
+enum class BasisKind : std::uint8_t { hat, constant_one, left_edge, right_edge };
+inline BasisKind basis_kind(int level, std::uint32_t index, BoundaryMode mode) {
+  if (mode == BoundaryMode::zero_boundary) return BasisKind::hat;
+  if (level == 1) return BasisKind::constant_one;
+  if (index == 1u) return BasisKind::left_edge;
+  return index == (1u << level) - 1u ? BasisKind::right_edge : BasisKind::hat;
+}
+inline double basis_value(BasisKind kind, double center, double inv_h, double x) {  // inv_h = 2^l, center = i 2^-l
+  double v = 1.0;
+  if (kind == BasisKind::constant_one) return v;
+  if (kind == BasisKind::left_edge)
+    v = 2.0 - x * inv_h;
+  else if (kind == BasisKind::right_edge)
+    v = 2.0 - (1.0 - x) * inv_h;
+  else
+    v = 1.0 - std::abs(x - center) * inv_h;
+  return v > 0.0 ? v : 0.0;
+}
+inline double basis_weight(BasisKind kind, double h) {  // integral over [0,1]
+  if (kind == BasisKind::constant_one) return 1.0;
+  return (kind == BasisKind::left_edge || kind == BasisKind::right_edge) ? 2.0 * h : h;
+}
+inline double basis_1d(int level, std::uint32_t index, double x, BoundaryMode mode) {
+  (void)heap_key(level, index);  // validates the pair
+  if (x < 0.0 || x > 1.0) throw std::domain_error("basis_1d: x outside [0,1]");
+  const double inv_h = std::ldexp(1.0, level);
+  return basis_value(basis_kind(level, index, mode), static_cast<double>(index) / inv_h, inv_h, x);
+}
+inline double basis_nd(const NodeKey& key, std::span<const double> x, BoundaryMode mode) {
+  if (key.size() != x.size()) throw std::invalid_argument("basis_nd: dimension mismatch between key and point");
+  double w = 1.0;
+  for (std::size_t j = 0; j < key.size() && w != 0.0; ++j)
+    w *= basis_1d(level_of(key[j]), index_of(key[j]), x[j], mode);
+  return w;
+}
+
+// ---- node counts (hdmr.hpp:134-171): |V_{L,n}| = sum_{j<L} C(n-1+j, j) 2^j
+// and 1 + sum_{k<=k_max} C(d,k) |V_{L,k}|; std::overflow_error beyond 64 bits.
+namespace detail {
+inline std::uint64_t checked_mul(std::uint64_t a, std::uint64_t b, const char* who) {
+  std::uint64_t r;
+  if (__builtin_mul_overflow(a, b, &r)) throw std::overflow_error(std::string(who) + ": 64-bit overflow");
+  return r;
+}
+inline std::uint64_t checked_add(std::uint64_t a, std::uint64_t b, const char* who) {
+  std::uint64_t r;
+  if (__builtin_add_overflow(a, b, &r)) throw std::overflow_error(std::string(who) + ": 64-bit overflow");
+  return r;
+}
+}  // namespace detail
+inline std::uint64_t sg_node_count(int dim, int max_level) {
+  constexpr const char* who = "sg_node_count";
+  std::uint64_t total = 0;
+  for (int j = 0; j < max_level; ++j) {
+    std::uint64_t binom = 1;  // C(dim-1+j, j), built factor by factor (exact at every step)
+    for (int i = 1; i <= j; ++i)
+      binom = detail::checked_mul(binom, static_cast<std::uint64_t>(dim - 1 + i), who) / static_cast<std::uint64_t>(i);
+    if (j >= 64) throw std::overflow_error(std::string(who) + ": 64-bit overflow");
+    total = detail::checked_add(total, detail::checked_mul(binom, std::uint64_t{1} << j, who), who);
+  }
+  return total;
+}
+inline std::uint64_t ddsg_grid_count(int d, int k_max, int max_level) {
+  constexpr const char* who = "ddsg_grid_count";
+  if (d < 0 || k_max < 0 || k_max > d || max_level < 1) throw std::invalid_argument("ddsg_grid_count: invalid arguments");
+  std::uint64_t total = 1;  // the anchor
+  for (int k = 1; k <= k_max; ++k) {
+    std::uint64_t binom = 1;  // C(d, k)
+    for (int i = 1; i <= k; ++i)
+      binom = detail::checked_mul(binom, static_cast<std::uint64_t>(d - k + i), who) / static_cast<std::uint64_t>(i);
+    total = detail::checked_add(total, detail::checked_mul(binom, sg_node_count(k, max_level), who), who);
+  }
+  return total;
+}
 
 class build_error : public std::runtime_error {  // sparse_grid.hpp:40-48
  public:

@@ -580,6 +580,75 @@ static void decompose_cpu_cases() {
   }
 }
 
+// ------------------------------------- node keys, basis, counts (host inline functions)
+
+static void index_basis_cpu_cases() {
+  // grid_index.hpp:24-55
+  CHECK(heap_key(1, 1) == 1u && heap_key(2, 1) == 2u && heap_key(2, 3) == 3u && heap_key(3, 5) == 6u);
+  for (int l = 1; l <= 12; ++l)
+    for (std::uint32_t i = 1; i < (1u << l); i += 2) {
+      const HeapKey hk = heap_key(l, i);
+      if (level_of(hk) != l || index_of(hk) != i || coordinate_of(hk) != static_cast<double>(i) / std::ldexp(1.0, l)) {
+        CHECK(false);
+        return;
+      }
+    }
+  CHECK(!has_parent(1u) && has_parent(2u) && parent_key(6u) == 3u && parent_key(7u) == 3u);
+  CHECK(level_sum(NodeKey{1u, 2u, 5u}) == 1 + 2 + 3);
+  std::vector<double> xy;
+  coordinates_of(NodeKey{heap_key(1, 1), heap_key(3, 7)}, xy);
+  CHECK((xy == std::vector<double>{0.5, 0.875}));
+  CHECK(throws<std::invalid_argument>([] { (void)heap_key(0, 1); }));
+  CHECK(throws<std::invalid_argument>([] { (void)heap_key(31, 1); }));
+  CHECK(throws<std::invalid_argument>([] { (void)heap_key(2, 2); }));
+  CHECK(throws<std::invalid_argument>([] { (void)heap_key(2, 5); }));
+  // test_sparse_grid.cpp:31-47
+  CHECK(basis_1d(1, 1, 0.5, BoundaryMode::zero_boundary) == 1.0);
+  CHECK(basis_1d(2, 1, 0.5, BoundaryMode::zero_boundary) == 0.0);
+  CHECK(std::abs(basis_1d(2, 3, 0.6, BoundaryMode::zero_boundary) - 0.4) <= 1e-15);
+  CHECK(basis_1d(1, 1, 0.0, BoundaryMode::modified_linear) == 1.0);
+  CHECK(basis_1d(2, 1, 0.0, BoundaryMode::modified_linear) == 2.0);
+  CHECK(basis_1d(2, 3, 1.0, BoundaryMode::modified_linear) == 2.0);
+  CHECK(std::abs(basis_1d(2, 3, 0.6, BoundaryMode::modified_linear) - 0.4) <= 1e-15);
+  CHECK(basis_1d(3, 3, 0.375, BoundaryMode::modified_linear) == 1.0);
+  CHECK(throws<std::invalid_argument>([] { (void)basis_1d(2, 2, 0.5, BoundaryMode::zero_boundary); }));
+  CHECK(throws<std::invalid_argument>([] { (void)basis_1d(2, 5, 0.5, BoundaryMode::zero_boundary); }));
+  CHECK(throws<std::invalid_argument>([] { (void)basis_1d(0, 1, 0.5, BoundaryMode::zero_boundary); }));
+  CHECK(throws<std::domain_error>([] { (void)basis_1d(1, 1, 1.5, BoundaryMode::zero_boundary); }));
+  // test_sparse_grid.cpp:49-64
+  {
+    const NodeKey unit{heap_key(1, 1), heap_key(1, 1)};
+    std::vector<double> x{0.5, 0.5}, x2{0.5, 0.0}, x3{0.25, 0.6}, wrong{0.5};
+    CHECK(basis_nd(unit, x, BoundaryMode::zero_boundary) == 1.0);
+    CHECK(basis_nd(NodeKey{heap_key(1, 1), heap_key(2, 1)}, x2, BoundaryMode::zero_boundary) == 0.0);
+    CHECK(std::abs(basis_nd(NodeKey{heap_key(2, 1), heap_key(2, 3)}, x3, BoundaryMode::zero_boundary) - 0.4) <= 1e-15);
+    CHECK(throws<std::invalid_argument>([&] { (void)basis_nd(unit, wrong, BoundaryMode::zero_boundary); }));
+  }
+  CHECK(basis_weight(BasisKind::constant_one, 0.5) == 1.0 && basis_weight(BasisKind::hat, 0.25) == 0.25 &&
+        basis_weight(BasisKind::left_edge, 0.25) == 0.5 && basis_weight(BasisKind::right_edge, 0.125) == 0.25);
+  // test_hdmr.cpp:293-313
+  CHECK(ddsg_grid_count(4, 1, 3) == 29);
+  CHECK(ddsg_grid_count(2, 2, 2) == 12);
+  CHECK(ddsg_grid_count(5, 0, 4) == 1);
+  {
+    bool ok = true;
+    for (int d = 1; d <= 6; ++d)
+      for (int k = 1; k <= std::min(d, 3); ++k)
+        for (int L = 1; L <= 5; ++L) {
+          std::uint64_t want = 1;
+          for (int kk = 1; kk <= k; ++kk) {
+            std::uint64_t binom = 1;
+            for (int i = 1; i <= kk; ++i) binom = binom * static_cast<std::uint64_t>(d - kk + i) / static_cast<std::uint64_t>(i);
+            want += binom * brute_count(kk, L);
+          }
+          ok = ok && ddsg_grid_count(d, k, L) == want;
+        }
+    CHECK(ok);
+  }
+  CHECK(throws<std::overflow_error>([] { (void)ddsg_grid_count(300, 10, 10); }));
+  CHECK(throws<std::invalid_argument>([] { (void)ddsg_grid_count(3, 4, 2); }));
+}
+
 static void decompose_gpu_cases() {
   // test_hdmr.cpp:175-190 and 245-251: the decomposition against the plain sparse grid
   {
@@ -629,6 +698,7 @@ int main(int argc, char** argv) {
     cpu_cases();
     irbc_cpu_cases();
     decompose_cpu_cases();
+    index_basis_cpu_cases();
   }
   if (which == "gpu" || which == "all") {
     gpu_cases();

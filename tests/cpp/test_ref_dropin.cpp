@@ -387,6 +387,59 @@ int main() {
     CHECK(throws<std::invalid_argument>([&] { (void)ddsg_b200::cut_evaluator(target, ab, ddsg_b200::ComponentIndex{}); }));
   }
 
+  // 7. the host inline functions of rows a1 / a2 (grid_index.hpp, basis.hpp)
+  //    and the node-count formulas against the reference's, bit for bit
+  {
+    std::mt19937_64 r2(77);
+    std::uniform_real_distribution<double> u01(0.0, 1.0);
+    int bad = 0;
+    for (int l = 1; l <= 14; ++l)
+      for (std::uint32_t i = 1; i < (1u << l); i += (l > 8 ? 37u * 2u : 2u)) {
+        const auto hk = ddsg::heap_key(l, i);
+        bad += hk != ddsg_b200::heap_key(l, i) || ddsg::level_of(hk) != ddsg_b200::level_of(hk) ||
+               ddsg::index_of(hk) != ddsg_b200::index_of(hk) || ddsg::parent_key(hk) != ddsg_b200::parent_key(hk);
+        const double cr = ddsg::coordinate_of(hk), cb = ddsg_b200::coordinate_of(hk);
+        bad += std::memcmp(&cr, &cb, sizeof(double)) != 0;
+        for (int rep = 0; rep < 6; ++rep) {
+          const double xs[6] = {u01(r2), cr, 0.0, 1.0, cr - std::ldexp(1.0, -l), cr + std::ldexp(1.0, -l) * u01(r2)};
+          const double x = std::min(1.0, std::max(0.0, xs[rep]));
+          for (int md = 0; md < 2; ++md) {
+            const double vr = ddsg::basis_1d(l, i, x, md ? ddsg::BoundaryMode::modified_linear : ddsg::BoundaryMode::zero_boundary);
+            const double vb = ddsg_b200::basis_1d(l, i, x, md ? ddsg_b200::BoundaryMode::modified_linear
+                                                              : ddsg_b200::BoundaryMode::zero_boundary);
+            bad += std::memcmp(&vr, &vb, sizeof(double)) != 0;
+            bad += static_cast<int>(ddsg::basis_kind(l, i, md ? ddsg::BoundaryMode::modified_linear : ddsg::BoundaryMode::zero_boundary)) !=
+                   static_cast<int>(ddsg_b200::basis_kind(l, i, md ? ddsg_b200::BoundaryMode::modified_linear
+                                                                    : ddsg_b200::BoundaryMode::zero_boundary));
+          }
+        }
+      }
+    CHECK(bad == 0);
+    bad = 0;
+    for (int rep = 0; rep < 2000; ++rep) {
+      ddsg::NodeKey key(4);
+      std::vector<double> x(4);
+      for (int j = 0; j < 4; ++j) {
+        const int l = 1 + static_cast<int>(r2() % 6);
+        key[j] = ddsg::heap_key(l, 2u * static_cast<std::uint32_t>(r2() % (1u << (l - 1))) + 1u);
+        x[j] = u01(r2);
+      }
+      const double vr = ddsg::basis_nd(key, x, ddsg::BoundaryMode::modified_linear);
+      const double vb = ddsg_b200::basis_nd(key, x, ddsg_b200::BoundaryMode::modified_linear);
+      bad += std::memcmp(&vr, &vb, sizeof(double)) != 0 || ddsg::level_sum(key) != ddsg_b200::level_sum(key);
+    }
+    CHECK(bad == 0);
+    bad = 0;
+    for (int dd2 = 1; dd2 <= 40; ++dd2)
+      for (int L = 1; L <= 12; ++L) {
+        bad += ddsg::sg_node_count(dd2, L) != ddsg_b200::sg_node_count(dd2, L);
+        for (int k = 0; k <= std::min(dd2, 3); ++k) bad += ddsg::ddsg_grid_count(dd2, k, L) != ddsg_b200::ddsg_grid_count(dd2, k, L);
+      }
+    CHECK(bad == 0);
+    CHECK(throws<std::overflow_error>([] { (void)ddsg_b200::sg_node_count(300, 70); }));
+    CHECK(throws<std::overflow_error>([] { (void)ddsg::sg_node_count(300, 70); }));
+  }
+
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;
 }
