@@ -350,7 +350,74 @@ class SparseGridFunction {
     return nodes()[static_cast<std::size_t>(idx)];
   }
 
+  // ---- refinement (sparse_grid.hpp:215-298; the steps the reference runs
+  // inside build, exposed so a host loop -- or several ranks -- can drive them)
+  // next_candidates(s): children of the significant nodes at level sum s,
+  // closed under missing ancestors, in insertion order.
+  std::vector<NodeKey> refine_candidates(int level_sum) const {
+    int64_t n = 0;
+    detail::check(ddsg_grid_refine_candidates(h_.get(), level_sum, &n, nullptr));
+    std::vector<uint32_t> flat(static_cast<std::size_t>(n) * static_cast<std::size_t>(dim_));
+    if (n > 0) detail::check(ddsg_grid_refine_candidates(h_.get(), level_sum, &n, flat.data()));
+    std::vector<NodeKey> keys(static_cast<std::size_t>(n));
+    for (std::size_t i = 0; i < keys.size(); ++i)
+      keys[i].assign(flat.begin() + static_cast<std::ptrdiff_t>(i * dim_),
+                     flat.begin() + static_cast<std::ptrdiff_t>((i + 1) * dim_));
+    return keys;
+  }
+  // surplus[i] = f_values[i] - interpolate(this grid, x(keys[i])) (sparse_grid.hpp:264-276),
+  // on the GPU, or on the host (the reference's own loop) with on_device = false.
+  std::vector<std::vector<double>> hierarchize(const std::vector<NodeKey>& keys,
+                                               const std::vector<std::vector<double>>& f_values,
+                                               bool on_device = true) const {
+    if (keys.size() != f_values.size()) throw std::invalid_argument("sparse grid: keys / values count mismatch");
+    std::vector<uint32_t> flat;
+    std::vector<double> f, sur(keys.size() * static_cast<std::size_t>(out_dim_));
+    for (std::size_t i = 0; i < keys.size(); ++i) {
+      if (keys[i].size() != static_cast<std::size_t>(dim_))
+        throw std::invalid_argument("sparse grid: node key dimension mismatch");
+      if (f_values[i].size() != static_cast<std::size_t>(out_dim_))
+        throw std::invalid_argument("sparse grid: node surplus length mismatch");
+      flat.insert(flat.end(), keys[i].begin(), keys[i].end());
+      f.insert(f.end(), f_values[i].begin(), f_values[i].end());
+    }
+    const int64_t n = static_cast<int64_t>(keys.size());
+    detail::check(on_device ? ddsg_hierarchize(h_.get(), n, flat.data(), f.data(), sur.data())
+                            : ddsg_hierarchize_host(h_.get(), n, flat.data(), f.data(), sur.data()));
+    std::vector<std::vector<double>> out(keys.size());
+    for (std::size_t i = 0; i < out.size(); ++i)
+      out[i].assign(sur.begin() + static_cast<std::ptrdiff_t>(i * out_dim_),
+                    sur.begin() + static_cast<std::ptrdiff_t>((i + 1) * out_dim_));
+    return out;
+  }
+  // insert_batch's append (sparse_grid.hpp:278-298): the only mutation.  Copies
+  // of this object share the grid; needs external synchronisation, like the
+  // reference's refinement.
+  void append(const std::vector<GridNode>& nodes) {
+    std::vector<uint32_t> flat;
+    std::vector<double> sur;
+    for (const auto& n : nodes) {
+      if (n.key.size() != static_cast<std::size_t>(dim_))
+        throw std::invalid_argument("sparse grid: node key dimension mismatch");
+      if (n.surplus.size() != static_cast<std::size_t>(out_dim_))
+        throw std::invalid_argument("sparse grid: node surplus length mismatch");
+      flat.insert(flat.end(), n.key.begin(), n.key.end());
+      sur.insert(sur.end(), n.surplus.begin(), n.surplus.end());
+    }
+    detail::check(ddsg_grid_append(h_.get(), static_cast<int64_t>(nodes.size()), flat.data(), sur.data()));
+    refresh();
+  }
+  // Re-reads the grid's properties after a mutation through the C-ABI
+  // (append, refine_step): drops the nodes() cache, picks up max_level.
+  void refresh() {
+    nodes_.reset();
+    int lvl = max_level_;
+    detail::check(ddsg_grid_info(h_.get(), nullptr, nullptr, nullptr, &lvl, nullptr, nullptr));
+    max_level_ = lvl;
+  }
+
   const ddsg_grid_t* handle() const { return h_.get(); }
+  ddsg_grid_t* mutable_handle() { return h_.get(); }
   // Takes ownership of a C-ABI grid handle (e.g. from ddsg_grid_from_json).
   static SparseGridFunction adopt(ddsg_grid_t* g) { return SparseGridFunction(g); }
 
@@ -376,6 +443,65 @@ class SparseGridFunction {
     mode_ = mode == DDSG_MODIFIED_LINEAR ? BoundaryMode::modified_linear : BoundaryMode::zero_boundary;
   }
 };
+
+// One adaptive refinement step of replicated grids across `world` ranks
+// (C-ABI ddsg_refine_step / ddsg_refine_step_nccl): grid g's
+// next build batch from level sum level_sums[g] is split over the ranks, each
+// rank evaluates `f(g, x, out)` at its share and hierarchizes it on its GPU,
+// the surplus rows are all-gathered (ncclAllGather over `nccl_comm`, an
+// ncclComm_t, on `stream`) and appended on every rank in batch order, so the
+// grids stay bit-identical everywhere and equal to the reference's build at
+// the next level.  world == 1: no communicator needed; on_device = false
+// hierarchizes on the host (no GPU).
+struct RefineStats {
+  std::int64_t new_nodes = 0, rounds = 0, gathered_bytes = 0;
+  double target_s = 0.0, hierarchize_s = 0.0, allgather_s = 0.0;
+};
+using NodeEvaluator = std::function<void(int grid, std::span<const double> x, std::span<double> out)>;
+inline RefineStats refine_step(const std::vector<SparseGridFunction*>& grids, const std::vector<int>& level_sums,
+                               const NodeEvaluator& f, void* nccl_comm = nullptr, int rank = 0, int world = 1,
+                               void* stream = nullptr, bool on_device = true) {
+  if (grids.size() != level_sums.size()) throw std::invalid_argument("refine_step: one level sum per grid");
+  struct Ctx {
+    const NodeEvaluator* f;
+    const std::vector<SparseGridFunction*>* grids;
+    std::exception_ptr err;
+  } ctx{&f, &grids, nullptr};
+  auto tramp = [](int g, const double* xs, int64_t count, double* out, void* c) -> int {
+    auto* cx = static_cast<Ctx*>(c);
+    const std::size_t d = static_cast<std::size_t>((*cx->grids)[static_cast<std::size_t>(g)]->dim());
+    const std::size_t m = static_cast<std::size_t>((*cx->grids)[static_cast<std::size_t>(g)]->out_dim());
+    try {
+      for (int64_t i = 0; i < count; ++i)
+        (*cx->f)(g, std::span<const double>(xs + i * d, d), std::span<double>(out + i * m, m));
+      return 0;
+    } catch (...) {
+      cx->err = std::current_exception();
+      return 1;
+    }
+  };
+  std::vector<ddsg_grid_t*> handles;
+  for (SparseGridFunction* g : grids) handles.push_back(g->mutable_handle());
+  ddsg_refine_stats st{};
+  ddsg_status s;
+  if (world > 1 || nccl_comm != nullptr)
+    s = ddsg_refine_step_nccl(handles.data(), static_cast<int>(handles.size()), level_sums.data(), tramp, &ctx,
+                              nccl_comm, rank, world, stream, &st);
+  else
+    s = ddsg_refine_step(handles.data(), static_cast<int>(handles.size()), level_sums.data(), tramp, &ctx, 0, 1,
+                         nullptr, nullptr, on_device ? 1 : 0, &st);
+  for (SparseGridFunction* g : grids) g->refresh();
+  if (ctx.err) std::rethrow_exception(ctx.err);
+  detail::check(s);
+  RefineStats out;
+  out.new_nodes = st.new_nodes;
+  out.rounds = st.rounds;
+  out.gathered_bytes = st.gathered_bytes;
+  out.target_s = st.target_s;
+  out.hierarchize_s = st.hierarchize_s;
+  out.allgather_s = st.allgather_s;
+  return out;
+}
 
 struct ComponentIndex {  // component_index.hpp:16-54
   std::vector<int> dims;

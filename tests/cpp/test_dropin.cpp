@@ -649,6 +649,91 @@ static void index_basis_cpu_cases() {
   CHECK(throws<std::invalid_argument>([] { (void)ddsg_grid_count(3, 4, 2); }));
 }
 
+// ------------------------------------------------ refinement through the shim
+
+static GridEvaluator refine_target() {  // 2 outputs, a kink: the adaptive build refines unevenly
+  return [](std::span<const double> x, std::span<double> out) {
+    double s = 0.0;
+    for (double v : x) s += v;
+    out[0] = std::max(0.0, s - 0.6 * static_cast<double>(x.size())) + 0.1 * x[0] * x[0];
+    out[1] = std::exp(-s) + 0.05 * x[x.size() - 1];
+  };
+}
+
+static bool same_nodes(const SparseGridFunction& a, const SparseGridFunction& b) {
+  if (a.size() != b.size() || a.max_level() != b.max_level()) return false;
+  const auto& na = a.nodes();
+  const auto& nb = b.nodes();
+  for (std::size_t i = 0; i < na.size(); ++i)
+    if (na[i].key != nb[i].key || na[i].surplus.size() != nb[i].surplus.size() ||
+        std::memcmp(na[i].surplus.data(), nb[i].surplus.data(), na[i].surplus.size() * sizeof(double)) != 0)
+      return false;
+  return true;
+}
+
+// One refinement step from level L equals the build at level L + 1
+// (sparse_grid.hpp:84-108 runs exactly these steps), node order and surplus bits.
+static void refine_cases(bool on_device) {
+  const GridEvaluator f = refine_target();
+  for (int dim = 1; dim <= 3; ++dim)
+    for (double eps : {0.0, 1e-3}) {
+      SgBuildOptions lo, hi;
+      lo.max_level = dim == 1 ? 5 : 3;
+      lo.eps_gamma = eps;
+      lo.mode = dim == 2 ? BoundaryMode::zero_boundary : BoundaryMode::modified_linear;
+      hi = lo;
+      hi.max_level = lo.max_level + 1;
+      SparseGridFunction g = SparseGridFunction::build(f, dim, 2, lo);
+      const SparseGridFunction want = SparseGridFunction::build(f, dim, 2, hi);
+      const std::size_t before = g.size();
+      (void)g.nodes();  // fill the cache: refine_step must drop it
+      const RefineStats st = refine_step({&g}, {lo.max_level + dim - 1},
+                                         [&](int, std::span<const double> x, std::span<double> out) { f(x, out); },
+                                         nullptr, 0, 1, nullptr, on_device);
+      CHECK(st.new_nodes == static_cast<std::int64_t>(want.size() - before));
+      CHECK(same_nodes(g, want));
+      if (eps == 0.0) {  // the manual steps: candidates, hierarchize, append (one level-sum group)
+        SparseGridFunction h = SparseGridFunction::build(f, dim, 2, lo);
+        const auto keys = h.refine_candidates(lo.max_level + dim - 1);
+        std::vector<std::vector<double>> fv(keys.size(), std::vector<double>(2));
+        std::vector<double> x;
+        for (std::size_t i = 0; i < keys.size(); ++i) {
+          coordinates_of(keys[i], x);
+          f(x, fv[i]);
+        }
+        const auto sur = h.hierarchize(keys, fv, on_device);
+        std::vector<GridNode> fresh(keys.size());
+        for (std::size_t i = 0; i < keys.size(); ++i) fresh[i] = GridNode{keys[i], sur[i], false};
+        h.append(fresh);
+        CHECK(h.size() == want.size());
+        bool same = h.size() == want.size();
+        for (std::size_t i = 0; same && i < h.size(); ++i)
+          same = h.nodes()[i].key == want.nodes()[i].key &&
+                 std::memcmp(h.nodes()[i].surplus.data(), want.nodes()[i].surplus.data(), 2 * sizeof(double)) == 0;
+        CHECK(same);
+        CHECK(throws<std::invalid_argument>([&] { h.append(fresh); }));  // duplicates are rejected
+      }
+    }
+  {  // a non-finite target value reports the node (build_error, sparse_grid.hpp:287-295)
+    SgBuildOptions lo;
+    lo.max_level = 2;
+    lo.mode = BoundaryMode::modified_linear;
+    SparseGridFunction g = SparseGridFunction::build(f, 1, 2, lo);
+    auto bad = [&](int, std::span<const double> x, std::span<double> out) {
+      f(x, out);
+      if (x[0] == 0.125) out[1] = std::numeric_limits<double>::infinity();
+    };
+    bool reported = false;
+    try {
+      (void)refine_step({&g}, {2}, bad, nullptr, 0, 1, nullptr, on_device);
+    } catch (const build_error& e) {
+      reported = e.point().size() == 1 && e.point()[0] == 0.125;
+    }
+    CHECK(reported);
+    CHECK(throws<std::invalid_argument>([&] { (void)refine_step({&g}, {1, 2}, bad); }));
+  }
+}
+
 static void decompose_gpu_cases() {
   // test_hdmr.cpp:175-190 and 245-251: the decomposition against the plain sparse grid
   {
@@ -699,11 +784,13 @@ int main(int argc, char** argv) {
     irbc_cpu_cases();
     decompose_cpu_cases();
     index_basis_cpu_cases();
+    refine_cases(false);
   }
   if (which == "gpu" || which == "all") {
     gpu_cases();
     irbc_gpu_cases();
     decompose_gpu_cases();
+    refine_cases(true);
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;

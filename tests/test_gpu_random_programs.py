@@ -14,6 +14,9 @@ and subnormal coordinates."""
 from __future__ import annotations
 
 import itertools
+import json
+import os
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -153,3 +156,47 @@ def test_random_grid_bit_exact(seed):
     nnz_o, h_o = O.port_grid_support(d, mode, keys, x)
     nnz, h = g.support(x)
     assert np.array_equal(nnz, nnz_o) and np.array_equal(h, h_o)
+
+
+# ------------------------------------------------------------------ campaign
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("DDSG_CAMPAIGN") is None,
+                    reason="long randomised campaign: set DDSG_CAMPAIGN=<seeds> (log in profiles/r2_parity_campaign.json)")
+def test_random_campaign():
+    """Seeds beyond the parametrised ones: DDSG_CAMPAIGN programs and as many
+    plain grids, values and support hashes bit for bit; the summary goes to
+    gpurun_out/parity_campaign.json."""
+    count = int(os.environ["DDSG_CAMPAIGN"])
+    bad, outputs, points, slot_kernel = [], 0, 0, 0
+    for seed in range(1000, 1000 + count):
+        d, m, fa, slots_o, vec, x = random_program(seed)
+        rc, want, _ = O.port_hdmr_eval(d, m, fa, slots_o, x)
+        y = vec.evaluate_batch(x)
+        nan = np.isnan(want)
+        nnz_o, h_o = O.port_hdmr_support(d, m, slots_o, x)
+        nnz, h = vec.support(x)
+        if rc != 0 or not (np.array_equal(np.isnan(y), nan) and np.array_equal(bits(y[~nan]), bits(want[~nan]))
+                           and np.array_equal(nnz, nnz_o) and np.array_equal(h, h_o)):
+            bad.append(("program", seed))
+        outputs += y.size
+        points += x.shape[0]
+        slot_kernel += int(vec.uses_slot_kernel())
+        d, m, mode, keys, sur, g, x = random_grid(seed)
+        rc, want, _ = O.port_grid_eval(d, m, mode, keys, sur, x)
+        y = g.interpolate(x)
+        nnz_o, h_o = O.port_grid_support(d, mode, keys, x)
+        nnz, h = g.support(x)
+        if rc != 0 or not (np.array_equal(bits(y), bits(want)) and np.array_equal(nnz, nnz_o)
+                           and np.array_equal(h, h_o)):
+            bad.append(("grid", seed))
+        outputs += y.size
+        points += x.shape[0]
+    out = Path(__file__).resolve().parent.parent / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    (out / "parity_campaign.json").write_text(json.dumps({
+        "what": "tests/test_gpu_random_programs.py::test_random_campaign: seeded random HDMR programs and plain grids "
+                "(seeds 1000..), GPU values and support hashes against the CPU oracle, bit for bit",
+        "programs": count, "grids": count, "programs_on_slot_kernel": slot_kernel, "points": points,
+        "outputs": outputs, "mismatching_cases": bad}, indent=1))
+    assert not bad, bad
