@@ -6,8 +6,10 @@
 // reference switches by replacing `ddsg::` with `ddsg_b200::`.  Evaluation
 // runs on the GPU; every batched call is one C-ABI call.
 //
-//   SparseGridFunction   sparse_grid.hpp:72-351
-//   DdsgFunction         hdmr.hpp:195-356   (from_parts, evaluate_naive; decompose / select_anchor: hdmr.hpp:45-133,364-483)
+//   node keys, basis     grid_index.hpp:24-55, basis.hpp:25-84 (heap_key, basis_1d, ... host inline)
+//   SparseGridFunction   sparse_grid.hpp:72-351 (+ refine_candidates / hierarchize / append, refine_step)
+//   DdsgFunction         hdmr.hpp:195-356   (from_parts, evaluate_naive)
+//   decompose            hdmr.hpp:45-133,364-483 (select_anchor, cut_evaluator, eta / rho, diagnostics)
 //   EvalWorkspace        ddsg_eval.hpp:21-24
 //   VectorizedDdsg       ddsg_eval.hpp:28-165
 //   JSON documents       serialize.hpp:17-160 (JsonDocument stands in for nlohmann::json)
