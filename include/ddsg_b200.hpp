@@ -1095,6 +1095,27 @@ class VectorizedDdsg {  // ddsg_eval.hpp:28-165
   int dim_ = 0, out_dim_ = 0;
 };
 
+// The time iteration's convergence measure (time_iteration.hpp:213-223): the
+// sup-norm change max_x max_c |p_new(x)[c] - p_prev(x)[c]| over a point set,
+// as two batched evaluations instead of two per-point calls per sample.
+inline double policy_change(const VectorizedDdsg& p_new, const VectorizedDdsg& p_prev,
+                            const std::vector<std::vector<double>>& points) {
+  if (p_new.dim() != p_prev.dim() || p_new.out_dim() != p_prev.out_dim())
+    throw std::invalid_argument("policy_change: the two policies differ in shape");
+  const std::size_t n = points.size(), d = static_cast<std::size_t>(p_new.dim()),
+                    m = static_cast<std::size_t>(p_new.out_dim());
+  std::vector<double> x(n * d), a(n * m), b(n * m);
+  for (std::size_t i = 0; i < n; ++i) {
+    if (points[i].size() != d) throw std::invalid_argument("ddsg: query dimension mismatch");
+    std::copy(points[i].begin(), points[i].end(), x.begin() + static_cast<std::ptrdiff_t>(i * d));
+  }
+  p_new.evaluate_batch(x.data(), static_cast<int64_t>(n), a.data());
+  p_prev.evaluate_batch(x.data(), static_cast<int64_t>(n), b.data());
+  double change = 0.0;
+  for (std::size_t k = 0; k < a.size(); ++k) change = std::max(change, std::abs(a[k] - b[k]));
+  return change;
+}
+
 // ------------------------------------------------------------ JSON documents
 // serialize.hpp:17-160 with JsonDocument in place of nlohmann::json: the
 // text of a schema-version-1 document; load_json / save_json do the file

@@ -387,6 +387,31 @@ int main() {
     CHECK(throws<std::invalid_argument>([&] { (void)ddsg_b200::cut_evaluator(target, ab, ddsg_b200::ComponentIndex{}); }));
   }
 
+  // 6b. the time iteration's policy-change measure (time_iteration.hpp:213-223)
+  {
+    ddsg::DdsgOptions o2 = opt;
+    o2.max_level = 4;
+    o2.eps_eta = 0.0;
+    auto d2 = std::make_shared<const ddsg::DdsgFunction>(ddsg::decompose(target, d, m, anchor, o2));
+    auto prev_ref = std::make_shared<const ddsg::VectorizedDdsg>(ddsg::VectorizedDdsg::compile(d2));
+    const ddsg_b200::VectorizedDdsg prev_gpu = to_b200(*d2);
+    double change = 0.0;  // the reference's loop, verbatim shape
+    {
+      auto p_new = ref_side::compiled_evaluator(vec_ref);
+      auto p_prev = ref_side::compiled_evaluator(prev_ref);
+      std::vector<double> a(static_cast<std::size_t>(m)), b(static_cast<std::size_t>(m));
+      for (const auto& x : pts) {
+        p_new(x, a);
+        p_prev(x, b);
+        for (int c = 0; c < m; ++c)
+          change = std::max(change, std::abs(a[static_cast<std::size_t>(c)] - b[static_cast<std::size_t>(c)]));
+      }
+    }
+    const double change_gpu = ddsg_b200::policy_change(*vec_gpu, prev_gpu, pts);
+    CHECK(change > 0.0 && std::memcmp(&change, &change_gpu, sizeof(double)) == 0);
+    std::printf("policy change over %zu points: %.17g (reference) %.17g (batched)\n", pts.size(), change, change_gpu);
+  }
+
   // 7. the host inline functions of rows a1 / a2 (grid_index.hpp, basis.hpp)
   //    and the node-count formulas against the reference's, bit for bit
   {
