@@ -869,6 +869,9 @@ inline DdsgFunction decompose(const Evaluator& f, int dim, int out_dim, const An
         } catch (const std::exception& e) {
           failed[id] = 1;
           failure[id] = e.what();
+        } catch (...) {  // never let an exception leave a pool thread
+          failed[id] = 1;
+          failure[id] = "unknown error";
         }
       }
     };
