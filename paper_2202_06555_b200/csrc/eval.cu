@@ -699,8 +699,19 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
     const size_t wb = pg->workspace_bytes(n);
     return pg->launch(exact, dx, n, base, dy, dbad, wb ? xt_scratch.get(wb) : nullptr, st);
   }
+  // (when the slot kernel can split this batch over its subtrees, the
+  // small-batch path is taken only while its estimate -- 0.25 ns per point,
+  // slot and column chunk -- stays below the split launch's)
+  const auto small_wins = [&] {
+    static const bool fixed = std::getenv("DDSG_SMALL_BATCH") != nullptr;  // explicit threshold: no estimate
+    const FastHdmr* f = prog.fast();
+    const double split_us = (f && !fixed) ? f->split_cost_us(n) : 0.0;
+    if (split_us <= 0.0) return true;
+    const double small_us = 40.0 + 0.25e-3 * static_cast<double>(n) * P.n_active * ((P.m + 7) / 8);
+    return small_us <= split_us;
+  };
   if (!P.plain && P.n_active > 1 && n <= small_batch_points() &&
-      static_cast<size_t>(2 * P.n_active) * 8 * 8 <= size_t{200} * 1024) {
+      static_cast<size_t>(2 * P.n_active) * 8 * 8 <= size_t{200} * 1024 && small_wins()) {
     // few points: slot-parallel rows, then the pairwise tree per (point, chunk)
     constexpr int kCols = 8;
     const int chunks = (P.m + kCols - 1) / kCols;
@@ -723,7 +734,9 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
     int64_t launches = 0;
     for (int64_t off = 0; off < n; off += chunk) {
       const int64_t cnt = std::min(chunk, n - off);
-      double* xt = static_cast<double*>(xt_scratch.get(static_cast<size_t>(std::min(chunk, n)) * d * 8));
+      // (a short last chunk may take the split path: its partial sums are small, but sized explicitly)
+      double* xt = static_cast<double*>(
+          xt_scratch.get(std::max(f->scratch_bytes(std::min(chunk, n)), f->scratch_bytes(cnt))));
       launches += f->launch(exact, dx + off * d, cnt, base + off, dy + off * P.m, dbad, xt, st);
     }
     return launches;

@@ -68,6 +68,11 @@ FastHdmr::~FastHdmr() {
   if (block_off_) cudaFree(block_off_);
   if (block_len_) cudaFree(block_len_);
   if (slot_dims_) cudaFree(slot_dims_);
+  for (auto& level : split_)
+    for (SubTree& t : level) {
+      if (t.off) cudaFree(t.off);
+      if (t.len) cudaFree(t.len);
+    }
 }
 
 // Position of subspace l in the canonical (|l|_1, l lex) order of a k-d grid.
@@ -365,10 +370,134 @@ bool FastHdmr::build(const HostProgram& hp) {
   DDSG_CUDA(cudaMalloc(&block_len_, len.size() * sizeof(int32_t)));
   DDSG_CUDA(cudaMemcpy(block_len_, len.data(), len.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   for (int e = 0; e < 2; ++e) DDSG_CUDA(instance_attr(e)(static_cast<int>(smem)));
+
+  // subtree block ranges for split launches (see fast_hdmr.cuh)
+  max_split_ = 0;
+  for (auto& level : split_) {
+    for (SubTree& t : level) {
+      if (t.off) cudaFree(t.off);
+      if (t.len) cudaFree(t.len);
+    }
+    level.clear();
+  }
+  for (int S = 1; S <= kMaxSplit && S < levels; ++S) {
+    bool ok = true;
+    for (int a = 0; a < na && ok; ++a) ok = tree_s[a] <= levels - S;  // every leaf at depth >= S
+    if (!ok) break;
+    std::vector<SubTree> subs(size_t{1} << S);
+    for (int blk = 0; blk < nb; ++blk) {
+      SubTree& t = subs[static_cast<size_t>(tree_t[plans[blk].slot] >> (levels - S))];
+      if (t.count == 0) t.first = blk;
+      ok = ok && t.first + t.count == blk;  // contiguous block range
+      ++t.count;
+    }
+    for (const SubTree& t : subs) ok = ok && t.count > 0;
+    if (!ok) break;
+    for (SubTree& t : subs) {
+      std::vector<int64_t> so(static_cast<size_t>(n_cb_) * t.count);
+      std::vector<int32_t> sl(so.size());
+      for (int cb = 0; cb < n_cb_; ++cb)
+        for (int i = 0; i < t.count; ++i) {
+          so[static_cast<size_t>(cb) * t.count + i] = off[static_cast<size_t>(cb) * nb + t.first + i];
+          sl[static_cast<size_t>(cb) * t.count + i] = len[static_cast<size_t>(cb) * nb + t.first + i];
+        }
+      DDSG_CUDA(cudaMalloc(&t.off, so.size() * sizeof(int64_t)));
+      DDSG_CUDA(cudaMemcpy(t.off, so.data(), so.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+      DDSG_CUDA(cudaMalloc(&t.len, sl.size() * sizeof(int32_t)));
+      DDSG_CUDA(cudaMemcpy(t.len, sl.data(), sl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    split_[S] = std::move(subs);
+    max_split_ = S;
+  }
   usable_ = true;
   why_.clear();
   return true;
 }
+
+// Depth at which a launch over n points is split: the deepest S with
+// tiles x column blocks x 2^S CTAs still within one wave of the SMs
+// (DDSG_SLOT_SPLIT=0 disables; A/B switch).
+int FastHdmr::split_levels(int64_t n) const {
+  static const bool enabled = [] {
+    const char* e = std::getenv("DDSG_SLOT_SPLIT");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!enabled || max_split_ == 0 || n <= 0) return 0;
+  static thread_local int sms[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  if (sms[dev] == 0 && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  const int64_t ctas = (n + kPoints - 1) / kPoints * n_cb_;
+  // cheapest depth within one wave of CTAs: ~5 us per sub-launch (fork, launch,
+  // join) against ~2 us per slot a CTA walks (profiles/r2_split_latency.jsonl)
+  int best = 0;
+  double best_us = kSlotUs * n_blocks_;
+  for (int S = 1; S <= max_split_ && (ctas << S) <= sms[dev]; ++S) {
+    const double us = kSubLaunchUs * (1 << S) + kSlotUs * ((n_blocks_ + (1 << S) - 1) >> S);
+    if (us < best_us) {
+      best_us = us;
+      best = S;
+    }
+  }
+  return best;
+}
+
+// Rough device time of a launch over n points that takes the split path (0
+// when it would not): lets the caller choose between this and the
+// small-batch path.
+double FastHdmr::split_cost_us(int64_t n) const {
+  const int S = split_levels(n);
+  if (S == 0) return 0.0;
+  return 40.0 + kSubLaunchUs * (1 << S) + kSlotUs * ((n_blocks_ + (1 << S) - 1) >> S);
+}
+
+size_t FastHdmr::scratch_bytes(int64_t n) const {
+  const size_t xt = static_cast<size_t>(n) * d_ * 8;
+  const int S = split_levels(n);
+  return S == 0 ? xt : (xt + 255) / 256 * 256 + (size_t{1} << S) * static_cast<size_t>(n) * m_ * 8;
+}
+
+namespace {
+// Streams and events of a split launch, per host thread and device.
+struct SplitStreams {
+  cudaStream_t s[1 << FastHdmr::kMaxSplitPublic] = {};
+  cudaEvent_t fork = nullptr, join[1 << FastHdmr::kMaxSplitPublic] = {};
+  bool ready = false;
+  void init() {
+    if (ready) return;
+    DDSG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (auto& st : s) DDSG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : join) DDSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ready = true;
+  }
+};
+SplitStreams& split_streams() {
+  static thread_local SplitStreams per_dev[64];
+  int dev = 0;
+  DDSG_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) fail(DDSG_CUDA_ERROR, "device ordinal out of range");
+  per_dev[dev].init();
+  return per_dev[dev];
+}
+
+// y[p][c] = the pairwise sum of the 2^S subtree roots part[k][p][c], k in tree order.
+template <int kExactUnused>
+__global__ void split_combine_kernel(const double* __restrict__ part, int64_t outs, int S, double* __restrict__ y) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= outs) return;
+  double v[1 << FastHdmr::kMaxSplitPublic];
+  const int K = 1 << S;
+#pragma unroll
+  for (int k = 0; k < (1 << FastHdmr::kMaxSplitPublic); ++k) v[k] = k < K ? part[static_cast<int64_t>(k) * outs + i] : 0.0;
+#pragma unroll
+  for (int w = 1; w < (1 << FastHdmr::kMaxSplitPublic); w <<= 1)
+    if (w < K) {
+#pragma unroll
+      for (int k = 0; k < (1 << FastHdmr::kMaxSplitPublic); k += 2 * w) v[k] = __dadd_rn(v[k], v[k + w]);
+    }
+  y[i] = v[0];
+}
+}  // namespace
 
 int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, double* y,
                          unsigned long long* bad, double* xt, cudaStream_t st) const {
@@ -376,6 +505,36 @@ int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, do
   dim3 tgrid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((d_ + 31) / 32));
   transpose_check_kernel<<<tgrid, dim3(32, 8), 0, st>>>(x, n, d_, base, xt, bad);
   DDSG_CUDA(cudaGetLastError());
+  if (const int S = split_levels(n); S > 0) {
+    // a few tiles only: the subtrees of depth S as concurrent launches
+    const int K = 1 << S;
+    const int64_t tiles_s = (n + kPoints - 1) / kPoints;
+    double* part = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(xt) +
+                                             (static_cast<size_t>(n) * d_ * 8 + 255) / 256 * 256);
+    const int lv = levels_ - S;
+    const int64_t deep_b = std::min(std::max(0, levels_ - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
+    const size_t smem_s = kHeaderBytes + n_stages_ * block_bytes_ + deep_b + has_carry_ * size_t{kCols} * kPoints * 8 +
+                          (2 * kSlotDims * static_cast<size_t>(n_blocks_) + 15) / 16 * 16;
+    SplitStreams& ss = split_streams();
+    kernel_timer().begin(st);
+    DDSG_CUDA(cudaEventRecord(ss.fork, st));
+    DDSG_CUDA(instance_attr(exact)(static_cast<int>(smem_s)));
+    for (int k = 0; k < K; ++k) {
+      const SubTree& t = split_[S][static_cast<size_t>(k)];
+      DDSG_CUDA(cudaStreamWaitEvent(ss.s[k], ss.fork, 0));
+      const KernelArgs args{static_cast<const unsigned char*>(blocks_), t.off, t.len, slot_dims_ + kSlotDims * t.first,
+                            t.count, n_cb_, n_cb_, lv, xt, n, m_, part + static_cast<int64_t>(k) * n * m_,
+                            block_bytes_, n_stages_};
+      instance_launch(exact)(dim3(static_cast<unsigned>(tiles_s * n_cb_)), smem_s, ss.s[k], args);
+      DDSG_CUDA(cudaEventRecord(ss.join[k], ss.s[k]));
+      DDSG_CUDA(cudaStreamWaitEvent(st, ss.join[k], 0));
+    }
+    const int64_t outs = n * m_;
+    split_combine_kernel<0><<<static_cast<unsigned>((outs + 255) / 256), 256, 0, st>>>(part, outs, S, y);
+    kernel_timer().end(st);
+    DDSG_CUDA(cudaGetLastError());
+    return 2 + K;
+  }
   const int64_t tiles = (n + kPoints - 1) / kPoints;
   const int64_t deep_bytes = std::min(std::max(0, levels_ - kTmemLevels), kSmemLevels) * int64_t{kCols} * kPoints * 8;
   const size_t smem = kHeaderBytes + n_stages_ * block_bytes_ + deep_bytes + has_carry_ * size_t{kCols} * kPoints * 8 +

@@ -128,6 +128,13 @@ class FastHdmr {
   // Returns the number of kernel launches.
   int64_t launch(int exact, const double* x, int64_t n, int64_t base, double* y, unsigned long long* bad,
                  double* xt, cudaStream_t st) const;
+  // Bytes of the device scratch `xt` a launch over n points needs: the
+  // dim-major points, plus the subtree partial sums of a split launch.
+  size_t scratch_bytes(int64_t n) const;
+  // Subtree split of a launch over n points (0 = one launch walks every slot).
+  int split_levels(int64_t n) const;
+  double split_cost_us(int64_t n) const;
+  static constexpr double kSubLaunchUs = 5.0, kSlotUs = 2.0;  // split cost model (measured, B200)
   int dim() const { return d_; }
   std::string why_not() const { return why_; }
 
@@ -143,6 +150,25 @@ class FastHdmr {
   int64_t* block_off_ = nullptr;  // device: [n_cb * n_active] byte offsets
   int32_t* block_len_ = nullptr;  // device: [n_cb * n_active] byte lengths
   int16_t* slot_dims_ = nullptr;  // device: [n_blocks][kSlotDims] point dims per block
+
+  // Mid-size batches (a few tiles: fewer CTAs than SMs, every CTA walking all
+  // slots one after another): the pairwise tree is cut at depth S and the 2^S
+  // subtrees run as concurrent launches over their own block ranges of the
+  // SAME staged tables (the kernel ignores tree-position bits >= its level
+  // count, so a subtree's root comes out where the full launch writes y);
+  // split_combine_kernel adds the subtree roots in tree order.  Bit-identical
+  // to the single launch: same leaves, same merges.
+  struct SubTree {
+    int first = 0, count = 0;       // block range
+    int64_t* off = nullptr;         // device: [n_cb][count] byte offsets into blocks_
+    int32_t* len = nullptr;         // device: [n_cb][count]
+  };
+  static constexpr int kMaxSplit = 4;
+ public:
+  static constexpr int kMaxSplitPublic = kMaxSplit;
+ private:
+  std::vector<SubTree> split_[kMaxSplit + 1];  // [S]: 2^S subtrees (empty: depth S not splittable)
+  int max_split_ = 0;
 };
 
 }  // namespace ddsg_b200

@@ -318,3 +318,51 @@ def test_small_batch_domain_error_lowest_index():
     with pytest.raises(DomainError) as e:
         vec.evaluate_batch(x)
     assert e.value.task_id == 5
+
+
+# ------------------------------------- mid-size batches (a few point tiles)
+# Fewer CTAs than SMs: the pairwise tree is cut at depth S and its 2^S
+# subtrees run as concurrent launches over their own block ranges, the
+# subtree roots added in tree order (fast_hdmr.cuh).  Same leaves, same
+# merges: bit-identical, checked against the oracle; the launch count shows
+# the split was taken.
+
+@pytest.mark.parametrize("n", [257, 300, 513, 1300, 2100])
+@pytest.mark.parametrize("case", ["modes", "b_kinds", "nonfinite", "deep_tree", "order3", "wide"])
+def test_mid_batches_split_bit_exact(case, n):
+    from paper_2202_06555_b200.ddsg import last_eval_stats
+
+    if case == "modes":
+        d, m = 6, 23
+        vec, fa, so = make(d, m, family_1d_2d(d, [(0, 1), (1, 2), (2, 5), (3, 4)]), {1: 6, 2: 4},
+                           mode=ZERO_BOUNDARY, seed=n)
+    elif case == "b_kinds":
+        d, m = 4, 7
+        vec, fa, so = make(d, m, family_1d_2d(d, [(0, 1), (2, 3)]), {1: 5, 2: 3}, b=[5, 1, -1, 2, -3, 1, 0])
+    elif case == "nonfinite":
+        d, m = 4, 3
+        vec, fa, so = make(d, m, family_1d_2d(d, [(0, 1)]), {1: 5, 2: 3}, poison=((0, 1), 7, 1, np.inf))
+    elif case == "deep_tree":
+        d, m = 60, 3
+        rng = np.random.default_rng(1)
+        pairs = set()
+        while len(pairs) < 200:
+            a, b = sorted(rng.choice(d, 2, replace=False).tolist())
+            pairs.add((a, b))
+        vec, fa, so = make(d, m, family_1d_2d(d, pairs), {1: 3, 2: 2})
+    elif case == "order3":
+        d, m = 5, 9
+        fam = [()] + [(j,) for j in range(d)] + [(0, 1), (0, 2), (1, 2), (3, 4)] + [(0, 1, 2)]
+        vec, fa, so = make(d, m, fam, {1: 5, 2: 3, 3: 3})
+    else:  # many slots and many column blocks: the split depth shrinks with the CTA count
+        d, m = 40, 70
+        vec, fa, so = make(d, m, family_1d_2d(d, [(j, j + 1) for j in range(0, 40, 2)] + [(0, 39), (5, 30)]),
+                           {1: 4, 2: 3})
+    assert vec.uses_slot_kernel()
+    x = pts(d, n, seed=n)
+    check(vec, d, m, fa, so, x, nan_ok=case == "nonfinite")
+    vec.evaluate_batch(x)
+    launches = last_eval_stats()[0]
+    tiles, n_cb = -(-n // 512), -(-m // 8)
+    if tiles * n_cb * 2 <= 148 and len(so) >= 64:  # (few slots: one launch is cheaper than the fork/join)
+        assert launches > 2, (launches, tiles, n_cb)  # transpose + 2^S subtrees + combine
