@@ -428,13 +428,19 @@ int FastHdmr::split_levels(int64_t n) const {
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
   if (sms[dev] == 0 && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   const int64_t ctas = (n + kPoints - 1) / kPoints * n_cb_;
-  // cheapest depth within one wave of CTAs: ~5 us per sub-launch (fork, launch,
-  // join) against ~2 us per slot a CTA walks (profiles/r2_split_latency.jsonl)
+  if (ctas > 16 * static_cast<int64_t>(sms[dev])) return 0;  // many waves: the tail is already small
+  // cheapest depth: waves of CTAs (one CTA per SM) x ~2 us per slot a CTA
+  // walks, plus ~5 us per sub-launch (fork, launch, join)
+  // (profiles/r2_split_latency.jsonl).  Shorter CTAs also fill the last wave:
+  // 4,096 points x 19 column blocks are 152 CTAs, two waves unsplit.
   int best = 0;
-  double best_us = kSlotUs * n_blocks_;
-  for (int S = 1; S <= max_split_ && (ctas << S) <= sms[dev]; ++S) {
-    const double us = kSubLaunchUs * (1 << S) + kSlotUs * ((n_blocks_ + (1 << S) - 1) >> S);
-    if (us < best_us) {
+  double best_us = 0.0;
+  for (int S = 0; S <= max_split_; ++S) {
+    if (S > 0 && (static_cast<size_t>(n) * m_ * 8) << S > (size_t{256} << 20)) break;  // partial sums <= 256 MiB
+    const int64_t waves = ((ctas << S) + sms[dev] - 1) / sms[dev];
+    const double us = static_cast<double>(waves) * kSlotUs * ((n_blocks_ + (1 << S) - 1) >> S) +
+                      (S > 0 ? kSubLaunchUs * (1 << S) : 0.0);
+    if (S == 0 || us < best_us) {
       best_us = us;
       best = S;
     }
@@ -448,7 +454,11 @@ int FastHdmr::split_levels(int64_t n) const {
 double FastHdmr::split_cost_us(int64_t n) const {
   const int S = split_levels(n);
   if (S == 0) return 0.0;
-  return 40.0 + kSubLaunchUs * (1 << S) + kSlotUs * ((n_blocks_ + (1 << S) - 1) >> S);
+  int dev = 0, sm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ctas = (n + kPoints - 1) / kPoints * n_cb_;
+  const int64_t waves = ((ctas << S) + sm - 1) / sm;
+  return 40.0 + kSubLaunchUs * (1 << S) + static_cast<double>(waves) * kSlotUs * ((n_blocks_ + (1 << S) - 1) >> S);
 }
 
 size_t FastHdmr::scratch_bytes(int64_t n) const {
