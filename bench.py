@@ -349,10 +349,11 @@ def run_ours(args, rank, world, local_rank, dist):
         except Exception:
             hbm_tbs = 6.55  # B200_PROFILING.md fallback
         roofline["traffic_note"] = (
-            "DRAM traffic is %.1fx the algorithmic bytes (mostly L2 misses on point coordinates: a CTA re-reads "
-            "each dim's coordinates for the ~2.7 slots that use it, and the tiles in flight hold 178 MB of them) at "
-            "%.2f TB/s of %.2f; the kernel is not HBM-bound: its time is flat while column-block grouping and L2 "
-            "persisting windows vary DRAM reads 2.7x (profiles/r1_l2_budget_sweep_config5.json)"
+            "DRAM traffic is %.1fx the algorithmic bytes: 12.0 of 14.4 GB per launch are point coordinates (4 "
+            "column-block groups x the 2.7 slots per dim a CTA evaluates ~0.5 ms apart, no L2 reuse between them), 2.4 "
+            "GB staged tables (profiles/r2_l2_hints_config5.json, tables-only build), at %.2f TB/s of %.2f; the kernel "
+            "is not HBM-bound: its time is flat while DRAM reads vary 2.7x with the grouping "
+            "(profiles/r1_l2_budget_sweep_config5.json)"
             % (traffic / alg_bytes, traffic / (kernel_ms / 1e3) / 1e12, hbm_tbs))
     roofline["binding_resource"] = {
         "resource": "shared-memory gather: 16 surplus doubles/clk/SM (LDS pipe, 128 B/clk/SM)",

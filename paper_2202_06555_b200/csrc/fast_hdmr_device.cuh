@@ -844,7 +844,13 @@ __global__ void __launch_bounds__(kPoints, 1)
                                             : static_cast<uint32_t>((tid & 7) << 4);
   const int64_t p = static_cast<int64_t>(tile) * kPoints + tid;
   const bool valid = p < n;
+#ifdef DDSG_SLOT_DEBUG_SAMEX
+  // measurement only (wrong results): every tile reads tile 0's coordinates,
+  // so the kernel's DRAM reads are its staged tables alone
+  const int64_t pc = tid < n ? tid : n - 1;
+#else
   const int64_t pc = valid ? p : n - 1;
+#endif
   const int64_t* offs = block_off + static_cast<int64_t>(cb) * n_active;
   const int32_t* lens = block_len + static_cast<int64_t>(cb) * n_active;
 
