@@ -552,35 +552,40 @@ struct DdsgOptions {  // hdmr.hpp:166-175 (only the fields evaluation uses matte
 
 using Evaluator = std::function<void(std::span<const double>, std::span<double>)>;  // hdmr.hpp:40
 
-// component_index.hpp:57-72: the order-k index sets of {0..d-1}, lexicographic.
+// component_index.hpp:57-72: the order-k index sets of {0..d-1} in
+// lexicographic order -- here as the permutations of a k-of-d selection mask
+// (std::prev_permutation walks the masks from 1..10..0 downwards, which lists
+// the selected positions lexicographically upwards).
 inline std::vector<ComponentIndex> order_k_indices(int d, std::size_t k) {
   std::vector<ComponentIndex> all;
-  if (k > static_cast<std::size_t>(d)) return all;
-  std::vector<int> c(k);
-  for (std::size_t i = 0; i < k; ++i) c[i] = static_cast<int>(i);
-  for (;;) {
-    all.push_back(ComponentIndex{c});
-    std::size_t i = k;  // rightmost position that can still advance
-    while (i > 0 && c[i - 1] == d - static_cast<int>(k - i) - 1) --i;
-    if (i == 0) return all;
-    ++c[i - 1];
-    for (std::size_t j = i; j < k; ++j) c[j] = c[j - 1] + 1;
-  }
+  if (d < 0 || k > static_cast<std::size_t>(d)) return all;
+  std::vector<char> pick(static_cast<std::size_t>(d), 0);
+  std::fill(pick.begin(), pick.begin() + static_cast<std::ptrdiff_t>(k), 1);
+  do {
+    ComponentIndex u;
+    u.dims.reserve(k);
+    for (int j = 0; j < d; ++j)
+      if (pick[static_cast<std::size_t>(j)]) u.dims.push_back(j);
+    all.push_back(std::move(u));
+  } while (std::prev_permutation(pick.begin(), pick.end()));
+  return all;
 }
 
-// component_index.hpp:75-87: every subset of u, in (order, lex) order.
+// component_index.hpp:75-87: every subset of u in (order, lex) order: each
+// dim of u doubles the family built so far (with / without it), then sorted.
 inline std::vector<ComponentIndex> all_subsets(const ComponentIndex& u) {
-  const std::size_t k = u.order();
-  std::vector<ComponentIndex> subs;
-  subs.reserve(std::size_t{1} << k);
-  for (std::size_t mask = 0; mask < (std::size_t{1} << k); ++mask) {
-    ComponentIndex v;
-    for (std::size_t j = 0; j < k; ++j)
-      if (mask & (std::size_t{1} << j)) v.dims.push_back(u.dims[j]);
-    subs.push_back(std::move(v));
+  std::vector<ComponentIndex> family(1);  // the empty index
+  family.reserve(std::size_t{1} << u.order());
+  for (int dim : u.dims) {
+    const std::size_t have = family.size();
+    for (std::size_t i = 0; i < have; ++i) {
+      ComponentIndex with = family[i];
+      with.dims.push_back(dim);  // u.dims ascend, so every member stays sorted
+      family.push_back(std::move(with));
+    }
   }
-  std::sort(subs.begin(), subs.end());
-  return subs;
+  std::sort(family.begin(), family.end());
+  return family;
 }
 
 struct ExpansionDiagnostics {  // hdmr.hpp:178-186
@@ -628,33 +633,39 @@ inline double eta_coefficient(const std::vector<double>& component_quadrature,
 // of n_samples uniform draws (std::mt19937_64(seed)); lowest index on ties.
 inline AnchorPoint select_anchor(const Evaluator& f, int dim, int out_dim, int n_samples, std::uint64_t seed) {
   if (n_samples < 1) throw std::invalid_argument("select_anchor: n_samples must be >= 1");
-  std::mt19937_64 rng(seed);
-  std::uniform_real_distribution<double> unif(0.0, 1.0);
-  const std::size_t m = static_cast<std::size_t>(out_dim), n = static_cast<std::size_t>(n_samples);
-  std::vector<std::vector<double>> pts(n, std::vector<double>(static_cast<std::size_t>(dim)));
-  std::vector<std::vector<double>> vals(n, std::vector<double>(m));
-  std::vector<double> mean(m, 0.0);
-  for (std::size_t i = 0; i < n; ++i) {
-    for (double& c : pts[i]) c = unif(rng);
-    f(pts[i], vals[i]);
-    for (std::size_t c = 0; c < m; ++c) {
-      if (!std::isfinite(vals[i][c]))
-        throw build_error("select_anchor: evaluator returned a non-finite value", pts[i]);
-      mean[c] += vals[i][c];
+  struct Sample {
+    std::vector<double> x, fx;
+  };
+  std::mt19937_64 engine(seed);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  std::vector<Sample> draws(static_cast<std::size_t>(n_samples));
+  std::vector<double> center(static_cast<std::size_t>(out_dim), 0.0);  // sums in sample order, then / n
+  for (Sample& s : draws) {
+    s.x.resize(static_cast<std::size_t>(dim));
+    std::generate(s.x.begin(), s.x.end(), [&] { return unit(engine); });
+    s.fx.resize(center.size());
+    f(s.x, s.fx);
+    for (std::size_t c = 0; c < center.size(); ++c) {
+      if (!std::isfinite(s.fx[c])) throw build_error("select_anchor: evaluator returned a non-finite value", s.x);
+      center[c] += s.fx[c];
     }
   }
-  for (double& c : mean) c /= static_cast<double>(n_samples);
+  for (double& c : center) c /= static_cast<double>(n_samples);
+  auto l1_to_center = [&](const Sample& s) {
+    double dist = 0.0;
+    for (std::size_t c = 0; c < center.size(); ++c) dist += std::abs(s.fx[c] - center[c]);
+    return dist;
+  };
+  // the first strict minimum: ties go to the lowest sample index; a sample
+  // whose distance is not below +inf (a NaN) can only win as sample 0
   std::size_t best = 0;
   double best_dist = std::numeric_limits<double>::infinity();
-  for (std::size_t i = 0; i < n; ++i) {
-    double dist = 0.0;
-    for (std::size_t c = 0; c < m; ++c) dist += std::abs(vals[i][c] - mean[c]);
-    if (dist < best_dist) {
-      best_dist = dist;
+  for (std::size_t i = 0; i < draws.size(); ++i)
+    if (const double dist = l1_to_center(draws[i]); dist < best_dist) {
       best = i;
+      best_dist = dist;
     }
-  }
-  return AnchorPoint{std::move(pts[best]), std::move(vals[best])};
+  return AnchorPoint{std::move(draws[best].x), std::move(draws[best].fx)};
 }
 
 // hdmr.hpp:81-93: f restricted to the cut through the anchor along the dims of u.
@@ -666,6 +677,10 @@ inline Evaluator cut_evaluator(const Evaluator& f, const AnchorPoint& anchor, co
     f(x, out);
   };
 }
+
+class DdsgFunction;
+inline DdsgFunction decompose(const Evaluator& f, int dim, int out_dim, const AnchorPoint& anchor, const DdsgOptions& opt,
+                       ExpansionDiagnostics* diag = nullptr);
 
 class DdsgFunction {  // hdmr.hpp:195-356
  public:
@@ -729,35 +744,39 @@ class DdsgFunction {  // hdmr.hpp:195-356
   }
   std::size_t order_reached() const { return order_reached_; }
 
-  // hdmr.hpp:257-270: the telescopic double sum without deduplication, one
-  // cut interpolation per (u, v subset of u) -- the vectorized form's oracle.
+  // hdmr.hpp:257-270: the telescopic double sum without deduplication -- for
+  // every accepted u, every subset v of u contributes (-1)^(|u|-|v|) times the
+  // cut interpolant of v, evaluated anew each time (the vectorized form's
+  // oracle; terms are added in (u, v) order).
   void evaluate_naive(std::span<const double> x, std::span<double> out, std::uint64_t* interp_calls = nullptr) const {
     check_point(x);
-    const std::size_t m = static_cast<std::size_t>(out_dim_);
-    for (std::size_t c = 0; c < m; ++c) out[c] = anchor_.f_anchor[c];
-    std::vector<double> term(m), y;
-    for (const auto& [u, grid] : accepted_)
-      for (const auto& v : all_subsets(u)) {
-        const double sign = ((u.order() - v.order()) % 2 == 0) ? 1.0 : -1.0;
-        evaluate_cut(v, x, y, term, interp_calls);
-        for (std::size_t c = 0; c < m; ++c) out[c] += sign * term[c];
+    std::copy(anchor_.f_anchor.begin(), anchor_.f_anchor.end(), out.begin());  // the u = {} term
+    std::vector<double> term(anchor_.f_anchor.size()), restricted;
+    for (const auto& entry : accepted_) {
+      const ComponentIndex& u = entry.first;
+      for (const ComponentIndex& v : all_subsets(u)) {
+        evaluate_cut(v, x, restricted, term, interp_calls);
+        const bool minus = ((u.order() - v.order()) & 1u) != 0u;
+        for (std::size_t c = 0; c < term.size(); ++c) out[c] += minus ? -1.0 * term[c] : 1.0 * term[c];
       }
+    }
   }
   std::vector<double> evaluate_naive(std::span<const double> x) const {  // hdmr.hpp:272-276
     std::vector<double> out(static_cast<std::size_t>(out_dim_));
     evaluate_naive(x, out);
     return out;
   }
-  // hdmr.hpp:280-297: the cut interpolant of an accepted index at x restricted to its dims.
+  // hdmr.hpp:280-297: the cut interpolant of an accepted index at x restricted
+  // to its dims (the anchor value for the empty index; counted otherwise).
   void evaluate_cut(const ComponentIndex& v, std::span<const double> x, std::vector<double>& restricted_scratch,
                     std::span<double> out, std::uint64_t* interp_calls = nullptr) const {
     if (v.empty()) {
-      for (std::size_t c = 0; c < static_cast<std::size_t>(out_dim_); ++c) out[c] = anchor_.f_anchor[c];
+      std::copy(anchor_.f_anchor.begin(), anchor_.f_anchor.end(), out.begin());
       return;
     }
-    restricted_scratch.resize(v.order());
-    for (std::size_t j = 0; j < v.order(); ++j) restricted_scratch[j] = x[static_cast<std::size_t>(v.dims[j])];
-    if (interp_calls) ++*interp_calls;
+    restricted_scratch.clear();
+    for (int j : v.dims) restricted_scratch.push_back(x[static_cast<std::size_t>(j)]);
+    if (interp_calls != nullptr) *interp_calls += 1;
     accepted_.at(v).interpolate(restricted_scratch, out);
   }
 
@@ -812,117 +831,122 @@ class DdsgFunction {  // hdmr.hpp:195-356
   }
 };
 
-// hdmr.hpp:364-483: the adaptive decomposition.  Per order k the index set is
-// the order-k indices that contain no rejected index; their cut grids are
-// built (here on opt.workers host threads, one component at a time each --
-// results do not depend on the schedule), eta prunes within the order
-// (order 1 is always kept), rho decides whether order k+1 is built.  Grids,
-// quadratures, eta, rho, the accepted / rejected sets and b are bit-identical
-// to the reference's (tests/cpp/test_ref_dropin.cpp).  exact_cuts is not
-// supported.
+namespace detail {
+// The cut grids of one expansion order, built on `workers` host threads
+// (an atomic work queue; a component's result does not depend on the
+// schedule).  The lowest failing component reports, as
+// "decompose: component {..} failed: <cause>" (hdmr.hpp:425-429).
+struct CutBuild {
+  SparseGridFunction grid;
+  std::vector<double> quadrature;
+};
+inline std::vector<CutBuild> build_cuts(const Evaluator& f, const AnchorPoint& anchor,
+                                        const std::vector<ComponentIndex>& wave, int out_dim,
+                                        const DdsgOptions& opt) {
+  std::vector<CutBuild> cuts(wave.size());
+  std::vector<std::string> failure(wave.size());
+  std::vector<char> failed(wave.size(), 0);
+  SgBuildOptions grid_opt;
+  grid_opt.max_level = opt.max_level;
+  grid_opt.eps_gamma = opt.eps_gamma;
+  grid_opt.mode = opt.mode;
+  std::atomic<std::size_t> queue{0};
+  auto drain = [&] {
+    for (std::size_t id; (id = queue.fetch_add(1)) < wave.size();) try {
+        cuts[id].grid = SparseGridFunction::build(cut_evaluator(f, anchor, wave[id]),
+                                                  static_cast<int>(wave[id].order()), out_dim, grid_opt);
+        cuts[id].quadrature = cuts[id].grid.quadrature();
+      } catch (const std::exception& e) {
+        failed[id] = 1;
+        failure[id] = e.what();
+      } catch (...) {  // nothing may leave a pool thread
+        failed[id] = 1;
+        failure[id] = "unknown error";
+      }
+  };
+  std::vector<std::thread> pool;
+  for (std::size_t t = 1; t < std::min<std::size_t>(std::max(1u, opt.workers), wave.size()); ++t) pool.emplace_back(drain);
+  drain();
+  for (std::thread& t : pool) t.join();
+  for (std::size_t id = 0; id < wave.size(); ++id)
+    if (failed[id]) throw std::runtime_error("decompose: component " + wave[id].to_string() + " failed: " + failure[id]);
+  return cuts;
+}
+}  // namespace detail
+
+// hdmr.hpp:364-483: the adaptive decomposition, order by order.  The wave of
+// order k is every order-k index without a rejected subset; its cut grids
+// are built (detail::build_cuts), eta screens the wave against the
+// cumulative quadrature of the lower orders (order 1 is always kept; eps_eta
+// = 0 keeps everything), and rho -- the relative change of the cumulative
+// quadrature -- ends the expansion.  Grids, quadratures, eta, rho, the
+// accepted / rejected sets and b are bit-identical to the reference's
+// (tests/cpp/test_ref_dropin.cpp).  exact_cuts is not supported.
 inline DdsgFunction decompose(const Evaluator& f, int dim, int out_dim, const AnchorPoint& anchor,
-                              const DdsgOptions& opt, ExpansionDiagnostics* diag = nullptr) {
+                              const DdsgOptions& opt, ExpansionDiagnostics* diag) {
   if (dim < 1) throw std::invalid_argument("decompose: dim must be >= 1");
-  if (opt.k_max < 1 || opt.k_max > dim)
-    throw std::invalid_argument("decompose: k_max must satisfy 1 <= k_max <= dim");
+  if (opt.k_max < 1 || opt.k_max > dim) throw std::invalid_argument("decompose: k_max must satisfy 1 <= k_max <= dim");
   if (opt.eps_rho < 0.0 || opt.eps_eta < 0.0) throw std::invalid_argument("decompose: thresholds must be >= 0");
-  if (anchor.coords.size() != static_cast<std::size_t>(dim))
-    throw std::invalid_argument("decompose: anchor dimension mismatch");
+  if (anchor.coords.size() != static_cast<std::size_t>(dim)) throw std::invalid_argument("decompose: anchor dimension mismatch");
   if (opt.exact_cuts) throw std::invalid_argument("decompose: exact_cuts is not supported by the B200 drop-in");
 
-  DdsgFunction out;
-  out.dim_ = dim;
-  out.out_dim_ = out_dim;
-  out.opt_ = opt;
-  out.anchor_ = anchor;
-  if (out.anchor_.f_anchor.empty()) {
-    out.anchor_.f_anchor.resize(static_cast<std::size_t>(out_dim));
-    f(out.anchor_.coords, out.anchor_.f_anchor);
+  DdsgFunction fn;
+  fn.dim_ = dim;
+  fn.out_dim_ = out_dim;
+  fn.opt_ = opt;
+  fn.anchor_ = anchor;
+  if (fn.anchor_.f_anchor.empty()) {  // the anchor value, if the caller did not bring it
+    fn.anchor_.f_anchor.assign(static_cast<std::size_t>(out_dim), 0.0);
+    f(fn.anchor_.coords, fn.anchor_.f_anchor);
   }
-  out.cut_quadratures_[ComponentIndex{}] = out.anchor_.f_anchor;
+  fn.cut_quadratures_.emplace(ComponentIndex{}, fn.anchor_.f_anchor);
 
-  for (int k = 1; k <= opt.k_max; ++k) {
-    std::vector<ComponentIndex> current;
-    for (auto& u : order_k_indices(dim, static_cast<std::size_t>(k))) {
-      const bool pruned = std::any_of(out.rejected_.begin(), out.rejected_.end(),
-                                      [&](const ComponentIndex& z) { return u.is_superset_of(z); });
-      if (!pruned) current.push_back(std::move(u));
-    }
-    if (current.empty()) break;
+  const auto has_rejected_subset = [&fn](const ComponentIndex& u) {
+    return std::any_of(fn.rejected_.begin(), fn.rejected_.end(),
+                       [&u](const ComponentIndex& z) { return u.is_superset_of(z); });
+  };
+  for (std::size_t order = 1; order <= static_cast<std::size_t>(opt.k_max); ++order) {
+    std::vector<ComponentIndex> wave = order_k_indices(dim, order);
+    wave.erase(std::remove_if(wave.begin(), wave.end(), has_rejected_subset), wave.end());
+    if (wave.empty()) break;
+    std::vector<detail::CutBuild> cuts = detail::build_cuts(f, fn.anchor_, wave, out_dim, opt);
 
-    // cut grids of this order: independent builds, the lowest failing component reports
-    std::vector<SparseGridFunction> grids(current.size());
-    std::vector<std::vector<double>> quads(current.size());
-    std::vector<std::string> failure(current.size());
-    std::vector<char> failed(current.size(), 0);
-    std::atomic<std::size_t> next{0};
-    auto worker = [&] {
-      for (std::size_t id = next.fetch_add(1); id < current.size(); id = next.fetch_add(1)) {
-        try {
-          SgBuildOptions sgo;
-          sgo.max_level = opt.max_level;
-          sgo.eps_gamma = opt.eps_gamma;
-          sgo.mode = opt.mode;
-          grids[id] = SparseGridFunction::build(cut_evaluator(f, out.anchor_, current[id]),
-                                                static_cast<int>(current[id].order()), out_dim, sgo);
-          quads[id] = grids[id].quadrature();
-        } catch (const std::exception& e) {
-          failed[id] = 1;
-          failure[id] = e.what();
-        } catch (...) {  // never let an exception leave a pool thread
-          failed[id] = 1;
-          failure[id] = "unknown error";
-        }
-      }
-    };
-    {
-      const std::size_t nthreads = std::min<std::size_t>(std::max(1u, opt.workers), current.size());
-      std::vector<std::thread> pool;
-      for (std::size_t t = 1; t < nthreads; ++t) pool.emplace_back(worker);
-      worker();
-      for (auto& t : pool) t.join();
-    }
-    for (std::size_t id = 0; id < current.size(); ++id)
-      if (failed[id])
-        throw std::runtime_error("decompose: component " + current[id].to_string() + " failed: " + failure[id]);
-
-    // order boundary: eta within the order, then the bookkeeping
-    const auto lower_sum = out.cumulative_quadrature(static_cast<std::size_t>(k) - 1);
-    if (diag && diag->eta_by_order.size() < static_cast<std::size_t>(k))
-      diag->eta_by_order.resize(static_cast<std::size_t>(k));
-    for (std::size_t id = 0; id < current.size(); ++id) {
-      const ComponentIndex& u = current[id];
-      out.cut_quadratures_[u] = quads[id];
-      bool accept = true;
+    const std::vector<double> below = fn.cumulative_quadrature(order - 1);  // orders < k, before this wave
+    std::vector<ExpansionDiagnostics::EtaRecord> screened;
+    for (std::size_t id = 0; id < wave.size(); ++id) {
+      const ComponentIndex& u = wave[id];
+      fn.cut_quadratures_[u] = std::move(cuts[id].quadrature);  // component_quadrature(u) reads it
       double eta = std::numeric_limits<double>::quiet_NaN();
-      if (u.order() >= 2) {
-        eta = eta_coefficient(out.component_quadrature(u), lower_sum);
-        accept = opt.eps_eta == 0.0 || eta > opt.eps_eta;
+      bool keep = true;
+      if (order >= 2) {
+        eta = eta_coefficient(fn.component_quadrature(u), below);
+        keep = opt.eps_eta == 0.0 || eta > opt.eps_eta;
+        screened.push_back({u, eta, keep});
       }
-      if (accept) {
-        out.accepted_[u] = std::move(grids[id]);
+      if (keep) {
+        fn.accepted_[u] = std::move(cuts[id].grid);
       } else {
-        out.rejected_.insert(u);
-        out.cut_quadratures_.erase(u);
+        fn.cut_quadratures_.erase(u);
+        fn.rejected_.insert(u);
       }
-      if (diag && u.order() >= 2) diag->eta_by_order[static_cast<std::size_t>(k) - 1].push_back({u, eta, accept});
     }
-    out.order_reached_ = static_cast<std::size_t>(k);
+    fn.order_reached_ = order;
+    if (diag) {
+      if (diag->eta_by_order.size() < order) diag->eta_by_order.resize(order);
+      auto& slot = diag->eta_by_order[order - 1];
+      slot.insert(slot.end(), screened.begin(), screened.end());
+    }
 
-    const auto cum_k = out.cumulative_quadrature(static_cast<std::size_t>(k));
-    double rho = std::numeric_limits<double>::quiet_NaN();
-    bool stop = false;
+    double rho = std::numeric_limits<double>::quiet_NaN();  // stays NaN on a zero denominator: no evidence, go on
     try {
-      rho = expansion_rho(cum_k, lower_sum);
-      stop = rho < opt.eps_rho;
+      rho = expansion_rho(fn.cumulative_quadrature(order), below);
     } catch (const rho_denominator_error&) {
-      stop = false;  // no evidence of convergence: keep expanding
     }
     if (diag) diag->rho_by_order.push_back(rho);
-    if (stop) break;
+    if (rho < opt.eps_rho) break;  // false for NaN
   }
-  out.finalize_coefficients();
-  return out;
+  fn.finalize_coefficients();
+  return fn;
 }
 
 // Reusable evaluation buffers (ddsg_eval.hpp:21-24): pinned host staging,
