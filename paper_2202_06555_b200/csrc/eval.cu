@@ -935,6 +935,37 @@ int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, i
   const int64_t bytes_per_pt = static_cast<int64_t>(d + m) * 8;
   const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(1024, (int64_t{64} << 20) / bytes_per_pt));
   const int64_t nchunks = (n + chunk - 1) / chunk;
+  if (nchunks == 1) {
+    // One chunk (the per-point and small-batch callers): one stream, and the
+    // lowest-bad-index flag rides behind the outputs -- one D2H copy and one
+    // wait instead of the two-stream pipeline's events and a second copy.
+    const size_t xb = static_cast<size_t>(n) * d * 8, yb = static_cast<size_t>(n) * m * 8;
+    ws.hx[0].get(xb);
+    ws.hy[0].get(yb + 8);
+    ws.dx[0].get(xb);
+    ws.dy[0].get(yb + 8);
+    cudaStream_t st = ws.st[0];
+    auto* dy0 = static_cast<double*>(ws.dy[0].ptr);
+    auto* hy0 = static_cast<double*>(ws.hy[0].ptr);
+    auto* dflag = reinterpret_cast<unsigned long long*>(dy0 + static_cast<size_t>(n) * m);
+    if (xrows)
+      rows_copy(true, static_cast<double*>(ws.hx[0].ptr), xrows, nullptr, 0, n, d);
+    else
+      host_copy(ws.hx[0].ptr, x, xb);
+    DDSG_CUDA(cudaMemsetAsync(dflag, 0xff, sizeof(unsigned long long), st));  // ULLONG_MAX
+    DDSG_CUDA(cudaMemcpyAsync(ws.dx[0].ptr, ws.hx[0].ptr, xb, cudaMemcpyHostToDevice, st));
+    stats.launches += launch_eval(prog, exact, static_cast<const double*>(ws.dx[0].ptr), n, 0, dy0, dflag, st, ws.xt[0]);
+    DDSG_CUDA(cudaMemcpyAsync(hy0, dy0, yb + 8, cudaMemcpyDeviceToHost, st));
+    DDSG_CUDA(cudaStreamSynchronize(st));
+    if (yrows)
+      rows_copy(false, hy0, nullptr, yrows, 0, n, m);
+    else
+      host_copy(y, hy0, yb);
+    stats.main_ms = kernel_timer().collect();
+    unsigned long long flag;
+    std::memcpy(&flag, hy0 + static_cast<size_t>(n) * m, sizeof(flag));
+    return flag == ULLONG_MAX ? -1 : static_cast<int64_t>(flag);
+  }
   auto* dbad = static_cast<unsigned long long*>(ws.bad.get(sizeof(unsigned long long)));
   auto* hbad = static_cast<unsigned long long*>(ws.hbad.get(sizeof(unsigned long long)));
   DDSG_CUDA(cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), ws.st[0]));  // ULLONG_MAX
