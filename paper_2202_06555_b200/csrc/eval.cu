@@ -670,9 +670,12 @@ static int64_t small_plain_points(const DeviceProgram& prog) {
 }
 
 // Launches the evaluation of n device-resident points; returns kernel launches.
+// `pipelined`: one chunk of a multi-stream host pipeline (the next chunk's
+// kernel fills this one's last wave; subtree-split launches would only add
+// sync points there).
 static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* dx, int64_t n,
                            int64_t base, double* dy, unsigned long long* dbad, cudaStream_t st,
-                           Scratch& xt_scratch) {
+                           Scratch& xt_scratch, bool pipelined = false) {
   if (n <= 0) return 0;
   const EvalParams P = prog.params(exact);
   if (P.plain && n <= small_plain_points(prog)) {
@@ -735,9 +738,10 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
     for (int64_t off = 0; off < n; off += chunk) {
       const int64_t cnt = std::min(chunk, n - off);
       // (a short last chunk may take the split path: its partial sums are small, but sized explicitly)
+      const bool split_ok = !pipelined && n <= chunk;
       double* xt = static_cast<double*>(
-          xt_scratch.get(std::max(f->scratch_bytes(std::min(chunk, n)), f->scratch_bytes(cnt))));
-      launches += f->launch(exact, dx + off * d, cnt, base + off, dy + off * P.m, dbad, xt, st);
+          xt_scratch.get(std::max(f->scratch_bytes(std::min(chunk, n), split_ok), f->scratch_bytes(cnt, split_ok))));
+      launches += f->launch(exact, dx + off * d, cnt, base + off, dy + off * P.m, dbad, xt, st, split_ok);
     }
     return launches;
   }
@@ -809,7 +813,7 @@ int64_t evaluate(const DeviceProgram& prog, int exact, const double* x, int64_t 
     if (!x_dev)
       DDSG_CUDA(cudaMemcpyAsync(const_cast<double*>(dx), x + off * d, cnt * d * 8,
                                 cudaMemcpyHostToDevice, st));
-    stats.launches += launch_eval(prog, exact, dx, cnt, off, dy, dbad, st, ts.xt[b]);
+    stats.launches += launch_eval(prog, exact, dx, cnt, off, dy, dbad, st, ts.xt[b], n > chunk);
     if (!y_dev)
       DDSG_CUDA(cudaMemcpyAsync(y + off * m, dy, cnt * m * 8, cudaMemcpyDeviceToHost, st));
   }
@@ -998,7 +1002,7 @@ int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, i
     cudaStream_t st = ws.st[b];
     DDSG_CUDA(cudaMemcpyAsync(ws.dx[b].ptr, ws.hx[b].ptr, cnt * d * 8, cudaMemcpyHostToDevice, st));
     stats.launches += launch_eval(prog, exact, static_cast<const double*>(ws.dx[b].ptr), cnt, off,
-                                  static_cast<double*>(ws.dy[b].ptr), dbad, st, ws.xt[b]);
+                                  static_cast<double*>(ws.dy[b].ptr), dbad, st, ws.xt[b], true);
     DDSG_CUDA(cudaMemcpyAsync(ws.hy[b].ptr, ws.dy[b].ptr, cnt * m * 8, cudaMemcpyDeviceToHost, st));
     DDSG_CUDA(cudaEventRecord(ws.done[b], st));
   }

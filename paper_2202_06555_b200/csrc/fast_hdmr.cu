@@ -438,8 +438,9 @@ int FastHdmr::split_levels(int64_t n) const {
   for (int S = 0; S <= max_split_; ++S) {
     if (S > 0 && (static_cast<size_t>(n) * m_ * 8) << S > (size_t{256} << 20)) break;  // partial sums <= 256 MiB
     const int64_t waves = ((ctas << S) + sms[dev] - 1) / sms[dev];
+    // (+ the subtree roots written and read back: 16 B per output and subtree at ~3 TB/s)
     const double us = static_cast<double>(waves) * kSlotUs * ((n_blocks_ + (1 << S) - 1) >> S) +
-                      (S > 0 ? kSubLaunchUs * (1 << S) : 0.0);
+                      (S > 0 ? kSubLaunchUs * (1 << S) + 16.0 * n * m_ * (1 << S) / 3.0e6 : 0.0);
     if (S == 0 || us < best_us) {
       best_us = us;
       best = S;
@@ -461,9 +462,9 @@ double FastHdmr::split_cost_us(int64_t n) const {
   return 40.0 + kSubLaunchUs * (1 << S) + static_cast<double>(waves) * kSlotUs * ((n_blocks_ + (1 << S) - 1) >> S);
 }
 
-size_t FastHdmr::scratch_bytes(int64_t n) const {
+size_t FastHdmr::scratch_bytes(int64_t n, bool allow_split) const {
   const size_t xt = static_cast<size_t>(n) * d_ * 8;
-  const int S = split_levels(n);
+  const int S = allow_split ? split_levels(n) : 0;
   return S == 0 ? xt : (xt + 255) / 256 * 256 + (size_t{1} << S) * static_cast<size_t>(n) * m_ * 8;
 }
 
@@ -510,12 +511,12 @@ __global__ void split_combine_kernel(const double* __restrict__ part, int64_t ou
 }  // namespace
 
 int64_t FastHdmr::launch(int exact, const double* x, int64_t n, int64_t base, double* y,
-                         unsigned long long* bad, double* xt, cudaStream_t st) const {
+                         unsigned long long* bad, double* xt, cudaStream_t st, bool allow_split) const {
   // dim-major copy of the points so each slot's coordinate read is coalesced
   dim3 tgrid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((d_ + 31) / 32));
   transpose_check_kernel<<<tgrid, dim3(32, 8), 0, st>>>(x, n, d_, base, xt, bad);
   DDSG_CUDA(cudaGetLastError());
-  if (const int S = split_levels(n); S > 0) {
+  if (const int S = allow_split ? split_levels(n) : 0; S > 0) {
     // a few tiles only: the subtrees of depth S as concurrent launches
     const int K = 1 << S;
     const int64_t tiles_s = (n + kPoints - 1) / kPoints;

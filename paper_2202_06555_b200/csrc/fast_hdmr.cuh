@@ -127,10 +127,10 @@ class FastHdmr {
   // device scratch of at least n*d doubles (the dim-major copy of x).
   // Returns the number of kernel launches.
   int64_t launch(int exact, const double* x, int64_t n, int64_t base, double* y, unsigned long long* bad,
-                 double* xt, cudaStream_t st) const;
+                 double* xt, cudaStream_t st, bool allow_split = true) const;
   // Bytes of the device scratch `xt` a launch over n points needs: the
   // dim-major points, plus the subtree partial sums of a split launch.
-  size_t scratch_bytes(int64_t n) const;
+  size_t scratch_bytes(int64_t n, bool allow_split = true) const;
   // Subtree split of a launch over n points (0 = one launch walks every slot).
   int split_levels(int64_t n) const;
   double split_cost_us(int64_t n) const;
