@@ -74,6 +74,8 @@ class DeviceProgram {
     const int32_t* height_off = nullptr;  // [heights + 1] node ranges per height
   };
   const SlotTree& slot_tree() const { return tree_; }
+  // Unique per uploaded program (never reused): the key of cached CUDA graphs.
+  uint64_t uid() const { return uid_; }
 
  private:
   HostProgram hp_;
@@ -83,6 +85,7 @@ class DeviceProgram {
   FastHdmr* fast_ = nullptr;    // slot-staged kernel program, when the program qualifies
   PlainGrid* plain_ = nullptr;  // prefix-walk plain-grid kernel program, when it qualifies
   SlotTree tree_;
+  uint64_t uid_ = 0;
   template <typename T>
   const T* put(const std::vector<T>& v);
 };

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <thread>
@@ -52,10 +53,15 @@ struct TimerState {
   }
 };
 thread_local TimerState g_timer;
+thread_local bool g_timer_off = false;  // during CUDA graph capture: no timing events in the graph
 }  // namespace
 
-void KernelTimer::begin(cudaStream_t st) { DDSG_CUDA(cudaEventRecord(g_timer.next(), st)); }
-void KernelTimer::end(cudaStream_t st) { DDSG_CUDA(cudaEventRecord(g_timer.next(), st)); }
+void KernelTimer::begin(cudaStream_t st) {
+  if (!g_timer_off) DDSG_CUDA(cudaEventRecord(g_timer.next(), st));
+}
+void KernelTimer::end(cudaStream_t st) {
+  if (!g_timer_off) DDSG_CUDA(cudaEventRecord(g_timer.next(), st));
+}
 double KernelTimer::collect() {
   double total = 0.0;
   for (size_t i = 0; i + 1 < g_timer.used; i += 2) {
@@ -99,6 +105,8 @@ const T* DeviceProgram::put(const std::vector<T>& v) {
 }
 
 void DeviceProgram::upload(const HostProgram& hp) {
+  static std::atomic<uint64_t> next_uid{1};
+  uid_ = next_uid.fetch_add(1);
   for (void* p : allocs_) cudaFree(p);
   allocs_.clear();
   delete fast_;
@@ -875,6 +883,22 @@ struct StagedWorkspace::Impl {
   cudaEvent_t init = nullptr;
   Pinned hx[2], hy[2], hbad;
   Scratch dx[2], dy[2], bad, xt[2];
+  // Per-point callers repeat one small call thousands of times: its memset,
+  // H2D copy, kernels and D2H copy are captured once into a CUDA graph and
+  // replayed with one launch (the buffers are the workspace's own, so the
+  // graph stays valid while the key below does).
+  struct SmallGraph {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t prog_uid = 0;
+    int exact = -1;
+    int64_t n = 0, launches = 0;
+    const void *hx = nullptr, *hy = nullptr, *dx = nullptr, *dy = nullptr, *xt = nullptr;
+    int seen = 0;  // identical consecutive eager calls (capture on the fourth); -1: capture failed, stay eager
+  } graph;
+  void drop_graph() {
+    if (graph.exec) cudaGraphExecDestroy(graph.exec);
+    graph = SmallGraph{};
+  }
   void bind() {
     int dev = 0;
     DDSG_CUDA(cudaGetDevice(&dev));
@@ -888,6 +912,7 @@ struct StagedWorkspace::Impl {
     DDSG_CUDA(cudaEventCreateWithFlags(&init, cudaEventDisableTiming));
   }
   ~Impl() {
+    if (graph.exec) cudaGraphExecDestroy(graph.exec);
     for (int b = 0; b < 2; ++b) {
       if (st[b]) cudaStreamDestroy(st[b]);
       if (done[b]) cudaEventDestroy(done[b]);
@@ -956,10 +981,69 @@ int64_t evaluate_staged(const DeviceProgram& prog, int exact, const double* x, i
       rows_copy(true, static_cast<double*>(ws.hx[0].ptr), xrows, nullptr, 0, n, d);
     else
       host_copy(ws.hx[0].ptr, x, xb);
-    DDSG_CUDA(cudaMemsetAsync(dflag, 0xff, sizeof(unsigned long long), st));  // ULLONG_MAX
-    DDSG_CUDA(cudaMemcpyAsync(ws.dx[0].ptr, ws.hx[0].ptr, xb, cudaMemcpyHostToDevice, st));
-    stats.launches += launch_eval(prog, exact, static_cast<const double*>(ws.dx[0].ptr), n, 0, dy0, dflag, st, ws.xt[0]);
-    DDSG_CUDA(cudaMemcpyAsync(hy0, dy0, yb + 8, cudaMemcpyDeviceToHost, st));
+    auto enqueue = [&] {
+      DDSG_CUDA(cudaMemsetAsync(dflag, 0xff, sizeof(unsigned long long), st));  // ULLONG_MAX
+      DDSG_CUDA(cudaMemcpyAsync(ws.dx[0].ptr, ws.hx[0].ptr, xb, cudaMemcpyHostToDevice, st));
+      const int64_t l = launch_eval(prog, exact, static_cast<const double*>(ws.dx[0].ptr), n, 0, dy0, dflag, st, ws.xt[0]);
+      DDSG_CUDA(cudaMemcpyAsync(hy0, dy0, yb + 8, cudaMemcpyDeviceToHost, st));
+      return l;
+    };
+    static const bool graphs_on = [] {
+      const char* e = std::getenv("DDSG_SMALL_GRAPH");  // A/B switch
+      return !(e && std::atoi(e) == 0);
+    }();
+    auto& G = ws.graph;
+    const bool same = graphs_on && n <= 64 && G.seen >= 0 && G.prog_uid == prog.uid() && G.exact == exact && G.n == n &&
+                      G.hx == ws.hx[0].ptr && G.hy == ws.hy[0].ptr && G.dx == ws.dx[0].ptr && G.dy == ws.dy[0].ptr &&
+                      G.xt == ws.xt[0].ptr;
+    if (same && G.exec) {
+      DDSG_CUDA(cudaGraphLaunch(G.exec, st));
+      stats.launches += G.launches;
+    } else if (same && G.seen >= 3) {
+      // the fourth identical call in a row: capture (the eager ones sized every
+      // buffer; callers that alternate programs on one workspace never get here)
+      cudaGraph_t graph = nullptr;
+      bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        g_timer_off = true;
+        try {
+          G.launches = enqueue();
+        } catch (...) {
+          ok = false;
+        }
+        g_timer_off = false;
+        ok = (cudaStreamEndCapture(st, &graph) == cudaSuccess) && ok && graph != nullptr;
+      }
+      if (ok) ok = cudaGraphInstantiate(&G.exec, graph, 0) == cudaSuccess;
+      if (graph) cudaGraphDestroy(graph);
+      if (!ok) {
+        (void)cudaGetLastError();
+        G.exec = nullptr;
+        G.seen = -1;  // not capturable here: stay on the eager path
+        stats.launches += enqueue();
+      } else {
+        DDSG_CUDA(cudaGraphLaunch(G.exec, st));
+        stats.launches += G.launches;
+      }
+    } else if (same) {
+      stats.launches += enqueue();
+      ++G.seen;
+    } else {
+      stats.launches += enqueue();
+      if (graphs_on && n <= 64 && G.seen >= 0) {
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        G = StagedWorkspace::Impl::SmallGraph{};
+        G.prog_uid = prog.uid();
+        G.exact = exact;
+        G.n = n;
+        G.hx = ws.hx[0].ptr;
+        G.hy = ws.hy[0].ptr;
+        G.dx = ws.dx[0].ptr;
+        G.dy = ws.dy[0].ptr;
+        G.xt = ws.xt[0].ptr;
+        G.seen = 1;
+      }
+    }
     DDSG_CUDA(cudaStreamSynchronize(st));
     if (yrows)
       rows_copy(false, hy0, nullptr, yrows, 0, n, m);
