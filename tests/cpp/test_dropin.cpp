@@ -734,6 +734,44 @@ static void refine_cases(bool on_device) {
   }
 }
 
+// Repeated per-point calls on one workspace are replayed as a CUDA graph
+// from the fourth identical call on: every call must still see its own point,
+// report its own domain error, and survive a change of program.
+static void workspace_replay_cases() {
+  auto fa = scalar([](std::span<const double> x) { return std::exp(x[0] - x[1]) + x[2] * x[0]; });
+  auto fb = scalar([](std::span<const double> x) { return std::sin(3.0 * x[0]) * x[1] + x[2]; });
+  DdsgOptions opt;
+  opt.k_max = 2;
+  opt.max_level = 4;
+  opt.mode = BoundaryMode::modified_linear;
+  const auto va = VectorizedDdsg::compile(std::make_shared<const DdsgFunction>(decompose(fa, 3, 1, center_anchor(fa, 3, 1), opt)));
+  const auto vb = VectorizedDdsg::compile(std::make_shared<const DdsgFunction>(decompose(fb, 3, 1, center_anchor(fb, 3, 1), opt)));
+  const auto pts = uniform_points(3, 60, 4242);
+  const auto want_a = va.evaluate_batch(pts), want_b = vb.evaluate_batch(pts);
+  EvalWorkspace ws;
+  std::vector<double> out(1);
+  int bad = 0;
+  for (std::size_t i = 0; i < 30; ++i) {  // one program, many calls: eager, captured, replayed
+    va.evaluate(pts[i], out, ws);
+    bad += std::memcmp(out.data(), want_a[i].data(), sizeof(double)) != 0;
+    if (i == 12) {  // a domain error in the middle of the replayed run, then on
+      std::vector<double> outside{0.5, 1.5, 0.5};
+      bad += !throws<std::domain_error>([&] { va.evaluate(outside, out, ws); });
+    }
+  }
+  for (std::size_t i = 30; i < 45; ++i) {  // the other program on the same workspace
+    vb.evaluate(pts[i], out, ws);
+    bad += std::memcmp(out.data(), want_b[i].data(), sizeof(double)) != 0;
+  }
+  for (std::size_t i = 45; i < 60; ++i) {  // alternating programs never replay
+    va.evaluate(pts[i], out, ws);
+    bad += std::memcmp(out.data(), want_a[i].data(), sizeof(double)) != 0;
+    vb.evaluate(pts[i], out, ws);
+    bad += std::memcmp(out.data(), want_b[i].data(), sizeof(double)) != 0;
+  }
+  CHECK(bad == 0);
+}
+
 static void decompose_gpu_cases() {
   // test_hdmr.cpp:175-190 and 245-251: the decomposition against the plain sparse grid
   {
@@ -791,6 +829,7 @@ int main(int argc, char** argv) {
     irbc_gpu_cases();
     decompose_gpu_cases();
     refine_cases(true);
+    workspace_replay_cases();
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;
