@@ -72,6 +72,9 @@ class DeviceProgram {
     const int32_t* left = nullptr;   // [nodes] child ids (< n_active: leaf / slot row)
     const int32_t* right = nullptr;
     const int32_t* height_off = nullptr;  // [heights + 1] node ranges per height
+    // fused small-batch kernel: every subspace of every active slot
+    int n_subs = 0;                       // subspaces of all active slots (concatenated, slot order)
+    const int32_t* sub_slot = nullptr;    // [n_subs] active slot of the subspace
   };
   const SlotTree& slot_tree() const { return tree_; }
   // Unique per uploaded program (never reused): the key of cached CUDA graphs.

@@ -185,6 +185,11 @@ void DeviceProgram::upload(const HostProgram& hp) {
     tree_.left = put(left);
     tree_.right = put(right);
     tree_.height_off = put(off);
+    std::vector<int32_t> sub_slot(hp.sub_lv_off.size(), 0);
+    for (int a = 0; a < na; ++a)
+      for (int sb = hp.slot_sub_begin[a]; sb < hp.slot_sub_end[a]; ++sb) sub_slot[static_cast<size_t>(sb)] = a;
+    tree_.n_subs = static_cast<int>(sub_slot.size());
+    tree_.sub_slot = put(sub_slot);
   }
   delete fast_;
   fast_ = new FastHdmr();
@@ -397,6 +402,103 @@ __global__ void __launch_bounds__(256) slot_tree_kernel(int na, DeviceProgram::S
   }
   const int root = T.nodes > 0 ? na + T.nodes - 1 : 0;
   if (threadIdx.x < nc) y[p * m + c0 + threadIdx.x] = vals[root * kCols + threadIdx.x];
+}
+
+// The same three steps fused into one launch per call (one CTA per (point,
+// column chunk); the per-point callers' latency is launches and dependent
+// loads, not arithmetic):
+//   A. one thread per subspace of every active slot: the term's weight (the
+//      reference's dim-ordered product with early exit), its surplus row and
+//      that row's stored-order run -> shared memory (-1: a term the reference
+//      skips: w == 0 or no node);
+//   B. one thread per (slot, column): the slot's terms in canonical order per
+//      run, acc = acc + w * s -- every load is independent of the accumulator
+//      (a skipped or other-run term adds 0 * 0 through selects, which leaves
+//      the accumulator's bits unchanged: it is never -0) -- then x b;
+//   C. the pairwise tree over the slot rows, height by height.
+// Same operations on the same operands as slot_rows_kernel + slot_tree_kernel.
+template <int kCols>
+__global__ void __launch_bounds__(1024, 1) small_fused_kernel(EvalParams P, DeviceProgram::SlotTree T,
+                                                              const double* __restrict__ x, int64_t n, int64_t base,
+                                                              double* __restrict__ y, unsigned long long* bad) {
+  extern __shared__ double sm[];
+  const int na = P.n_active, ns = T.n_subs;
+  double* vals = sm;                                          // [na + T.nodes][kCols]
+  double* wts = vals + static_cast<size_t>(na + T.nodes) * kCols;  // [ns]
+  int32_t* rows = reinterpret_cast<int32_t*>(wts + ns);       // [ns]
+  int16_t* runs = reinterpret_cast<int16_t*>(rows + ns);      // [ns]
+  const int chunks = (P.m + kCols - 1) / kCols;
+  const int64_t p = blockIdx.x / chunks;
+  const int c0 = static_cast<int>(blockIdx.x % chunks) * kCols;
+  const int nc = min(kCols, P.m - c0);
+  const double* xp = x + p * P.d;
+  if (threadIdx.x == 0 && c0 == 0 && !point_ok(xp, P.d)) atomicMin(bad, static_cast<unsigned long long>(base + p));
+
+  // A. terms
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+    const int a = T.sub_slot[s];
+    const int k = P.slot_k[a];
+    const int32_t* dims = P.slot_dims + P.slot_dims_off[a];
+    const int mode = P.slot_mode[a];
+    const uint8_t* lv = P.levels + P.sub_lv_off[s];
+    double w = 1.0;
+    int64_t lin = 0;
+    bool ok = true;  // the slot's own coordinates (a bad point's rows are never used)
+    for (int j = 0; j < k; ++j) ok &= (xp[dims[j]] >= 0.0 && xp[dims[j]] <= 1.0);
+    for (int j = 0; ok && j < k; ++j) {
+      const int l = lv[j];
+      const double xv = xp[dims[j]];
+      const uint32_t kk = cell_at(xv, l);
+      w = __dmul_rn(w, basis_at(mode, l, kk, xv));
+      lin = (lin << (l - 1)) | kk;
+      if (w == 0.0) break;
+    }
+    int32_t row = -1;
+    if (ok && w != 0.0) row = P.slab[P.sub_slab_off[s] + lin];
+    wts[s] = w;
+    rows[s] = row;
+    runs[s] = row >= 0 ? P.row_run[row] : int16_t{0};
+  }
+  __syncthreads();
+
+  // B. slot rows
+  for (int i = threadIdx.x; i < na * kCols; i += blockDim.x) {
+    const int a = i / kCols, c = i % kCols;
+    const double b = P.slot_b[a];
+    double acc = 0.0;
+    if (c < nc) {
+      if (P.slot_k[a] == 0) {
+        acc = __dmul_rn(b, P.f_anchor[c0 + c]);
+      } else {
+        const int s0 = P.slot_sub_begin[a], s1 = P.slot_sub_end[a];
+        const int nruns = P.slot_runs[a];
+        const double* sur = P.surplus + c0 + c;
+        for (int run = 0; run < nruns; ++run)
+          for (int s = s0; s < s1; ++s) {
+            const int32_t row = rows[s];
+            const bool use = row >= 0 && (nruns == 1 || runs[s] == run);
+            const double v = use ? sur[static_cast<int64_t>(row) * P.m] : 0.0;
+            const double w = use ? wts[s] : 0.0;
+            acc = accum(acc, w, v, P.exact);
+          }
+        acc = __dmul_rn(acc, b);
+      }
+    }
+    vals[i] = acc;
+  }
+  __syncthreads();
+
+  // C. pairwise tree
+  for (int h = 1; h <= T.heights; ++h) {
+    const int lo = h == 1 ? 0 : T.height_off[h - 1], hi = T.height_off[h];
+    for (int i = lo * kCols + threadIdx.x; i < hi * kCols; i += blockDim.x) {
+      const int q = i / kCols, c = i % kCols;
+      vals[(na + q) * kCols + c] = __dadd_rn(vals[T.left[q] * kCols + c], vals[T.right[q] * kCols + c]);
+    }
+    __syncthreads();
+  }
+  const int root = T.nodes > 0 ? na + T.nodes - 1 : 0;
+  if (threadIdx.x < nc) y[p * P.m + c0 + threadIdx.x] = vals[root * kCols + threadIdx.x];
 }
 
 // -------------------------------------------------- small plain batches
@@ -726,6 +828,33 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
     // few points: slot-parallel rows, then the pairwise tree per (point, chunk)
     constexpr int kCols = 8;
     const int chunks = (P.m + kCols - 1) / kCols;
+    {
+      // one fused launch when the terms and slot rows of a (point, chunk) fit a
+      // CTA's shared memory (DDSG_SMALL_FUSED=0: the two-kernel form below)
+      static const bool fused_on = [] {
+        const char* e = std::getenv("DDSG_SMALL_FUSED");
+        return !(e && std::atoi(e) == 0);
+      }();
+      const DeviceProgram::SlotTree& T = prog.slot_tree();
+      const size_t smem = static_cast<size_t>(P.n_active + T.nodes) * kCols * 8 + static_cast<size_t>(T.n_subs) * 14 + 16;
+      // measured (profiles/r2_small_fused.json): ahead for programs of up to ~2,000 subspaces
+      // and <= 32 points (config 4: 26 vs 39 us at n = 1); config 5's 6,244 subspaces on 19 CTAs
+      // lose to the two-kernel form (50 vs 44 us), and one CTA per (point, chunk) does not scale in n
+      static const bool fused_all = [] {
+        const char* e = std::getenv("DDSG_SMALL_FUSED");
+        return e && std::atoi(e) == 2;  // 2: whenever it fits (tests, A/B)
+      }();
+      const bool fused_pays = fused_all || (T.n_subs <= 2048 && n <= 32);
+      if (fused_on && fused_pays && T.sub_slot != nullptr && smem <= size_t{200} * 1024 &&
+          n * chunks <= (int64_t{1} << 30)) {
+        ensure_dynamic_smem(reinterpret_cast<const void*>(small_fused_kernel<kCols>), smem);
+        kernel_timer().begin(st);
+        small_fused_kernel<kCols><<<static_cast<unsigned>(n * chunks), 1024, smem, st>>>(P, T, dx, n, base, dy, dbad);
+        kernel_timer().end(st);
+        DDSG_CUDA(cudaGetLastError());
+        return 1;
+      }
+    }
     double* rows = static_cast<double*>(xt_scratch.get(static_cast<size_t>(n) * P.n_active * P.m * 8));
     const int64_t threads = n * P.n_active * chunks;
     kernel_timer().begin(st);

@@ -366,3 +366,41 @@ def test_mid_batches_split_bit_exact(case, n):
     tiles, n_cb = -(-n // 512), -(-m // 8)
     if tiles * n_cb * 2 <= 148 and len(so) >= 64:  # (few slots: one launch is cheaper than the fork/join)
         assert launches > 2, (launches, tiles, n_cb)  # transpose + 2^S subtrees + combine
+
+
+# The small-batch forms (fused one-launch kernel / rows + tree kernels) and the
+# split launches are chosen by switches read once per process: run a few
+# programs in child processes under each setting and compare the raw bits.
+
+_CHILD = r"""
+import hashlib, sys
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import numpy as np
+from test_gpu_random_programs import random_program
+from helpers import bits
+h = hashlib.sha256()
+for seed in (3, 11, 42, 77):
+    d, m, fa, slots_o, vec, x = random_program(seed)
+    for n in (1, 5, 40, 300):
+        xs = np.ascontiguousarray(np.resize(x, (n, d)))
+        h.update(bits(vec.evaluate_batch(xs)).tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_small_and_mid_batch_forms_agree_bitwise():
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parent.parent)
+    digests = {}
+    for name, env in {"default": {}, "fused_everywhere": {"DDSG_SMALL_FUSED": "2"},
+                      "two_kernels": {"DDSG_SMALL_FUSED": "0"}, "no_split": {"DDSG_SLOT_SPLIT": "0"},
+                      "slot_kernel_only": {"DDSG_SMALL_BATCH": "0"}}.items():
+        out = subprocess.run([sys.executable, "-c", _CHILD, root], env={**os.environ, **env}, capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        digests[name] = out.stdout.strip().splitlines()[-1]
+    assert len(set(digests.values())) == 1, digests
