@@ -417,6 +417,94 @@ __global__ void __launch_bounds__(256) slot_tree_kernel(int na, DeviceProgram::S
 //      the accumulator's bits unchanged: it is never -0) -- then x b;
 //   C. the pairwise tree over the slot rows, height by height.
 // Same operations on the same operands as slot_rows_kernel + slot_tree_kernel.
+// Term s (a subspace of an active slot) at point xp: weight, surplus row
+// (-1: skipped by the reference) and the row's stored-order run.
+__device__ __forceinline__ void slot_term(const EvalParams& P, const DeviceProgram::SlotTree& T, const double* xp,
+                                          int s, double& w_out, int32_t& row_out, int16_t& run_out) {
+  const int a = T.sub_slot[s];
+  const int k = P.slot_k[a];
+  const int32_t* dims = P.slot_dims + P.slot_dims_off[a];
+  const int mode = P.slot_mode[a];
+  const uint8_t* lv = P.levels + P.sub_lv_off[s];
+  double w = 1.0;
+  int64_t lin = 0;
+  bool ok = true;  // the slot's own coordinates (a bad point's rows are never used)
+  for (int j = 0; j < k; ++j) ok &= (xp[dims[j]] >= 0.0 && xp[dims[j]] <= 1.0);
+  for (int j = 0; ok && j < k; ++j) {
+    const int l = lv[j];
+    const double xv = xp[dims[j]];
+    const uint32_t kk = cell_at(xv, l);
+    w = __dmul_rn(w, basis_at(mode, l, kk, xv));
+    lin = (lin << (l - 1)) | kk;
+    if (w == 0.0) break;
+  }
+  int32_t row = -1;
+  if (ok && w != 0.0) row = P.slab[P.sub_slab_off[s] + lin];
+  w_out = w;
+  row_out = row;
+  run_out = row >= 0 ? P.row_run[row] : int16_t{0};
+}
+
+// The two-launch form of steps A and B for batches the fused kernel does not
+// take: one thread per (point, subspace) writes the term to a scratch, then
+// one thread per (point, slot, output) sums the slot's terms in canonical
+// order per run with the loads of four terms in flight ahead of the dependent
+// additions; slot_tree_kernel folds the rows.
+__global__ void __launch_bounds__(128) slot_terms_kernel(EvalParams P, DeviceProgram::SlotTree T,
+                                                         const double* __restrict__ x, int64_t n, int64_t base,
+                                                         double* __restrict__ wts, int32_t* __restrict__ rows,
+                                                         int16_t* __restrict__ runs, unsigned long long* bad) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p = t / T.n_subs;
+  if (p >= n) return;
+  const int s = static_cast<int>(t - p * T.n_subs);
+  const double* xp = x + p * P.d;
+  if (s == 0 && !point_ok(xp, P.d)) atomicMin(bad, static_cast<unsigned long long>(base + p));
+  slot_term(P, T, xp, s, wts[t], rows[t], runs[t]);
+}
+
+__global__ void __launch_bounds__(128) slot_sums_kernel(EvalParams P, DeviceProgram::SlotTree T, int64_t n,
+                                                        const double* __restrict__ wts,
+                                                        const int32_t* __restrict__ rows,
+                                                        const int16_t* __restrict__ runs,
+                                                        double* __restrict__ out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t pa = t / P.m;
+  if (pa >= n * P.n_active) return;
+  const int c = static_cast<int>(t - pa * P.m);
+  const int a = static_cast<int>(pa % P.n_active);
+  const int64_t p = pa / P.n_active;
+  const double b = P.slot_b[a];
+  double acc;
+  if (P.slot_k[a] == 0) {
+    acc = __dmul_rn(b, P.f_anchor[c]);
+  } else {
+    acc = 0.0;
+    const int s0 = P.slot_sub_begin[a], s1 = P.slot_sub_end[a], nruns = P.slot_runs[a];
+    const double* sur = P.surplus + c;
+    const double* w_p = wts + p * T.n_subs;
+    const int32_t* r_p = rows + p * T.n_subs;
+    const int16_t* u_p = runs + p * T.n_subs;
+    constexpr int kAheadTerms = 4;
+    for (int run = 0; run < nruns; ++run)
+      for (int s = s0; s < s1; s += kAheadTerms) {
+        double w[kAheadTerms], v[kAheadTerms];
+#pragma unroll
+        for (int q = 0; q < kAheadTerms; ++q) {
+          const int sq = min(s + q, s1 - 1);
+          const int32_t row = r_p[sq];
+          const bool use = s + q < s1 && row >= 0 && (nruns == 1 || u_p[sq] == run);
+          w[q] = use ? w_p[sq] : 0.0;
+          v[q] = use ? sur[static_cast<int64_t>(row) * P.m] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < kAheadTerms; ++q) acc = accum(acc, w[q], v[q], P.exact);  // a skipped term adds 0 * 0
+      }
+    acc = __dmul_rn(acc, b);
+  }
+  out[pa * P.m + c] = acc;
+}
+
 template <int kCols>
 __global__ void __launch_bounds__(1024, 1) small_fused_kernel(EvalParams P, DeviceProgram::SlotTree T,
                                                               const double* __restrict__ x, int64_t n, int64_t base,
@@ -435,30 +523,7 @@ __global__ void __launch_bounds__(1024, 1) small_fused_kernel(EvalParams P, Devi
   if (threadIdx.x == 0 && c0 == 0 && !point_ok(xp, P.d)) atomicMin(bad, static_cast<unsigned long long>(base + p));
 
   // A. terms
-  for (int s = threadIdx.x; s < ns; s += blockDim.x) {
-    const int a = T.sub_slot[s];
-    const int k = P.slot_k[a];
-    const int32_t* dims = P.slot_dims + P.slot_dims_off[a];
-    const int mode = P.slot_mode[a];
-    const uint8_t* lv = P.levels + P.sub_lv_off[s];
-    double w = 1.0;
-    int64_t lin = 0;
-    bool ok = true;  // the slot's own coordinates (a bad point's rows are never used)
-    for (int j = 0; j < k; ++j) ok &= (xp[dims[j]] >= 0.0 && xp[dims[j]] <= 1.0);
-    for (int j = 0; ok && j < k; ++j) {
-      const int l = lv[j];
-      const double xv = xp[dims[j]];
-      const uint32_t kk = cell_at(xv, l);
-      w = __dmul_rn(w, basis_at(mode, l, kk, xv));
-      lin = (lin << (l - 1)) | kk;
-      if (w == 0.0) break;
-    }
-    int32_t row = -1;
-    if (ok && w != 0.0) row = P.slab[P.sub_slab_off[s] + lin];
-    wts[s] = w;
-    rows[s] = row;
-    runs[s] = row >= 0 ? P.row_run[row] : int16_t{0};
-  }
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) slot_term(P, T, xp, s, wts[s], rows[s], runs[s]);
   __syncthreads();
 
   // B. slot rows
@@ -855,17 +920,35 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
         return 1;
       }
     }
-    double* rows = static_cast<double*>(xt_scratch.get(static_cast<size_t>(n) * P.n_active * P.m * 8));
-    const int64_t threads = n * P.n_active * chunks;
-    kernel_timer().begin(st);
-    slot_rows_kernel<kCols><<<static_cast<unsigned>((threads + 127) / 128), 128, 0, st>>>(P, dx, n, base, rows, dbad);
     const DeviceProgram::SlotTree& T = prog.slot_tree();
+    static const bool term_split = [] {
+      const char* e = std::getenv("DDSG_SMALL_TERMS");  // 0: slot_rows_kernel walks each slot in one thread
+      return !(e && std::atoi(e) == 0);
+    }();
+    const size_t rows_bytes = (static_cast<size_t>(n) * P.n_active * P.m * 8 + 255) / 256 * 256;
+    const size_t terms = static_cast<size_t>(n) * T.n_subs;
+    const bool use_terms = term_split && T.sub_slot != nullptr && terms > 0 && terms * 14 <= (size_t{512} << 20);
+    char* ws = static_cast<char*>(xt_scratch.get(rows_bytes + (use_terms ? terms * 14 + 64 : 0)));
+    double* rows = reinterpret_cast<double*>(ws);
+    kernel_timer().begin(st);
+    if (use_terms) {
+      double* wts = reinterpret_cast<double*>(ws + rows_bytes);
+      int32_t* trow = reinterpret_cast<int32_t*>(wts + terms);
+      int16_t* trun = reinterpret_cast<int16_t*>(trow + terms);
+      slot_terms_kernel<<<static_cast<unsigned>((terms + 127) / 128), 128, 0, st>>>(P, T, dx, n, base, wts, trow, trun,
+                                                                                   dbad);
+      const int64_t sums = n * P.n_active * P.m;
+      slot_sums_kernel<<<static_cast<unsigned>((sums + 127) / 128), 128, 0, st>>>(P, T, n, wts, trow, trun, rows);
+    } else {
+      const int64_t threads = n * P.n_active * chunks;
+      slot_rows_kernel<kCols><<<static_cast<unsigned>((threads + 127) / 128), 128, 0, st>>>(P, dx, n, base, rows, dbad);
+    }
     const size_t smem = static_cast<size_t>(P.n_active + T.nodes) * kCols * 8;
     ensure_dynamic_smem(reinterpret_cast<const void*>(slot_tree_kernel<kCols>), smem);
     slot_tree_kernel<kCols><<<static_cast<unsigned>(n * chunks), 256, smem, st>>>(P.n_active, T, rows, P.m, dy);
     kernel_timer().end(st);
     DDSG_CUDA(cudaGetLastError());
-    return 2;
+    return use_terms ? 3 : 2;
   }
   if (const FastHdmr* f = prog.fast()) {
     // chunk so the dim-major scratch stays <= ~1 GiB

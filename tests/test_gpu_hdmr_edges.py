@@ -397,7 +397,8 @@ def test_small_and_mid_batch_forms_agree_bitwise():
     root = str(Path(__file__).resolve().parent.parent)
     digests = {}
     for name, env in {"default": {}, "fused_everywhere": {"DDSG_SMALL_FUSED": "2"},
-                      "two_kernels": {"DDSG_SMALL_FUSED": "0"}, "no_split": {"DDSG_SLOT_SPLIT": "0"},
+                      "two_kernels": {"DDSG_SMALL_FUSED": "0"}, "slot_rows": {"DDSG_SMALL_FUSED": "0", "DDSG_SMALL_TERMS": "0"},
+                      "no_split": {"DDSG_SLOT_SPLIT": "0"},
                       "slot_kernel_only": {"DDSG_SMALL_BATCH": "0"}}.items():
         out = subprocess.run([sys.executable, "-c", _CHILD, root], env={**os.environ, **env}, capture_output=True,
                              text=True, timeout=600)
