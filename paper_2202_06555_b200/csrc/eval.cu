@@ -878,17 +878,18 @@ static int64_t launch_eval(const DeviceProgram& prog, int exact, const double* d
     return pg->launch(exact, dx, n, base, dy, dbad, wb ? xt_scratch.get(wb) : nullptr, st);
   }
   // (when the slot kernel can split this batch over its subtrees, the
-  // small-batch path is taken only while its estimate -- 0.25 ns per point,
-  // slot and column chunk -- stays below the split launch's)
+  // small-batch path is taken while its estimate -- 25 us + 35 ps per point,
+  // slot and output -- stays below 0.7x the split launch's model, the
+  // calibration of profiles/r2_split_latency.jsonl; it may then serve up to
+  // 1,024 points, e.g. config 4, whose small path beats the split to ~450)
+  static const bool fixed_threshold = std::getenv("DDSG_SMALL_BATCH") != nullptr;  // explicit: no estimate
+  const double split_us = (prog.fast() && !fixed_threshold) ? prog.fast()->split_cost_us(n) : 0.0;
   const auto small_wins = [&] {
-    static const bool fixed = std::getenv("DDSG_SMALL_BATCH") != nullptr;  // explicit threshold: no estimate
-    const FastHdmr* f = prog.fast();
-    const double split_us = (f && !fixed) ? f->split_cost_us(n) : 0.0;
     if (split_us <= 0.0) return true;
-    const double small_us = 40.0 + 0.25e-3 * static_cast<double>(n) * P.n_active * ((P.m + 7) / 8);
-    return small_us <= split_us;
+    const double small_us = 25.0 + 3.5e-5 * static_cast<double>(n) * P.n_active * P.m;
+    return small_us <= 0.7 * split_us;
   };
-  if (!P.plain && P.n_active > 1 && n <= small_batch_points() &&
+  if (!P.plain && P.n_active > 1 && n <= (split_us > 0.0 ? int64_t{1024} : small_batch_points()) &&
       static_cast<size_t>(2 * P.n_active) * 8 * 8 <= size_t{200} * 1024 && small_wins()) {
     // few points: slot-parallel rows, then the pairwise tree per (point, chunk)
     constexpr int kCols = 8;

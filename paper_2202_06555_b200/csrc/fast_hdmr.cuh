@@ -135,6 +135,7 @@ class FastHdmr {
   int split_levels(int64_t n) const;
   double split_cost_us(int64_t n) const;
   static constexpr double kSubLaunchUs = 5.0, kSlotUs = 2.0;  // split cost model (measured, B200)
+
   int dim() const { return d_; }
   std::string why_not() const { return why_; }
 
