@@ -7,8 +7,10 @@ arXiv 2202.06555, BASELINE.json).
 
 A step evaluates the HDMR interpolant of the chosen BASELINE config (default:
 config 5, d=300, m=151, 519 active slots, 115,198 nodes) at n points:
-value = points x outputs per second over the whole job (strong scaling:
-n = 2^22 points split across the ranks, grids replicated).  Inputs are
+value = points x outputs per second over the whole job (weak scaling by
+default: every rank evaluates n = 2^22 points, its contiguous shard of ONE
+seeded stream of N x 2^22 points, grids replicated; `--scaling strong` splits
+2^22 points across the ranks instead).  Inputs are
 device-resident for `value`; `e2e` repeats the measurement through the same
 public API with pinned host buffers (H2D of x and D2H of y inside every step).
 One JSON line on rank 0.
@@ -41,6 +43,8 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--points", type=int, default=0, help="total points (default: the config's n)")
     ap.add_argument("--mode", choices=["exact", "fast"], default="exact")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: the config's n points per GPU (default); strong: n points split over the GPUs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
@@ -222,7 +226,7 @@ def run_ours(args, rank, world, local_rank, dist):
 
     torch.cuda.set_device(local_rank)
     cfg = W.CONFIGS[args.config]
-    n_total = args.points or cfg.n_points
+    n_total = (args.points or cfg.n_points) * (world if args.scaling == "weak" else 1)
     n_local = n_total // world + (1 if rank < n_total % world else 0)
     t0 = time.time()
     refine_info = None
@@ -406,7 +410,7 @@ def run_ours(args, rank, world, local_rank, dist):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "d": cfg.d, "m": cfg.m, "points_total": n_total,
                        "points_per_gpu": n_local, "active_slots": obj.info()["n_active"] if parts else 1,
@@ -460,7 +464,7 @@ def run_reference(args, rank, world):
                      and str(ROOT) in p})
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "d": cfg.d, "m": cfg.m, "points_per_step": n},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample},
