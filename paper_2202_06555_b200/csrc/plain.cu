@@ -207,6 +207,100 @@ __global__ void __launch_bounds__(kThreads, (kMC <= 12 && kDMax <= 10) ? 4 : 1) 
 
 
 // ---------------------------------------------------------------------------
+// Term-parallel form for small single-output grids (config 1: d = 4, 70
+// subspaces, m = 1).  plain_kernel walks a point's subspaces serially, so a
+// batch that fills less than a few waves is bound by that chain's latency
+// (65,536 points: 33 us for 9 MFLOP).  Here a CTA of kWarps warps takes 32
+// points (lane = point; 16 warps up to 8,192 points, where the kernel is one
+// latency-bound wave, 8 beyond) and warp w computes the products
+// fl(w_s * s_row) of the subspaces s = w, w + kWarps, ... from scratch (the full dim-ordered weight
+// product, same factor() and the same zero row for skipped terms) into shared
+// memory; warp 0 then adds them in canonical order, acc = fl(acc + prod_s):
+// the reference's operation sequence per point (sparse_grid.hpp:116-126), so
+// the result is bit-identical to plain_kernel's EXACT mode.  More instructions
+// per term (no prefix reuse), so it only serves batches up to kTermsMaxPoints.
+constexpr int kTermsMaxSub = 192;              // 48 KB of products per CTA
+constexpr int64_t kTermsMaxPoints = 1 << 16;   // beyond: plain_kernel's prefix reuse wins (crossover just below 2^17 on config 1)
+
+template <int kDMax, int kMode, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32) plain_terms_kernel(Params P, const double* __restrict__ x,
+                                                                       int64_t n, int64_t base,
+                                                                       double* __restrict__ y,
+                                                                       unsigned long long* bad, int n_sub) {
+  extern __shared__ double prod[];  // [n_sub][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  const bool valid = p < n;
+  const int d = P.d;
+  double xr[kDMax];
+  uint32_t xi[kDMax];
+  bool ok = valid;
+#pragma unroll
+  for (int j = 0; j < kDMax; ++j) {
+    xr[j] = 0.5;  // padding dims: level 1 at x = 1/2, factor 1 and cell 0
+    if (j < d && valid) {
+      const double xv = x[p * d + j];
+      ok &= (xv >= 0.0 && xv <= 1.0);
+      xr[j] = xv;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kDMax; ++j) {
+    if (!ok) xr[j] = 0.5;  // keeps every index in range; nothing of this point is written
+    xi[j] = min(static_cast<uint32_t>(__dmul_rn(xr[j], 2147483648.0)), 0x7fffffffu);
+  }
+  if (warp == 0 && valid && !ok) atomicMin(bad, static_cast<unsigned long long>(base + p));
+  const uint4* rec = P.rec + 2 * __ldg(P.run_off);
+#pragma unroll 2
+  for (int s = warp; s < n_sub; s += kWarps) {
+    const uint4 r0 = __ldg(rec + 2 * s);
+    const uint32_t lw[2] = {r0.z, r0.w};
+    double w = 0.0;
+    uint32_t pc = 0u;
+#pragma unroll
+    for (int j = 0; j < kDMax; ++j) {
+      const int l = static_cast<int>((lw[j / 8] >> (4 * (j % 8))) & 15u);
+      uint32_t kk;
+      double v;
+      factor<kMode>(xr[j], xi[j], l, kk, v);
+      w = j == 0 ? v : __dmul_rn(w, v);  // ((1 * v_0) * v_1) * ...
+      pc = j == 0 ? kk : ((pc << (l - 1)) | kk);
+    }
+    int row = static_cast<int>(r0.x) + static_cast<int>(pc);
+    if (!((r0.y >> 8) & 1u)) row = __ldg(P.slab + row);
+    row = (w != 0.0 && row >= 0) ? row : P.zero_row;  // sparse_grid.hpp:123
+    prod[s * 32 + lane] = __dmul_rn(w, __ldg(P.surplus + static_cast<int64_t>(row) * P.ms));
+  }
+  __syncthreads();
+  if (warp == 0 && valid && ok) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int s = 0; s < n_sub; ++s) acc = __dadd_rn(acc, prod[s * 32 + lane]);
+    y[p * P.m] = acc;
+  }
+}
+
+template <int kDMax, int kWarps>
+static void launch_terms_w(int mode, const Params& P, const double* x, int64_t n, int64_t base, double* y,
+                           unsigned long long* bad, int n_sub, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>((n + 31) / 32);
+  const size_t smem = static_cast<size_t>(n_sub) * 32 * sizeof(double);
+  if (mode == 1)
+    plain_terms_kernel<kDMax, 1, kWarps><<<grid, kWarps * 32, smem, st>>>(P, x, n, base, y, bad, n_sub);
+  else
+    plain_terms_kernel<kDMax, 0, kWarps><<<grid, kWarps * 32, smem, st>>>(P, x, n, base, y, bad, n_sub);
+}
+
+template <int kDMax>
+static void launch_terms(int mode, const Params& P, const double* x, int64_t n, int64_t base, double* y,
+                         unsigned long long* bad, int n_sub, cudaStream_t st) {
+  if (n <= 8192)
+    launch_terms_w<kDMax, 16>(mode, P, x, n, base, y, bad, n_sub, st);
+  else
+    launch_terms_w<kDMax, 8>(mode, P, x, n, base, y, bad, n_sub, st);
+}
+
+// ---------------------------------------------------------------------------
 // Sparse walk for modified-linear grids (config 3).  There the level-1 factor
 // is exactly 1 (basis.hpp:40), so the reference's dim-ordered product
 // w = ((1 * v_0) * v_1) * ... equals the product over the dims with l_j > 1
@@ -645,6 +739,34 @@ int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, d
                           unsigned long long* bad, void* ws, cudaStream_t st) const {
   int64_t launches = 1;
   const uint32_t* perm = nullptr;
+  // small single-output grids, batches of a few waves: term-parallel form
+  static const bool terms_on = [] {
+    const char* e = std::getenv("DDSG_PLAIN_TERMS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const int n_sub0 = run_off_.size() > 1 ? run_off_[1] - run_off_[0] : 0;
+  if (terms_on && exact && !sparse_ && m_ == 1 && runs_ == 1 && d_ <= 10 && n_sub0 > 0 && n_sub0 <= plain::kTermsMaxSub &&
+      n <= plain::kTermsMaxPoints && !(sort_ && n >= kSortMinPoints)) {  // Morton-sorted batches keep the serial walk
+    Params P{};
+    P.d = d_;
+    P.m = m_;
+    P.runs = runs_;
+    P.run_off = run_off_dev_;
+    P.rec = rec_;
+    P.slab = slab_;
+    P.slab_len = slab_len_;
+    P.surplus = surplus_;
+    P.ms = ms_;
+    P.zero_row = zero_row_;
+    kernel_timer().begin(st);
+    if (d_ <= 4)
+      plain::launch_terms<4>(mode_, P, x, n, base, y, bad, n_sub0, st);
+    else
+      plain::launch_terms<10>(mode_, P, x, n, base, y, bad, n_sub0, st);
+    kernel_timer().end(st);
+    DDSG_CUDA(cudaGetLastError());
+    return launches;
+  }
   if (ws && workspace_bytes(n) > 0) {
     auto* k0 = static_cast<unsigned long long*>(ws);
     auto* k1 = k0 + n;
