@@ -217,17 +217,19 @@ __global__ void __launch_bounds__(kThreads, (kMC <= 12 && kDMax <= 10) ? 4 : 1) 
 // product, same factor() and the same zero row for skipped terms) into shared
 // memory; warp 0 then adds them in canonical order, acc = fl(acc + prod_s):
 // the reference's operation sequence per point (sparse_grid.hpp:116-126), so
-// the result is bit-identical to plain_kernel's EXACT mode.  More instructions
-// per term (no prefix reuse), so it only serves batches up to kTermsMaxPoints.
-constexpr int kTermsMaxSub = 192;              // 48 KB of products per CTA
+// the result is bit-identical to plain_kernel's EXACT mode (FAST keeps w_s
+// and s_row apart and chains one DFMA per term, as plain_kernel's FAST mode
+// does).  More instructions per term (no prefix reuse), so it only serves
+// batches up to kTermsMaxPoints.
+constexpr int kTermsMaxSub = 192;              // 48 KB of products per CTA (FAST keeps weight and surplus: half as many)
 constexpr int64_t kTermsMaxPoints = 1 << 16;   // beyond: plain_kernel's prefix reuse wins (crossover just below 2^17 on config 1)
 
-template <int kDMax, int kMode, int kWarps>
+template <int kDMax, int kMode, int kWarps, int kExact>
 __global__ void __launch_bounds__(kWarps * 32) plain_terms_kernel(Params P, const double* __restrict__ x,
                                                                        int64_t n, int64_t base,
                                                                        double* __restrict__ y,
                                                                        unsigned long long* bad, int n_sub) {
-  extern __shared__ double prod[];  // [n_sub][32]
+  extern __shared__ double prod[];  // EXACT: products [n_sub][32]; FAST: weights, then surpluses [2][n_sub][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t p = static_cast<int64_t>(blockIdx.x) * 32 + lane;
   const bool valid = p < n;
@@ -269,35 +271,45 @@ __global__ void __launch_bounds__(kWarps * 32) plain_terms_kernel(Params P, cons
     int row = static_cast<int>(r0.x) + static_cast<int>(pc);
     if (!((r0.y >> 8) & 1u)) row = __ldg(P.slab + row);
     row = (w != 0.0 && row >= 0) ? row : P.zero_row;  // sparse_grid.hpp:123
-    prod[s * 32 + lane] = __dmul_rn(w, __ldg(P.surplus + static_cast<int64_t>(row) * P.ms));
+    const double sv = __ldg(P.surplus + static_cast<int64_t>(row) * P.ms);
+    if (kExact) {
+      prod[s * 32 + lane] = __dmul_rn(w, sv);
+    } else {
+      prod[s * 32 + lane] = w;
+      prod[(n_sub + s) * 32 + lane] = sv;
+    }
   }
   __syncthreads();
   if (warp == 0 && valid && ok) {
     double acc = 0.0;
 #pragma unroll 8
-    for (int s = 0; s < n_sub; ++s) acc = __dadd_rn(acc, prod[s * 32 + lane]);
+    for (int s = 0; s < n_sub; ++s)
+      acc = kExact ? __dadd_rn(acc, prod[s * 32 + lane])
+                   : __fma_rn(prod[s * 32 + lane], prod[(n_sub + s) * 32 + lane], acc);  // FAST: one DFMA per term
     y[p * P.m] = acc;
   }
 }
 
-template <int kDMax, int kWarps>
+template <int kDMax, int kWarps, int kExact>
 static void launch_terms_w(int mode, const Params& P, const double* x, int64_t n, int64_t base, double* y,
                            unsigned long long* bad, int n_sub, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>((n + 31) / 32);
-  const size_t smem = static_cast<size_t>(n_sub) * 32 * sizeof(double);
+  const size_t smem = static_cast<size_t>(n_sub) * 32 * sizeof(double) * (kExact ? 1 : 2);
   if (mode == 1)
-    plain_terms_kernel<kDMax, 1, kWarps><<<grid, kWarps * 32, smem, st>>>(P, x, n, base, y, bad, n_sub);
+    plain_terms_kernel<kDMax, 1, kWarps, kExact><<<grid, kWarps * 32, smem, st>>>(P, x, n, base, y, bad, n_sub);
   else
-    plain_terms_kernel<kDMax, 0, kWarps><<<grid, kWarps * 32, smem, st>>>(P, x, n, base, y, bad, n_sub);
+    plain_terms_kernel<kDMax, 0, kWarps, kExact><<<grid, kWarps * 32, smem, st>>>(P, x, n, base, y, bad, n_sub);
 }
 
 template <int kDMax>
-static void launch_terms(int mode, const Params& P, const double* x, int64_t n, int64_t base, double* y,
+static void launch_terms(int mode, int exact, const Params& P, const double* x, int64_t n, int64_t base, double* y,
                          unsigned long long* bad, int n_sub, cudaStream_t st) {
   if (n <= 8192)
-    launch_terms_w<kDMax, 16>(mode, P, x, n, base, y, bad, n_sub, st);
+    exact ? launch_terms_w<kDMax, 16, 1>(mode, P, x, n, base, y, bad, n_sub, st)
+          : launch_terms_w<kDMax, 16, 0>(mode, P, x, n, base, y, bad, n_sub, st);
   else
-    launch_terms_w<kDMax, 8>(mode, P, x, n, base, y, bad, n_sub, st);
+    exact ? launch_terms_w<kDMax, 8, 1>(mode, P, x, n, base, y, bad, n_sub, st)
+          : launch_terms_w<kDMax, 8, 0>(mode, P, x, n, base, y, bad, n_sub, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -745,7 +757,8 @@ int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, d
     return !(e && std::atoi(e) == 0);
   }();
   const int n_sub0 = run_off_.size() > 1 ? run_off_[1] - run_off_[0] : 0;
-  if (terms_on && exact && !sparse_ && m_ == 1 && runs_ == 1 && d_ <= 10 && n_sub0 > 0 && n_sub0 <= plain::kTermsMaxSub &&
+  if (terms_on && !sparse_ && m_ == 1 && runs_ == 1 && d_ <= 10 && n_sub0 > 0 &&
+      n_sub0 <= plain::kTermsMaxSub / (exact ? 1 : 2) &&
       n <= plain::kTermsMaxPoints && !(sort_ && n >= kSortMinPoints)) {  // Morton-sorted batches keep the serial walk
     Params P{};
     P.d = d_;
@@ -760,9 +773,9 @@ int64_t PlainGrid::launch(int exact, const double* x, int64_t n, int64_t base, d
     P.zero_row = zero_row_;
     kernel_timer().begin(st);
     if (d_ <= 4)
-      plain::launch_terms<4>(mode_, P, x, n, base, y, bad, n_sub0, st);
+      plain::launch_terms<4>(mode_, exact, P, x, n, base, y, bad, n_sub0, st);
     else
-      plain::launch_terms<10>(mode_, P, x, n, base, y, bad, n_sub0, st);
+      plain::launch_terms<10>(mode_, exact, P, x, n, base, y, bad, n_sub0, st);
     kernel_timer().end(st);
     DDSG_CUDA(cudaGetLastError());
     return launches;

@@ -81,26 +81,28 @@ import sys, json, hashlib
 sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
 import numpy as np
 from test_gpu_plain_terms import _grid, _points
-from paper_2202_06555_b200.ddsg import last_eval_stats
+from paper_2202_06555_b200.ddsg import EXACT, FAST
 out = {}
 for mode in (0, 1):
     for d, level, eps in ((2, 8, 1e-4), (4, 5, 0.0), (4, 6, 1e-3)):
         g = _grid(mode, d, level, eps)
         for n in (257, 2049, 40000):
-            y = g.interpolate(_points(d, n, 3 * n + d))
-            out[f"{mode}-{d}-{level}-{n}"] = hashlib.sha256(np.ascontiguousarray(y).tobytes()).hexdigest()
+            for em in (EXACT, FAST):
+                g.set_eval_mode(em)
+                y = g.interpolate(_points(d, n, 3 * n + d))
+                out[f"{mode}-{d}-{level}-{n}-{em}"] = hashlib.sha256(np.ascontiguousarray(y).tobytes()).hexdigest()
 print(json.dumps(out))
 """
 
 
 def test_term_parallel_equals_serial_walk():
     """The same grids and points in two child processes: term-parallel form
-    (default) and serial walk (DDSG_PLAIN_TERMS=0); d <= 4, so 40,000 points
-    stay unsorted and take the term-parallel kernel too."""
+    (default) and serial walk (DDSG_PLAIN_TERMS=0), EXACT and FAST; d <= 4, so
+    40,000 points stay unsorted and take the term-parallel kernel too."""
     res = []
     for v in ("1", "0"):
         r = subprocess.run([sys.executable, "-c", _CHILD, str(ROOT)], env={**os.environ, "DDSG_PLAIN_TERMS": v},
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(json.loads(r.stdout.strip().splitlines()[-1]))
-    assert res[0] == res[1] and len(res[0]) == 18
+    assert res[0] == res[1] and len(res[0]) == 36
